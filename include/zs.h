@@ -1,0 +1,144 @@
+/*
+ * zs.h -- C ABI of the B200-native ZSMILES per-line codec (libzs.so).
+ *
+ * Plain pointers and sizes only; no torch / CUDA types cross this boundary.
+ * Every entry point returns an int status (ZS_OK or a negative ZS_E_*) and
+ * never throws.  Per-line data errors (decode failures, preprocess errors,
+ * carriage returns) are *results*, reported in zs_result, not call failures.
+ *
+ * Two surfaces, both replacing the reference's Python->numba plugin seam
+ * (pkg/src/zsmiles/kernels/__init__.py:28-33, called from codec.py:38-39,
+ * 64-70):
+ *
+ *  1. Fine-grained parity shim with the exact semantics/layouts of the
+ *     reference kernels (host pointers; the library stages them through HBM):
+ *       zs_compress_batch    <- kernels.compress_batch   numba_impl.py:16-71
+ *       zs_decompress_sizes  <- kernels.decompress_sizes numba_impl.py:74-112
+ *       zs_decompress_fill   <- kernels.decompress_fill  numba_impl.py:115-139
+ *       zs_preprocess_batch  <- smiles.preprocess_line   smiles.py:183-213
+ *
+ *  2. Coarse whole-buffer API (the hot path): one newline-framed buffer in,
+ *     one newline-framed buffer out, with the stream semantics of
+ *     pipeline.run_stream (pipeline.py:97-167): framing, CR policy,
+ *     strict/lenient, stats, first error with its 1-based line number.
+ *       zs_compress_device / zs_decompress_device   (buffers already in HBM)
+ *       zs_compress_host   / zs_decompress_host     (host buffers; chunked,
+ *                                                    H2D/D2H overlapped)
+ *
+ * Dictionary tables are passed in the reference's own layouts
+ * (Dictionary.encode_trie -> trie.py:22-50; Dictionary.decode_tables ->
+ * dictionary.py:112-129); the library derives its device tables from them.
+ */
+#ifndef ZS_H
+#define ZS_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    ZS_OK = 0,
+    ZS_E_ARG = -1,      /* bad argument */
+    ZS_E_CUDA = -2,     /* CUDA runtime error (see zs_last_error) */
+    ZS_E_NOMEM = -3,    /* device or host allocation failed */
+    ZS_E_NODICT = -4,   /* no dictionary uploaded */
+    ZS_E_CAPACITY = -5  /* caller's output buffer too small (result.out_bytes = needed) */
+};
+
+/* per-line error kinds (pipeline.py:106-107, smiles.py:99-176, errors.py:64-78) */
+enum {
+    ZS_ERR_NONE = 0,
+    ZS_ERR_CR = 1,                 /* "carriage return in line" */
+    ZS_ERR_UNBALANCED_BRACKET = 2, /* "unclosed '[' at offset {offset}" */
+    ZS_ERR_MALFORMED_PERCENT = 3,  /* "'%' without two digits at offset {offset}" */
+    ZS_ERR_UNPAIRED_RING = 4,      /* "ring id(s) {ids} never close" */
+    ZS_ERR_RING_OVERFLOW = 5,      /* "more than 100 mutually overlapping rings" */
+    ZS_ERR_UNKNOWN_CODE = 6,       /* "unknown code 0x{code:02x} at offset {offset} ..." */
+    ZS_ERR_TRUNCATED_ESCAPE = 7    /* "payload ends with a dangling escape at offset {offset}" */
+};
+
+/* flags for the whole-buffer calls */
+enum { ZS_F_PREPROCESS = 1, ZS_F_LENIENT = 2 };
+
+typedef struct zs_ctx zs_ctx;
+
+/* CorpusStats (pipeline.py:21-40) + first strict error */
+typedef struct {
+    int64_t lines;      /* records written */
+    int64_t in_bytes;
+    int64_t out_bytes;
+    int64_t escapes;
+    int64_t skipped;
+    int64_t flagged;
+    int64_t err_line;   /* 1-based line of the first strict-mode error, 0 = none */
+    int32_t err_kind;   /* ZS_ERR_* */
+    int32_t err_code;   /* offending byte for ZS_ERR_UNKNOWN_CODE */
+    int64_t err_offset; /* in-line byte offset (bracket, percent, decode errors) */
+    uint64_t err_ids[2];/* bitmap of unpaired ring ids 0..99 (ZS_ERR_UNPAIRED_RING) */
+    int32_t gpu_launches; /* kernels launched by this call */
+    int32_t pad;
+} zs_result;
+
+/* ---- context / dictionary ---- */
+int zs_ctx_create(int device, zs_ctx **out);
+int zs_ctx_destroy(zs_ctx *ctx);
+const char *zs_last_error(zs_ctx *ctx);
+int zs_device_count(int *n);
+
+/* children: int32 [n_nodes][256] (-1 = no edge, row 0 = root)
+ * term_code: int16 [n_nodes] (-1 = not terminal)
+ * exp_len: int32[256], valid: uint8[256], exp_off: int64[257], exp_flat: uint8[exp_off[256]] */
+int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_code,
+                      int32_t n_nodes, const int32_t *exp_len, const uint8_t *valid,
+                      const int64_t *exp_off, const uint8_t *exp_flat);
+/* DFA window width (2/4/6/8) if the sm_100a fast path (shared-memory DFA)
+ * serves the uploaded dictionary, 0 for the generic trie walk */
+int zs_dictionary_fast(zs_ctx *ctx);
+/* Host-only inspection (no GPU needed): derive the fast-path tables from a
+ * reference trie.  dfa: uint16[256*97], codes: uint8[256*8].  Returns 1 if
+ * the fast path applies, 0 if not, <0 on bad arguments. */
+int zs_build_tables_host(const int32_t *children, const int16_t *term_code, int32_t n_nodes,
+                         uint16_t *dfa, uint8_t *codes, int32_t *n_states, int32_t *max_len);
+
+/* ---- fine-grained parity shim (reference kernel layouts, host memory) ---- */
+/* out must hold 2*starts[n_lines] bytes; record i lands at out[2*starts[i]] */
+int zs_compress_batch(zs_ctx *ctx, const uint8_t *flat, const int64_t *starts, int64_t n_lines,
+                      uint8_t *out, int64_t *out_lens, int64_t *escapes);
+int zs_decompress_sizes(zs_ctx *ctx, const uint8_t *flat, const int64_t *starts,
+                        int64_t n_lines, int64_t *out_lens, int8_t *status, int64_t *errpos,
+                        int64_t *total, int64_t *escapes);
+int zs_decompress_fill(zs_ctx *ctx, const uint8_t *flat, const int64_t *starts, int64_t n_lines,
+                       const int8_t *status, uint8_t *out, const int64_t *out_starts);
+/* out must hold 3*starts[n_lines] + 3*n_lines bytes; line i lands at
+ * out[3*starts[i] + 3*i] with length out_lens[i]; status[i] = ZS_ERR_* with
+ * err_off[i] / err_ids[2*i..2*i+1] filled on error (strict semantics). */
+int zs_preprocess_batch(zs_ctx *ctx, const uint8_t *flat, const int64_t *starts,
+                        int64_t n_lines, uint8_t *out, int64_t *out_lens, int8_t *status,
+                        int64_t *err_off, uint64_t *err_ids);
+
+/* ---- whole-buffer stream API (hot path) ---- */
+/* device pointers; d_out must hold out_cap bytes.  Runs on the context's
+ * stream and synchronises before returning. */
+int zs_compress_device(zs_ctx *ctx, const uint8_t *d_in, int64_t n, uint8_t *d_out,
+                       int64_t out_cap, int flags, zs_result *res);
+int zs_decompress_device(zs_ctx *ctx, const uint8_t *d_in, int64_t n, uint8_t *d_out,
+                         int64_t out_cap, int flags, zs_result *res);
+/* host pointers (pinned memory gives full PCIe rate) */
+int zs_compress_host(zs_ctx *ctx, const uint8_t *h_in, int64_t n, uint8_t *h_out,
+                     int64_t out_cap, int flags, zs_result *res);
+int zs_decompress_host(zs_ctx *ctx, const uint8_t *h_in, int64_t n, uint8_t *h_out,
+                       int64_t out_cap, int flags, zs_result *res);
+
+/* upper bound of the output size for an n-byte input (for buffer sizing) */
+int64_t zs_compress_bound(int64_t n);
+int64_t zs_decompress_bound(zs_ctx *ctx, int64_t n);
+
+/* timing of the last whole-buffer call's main kernel (CUDA events on the
+ * launching stream), milliseconds */
+float zs_last_kernel_ms(zs_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,170 @@
+"""ctypes binding of libzs.so (include/zs.h) and per-device contexts.
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``python -m paper_2404_19391_b200.build``).  There is no CPU fallback: if
+the library is missing, or no CUDA device is present when a compute call is
+made, this module raises.
+"""
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libzs.so")
+
+ZS_OK, ZS_E_ARG, ZS_E_CUDA, ZS_E_NOMEM, ZS_E_NODICT, ZS_E_CAPACITY = 0, -1, -2, -3, -4, -5
+F_PREPROCESS, F_LENIENT = 1, 2
+
+# every symbol include/zs.h declares
+EXPORTS = (
+    "zs_ctx_create", "zs_ctx_destroy", "zs_last_error", "zs_device_count", "zs_set_dictionary",
+    "zs_dictionary_fast", "zs_compress_batch", "zs_decompress_sizes", "zs_decompress_fill",
+    "zs_preprocess_batch", "zs_compress_device", "zs_decompress_device", "zs_compress_host",
+    "zs_decompress_host", "zs_compress_bound", "zs_decompress_bound", "zs_last_kernel_ms",
+    "zs_build_tables_host",
+)
+
+
+class Result(ctypes.Structure):
+    """zs_result (include/zs.h)"""
+    _fields_ = [("lines", ctypes.c_int64), ("in_bytes", ctypes.c_int64),
+                ("out_bytes", ctypes.c_int64), ("escapes", ctypes.c_int64),
+                ("skipped", ctypes.c_int64), ("flagged", ctypes.c_int64),
+                ("err_line", ctypes.c_int64), ("err_kind", ctypes.c_int32),
+                ("err_code", ctypes.c_int32), ("err_offset", ctypes.c_int64),
+                ("err_ids", ctypes.c_uint64 * 2), ("gpu_launches", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
+
+
+class ZsCudaError(RuntimeError):
+    pass
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load():
+    """Load libzs.so (raises if it was not built)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with "
+                              "`python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(LIB_PATH)
+        P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        sig = {
+            "zs_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+            "zs_ctx_destroy": (ctypes.c_int, [P]),
+            "zs_last_error": (ctypes.c_char_p, [P]),
+            "zs_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+            "zs_set_dictionary": (ctypes.c_int, [P, P, P, I32, P, P, P, P]),
+            "zs_dictionary_fast": (ctypes.c_int, [P]),
+            "zs_compress_batch": (ctypes.c_int, [P, P, P, I64, P, P, P]),
+            "zs_decompress_sizes": (ctypes.c_int, [P, P, P, I64, P, P, P, P, P]),
+            "zs_decompress_fill": (ctypes.c_int, [P, P, P, I64, P, P, P]),
+            "zs_preprocess_batch": (ctypes.c_int, [P, P, P, I64, P, P, P, P, P]),
+            "zs_compress_device": (ctypes.c_int, [P, P, I64, P, I64, ctypes.c_int, ctypes.POINTER(Result)]),
+            "zs_decompress_device": (ctypes.c_int, [P, P, I64, P, I64, ctypes.c_int, ctypes.POINTER(Result)]),
+            "zs_compress_host": (ctypes.c_int, [P, P, I64, P, I64, ctypes.c_int, ctypes.POINTER(Result)]),
+            "zs_decompress_host": (ctypes.c_int, [P, P, I64, P, I64, ctypes.c_int, ctypes.POINTER(Result)]),
+            "zs_compress_bound": (I64, [I64]),
+            "zs_decompress_bound": (I64, [P, I64]),
+            "zs_last_kernel_ms": (ctypes.c_float, [P]),
+            "zs_build_tables_host": (ctypes.c_int, [P, P, I32, P, P, P, P]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+        return lib
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    load().zs_device_count(ctypes.byref(n))
+    return n.value
+
+
+def ptr(a: np.ndarray):
+    return a.ctypes.data if a.size else None
+
+
+class Context:
+    """One libzs context (stream pair + device buffers) on one GPU.  Calls are
+    serialised by a lock; the currently uploaded dictionary is cached."""
+
+    def __init__(self, device: int = 0):
+        lib = load()
+        if device_count() <= device:
+            raise ZsCudaError("no CUDA device available: the ZSMILES codec runs on sm_100a "
+                              "GPUs only (there is no CPU fallback)")
+        h = ctypes.c_void_p()
+        rc = lib.zs_ctx_create(device, ctypes.byref(h))
+        if rc != ZS_OK:
+            raise ZsCudaError(f"zs_ctx_create({device}) failed: {rc}")
+        self.lib = lib
+        self.h = h
+        self.device = device
+        self.lock = threading.RLock()
+        self._dict_key = None
+        self._keep = None
+
+    def check(self, rc, what):
+        if rc == ZS_OK:
+            return
+        msg = self.lib.zs_last_error(self.h)
+        raise ZsCudaError(f"{what} failed ({rc}): {msg.decode() if msg else ''}")
+
+    def set_dictionary(self, d):
+        """Upload a Dictionary's tables (reference layouts) if not current."""
+        key = d.cache_key()
+        if key == self._dict_key:
+            return
+        trie = d.encode_trie
+        exp_len, valid, exp_off, exp_flat = d.decode_tables
+        children = np.ascontiguousarray(trie.children, np.int32)
+        term = np.ascontiguousarray(trie.term_code, np.int16)
+        exp_len = np.ascontiguousarray(exp_len, np.int32)
+        valid = np.ascontiguousarray(valid, np.uint8)
+        exp_off = np.ascontiguousarray(exp_off, np.int64)
+        flat = np.ascontiguousarray(exp_flat, np.uint8)
+        if flat.size == 0:
+            flat = np.zeros(1, np.uint8)
+        rc = self.lib.zs_set_dictionary(self.h, ptr(children), ptr(term), children.shape[0],
+                                        ptr(exp_len), ptr(valid), ptr(exp_off), ptr(flat))
+        self.check(rc, "zs_set_dictionary")
+        self._dict_key = key
+
+    def fast_width(self) -> int:
+        return self.lib.zs_dictionary_fast(self.h)
+
+    def last_kernel_ms(self) -> float:
+        return self.lib.zs_last_kernel_ms(self.h)
+
+    def close(self):
+        if self.h:
+            self.lib.zs_ctx_destroy(self.h)
+            self.h = None
+
+
+_ctx = {}
+_ctx_lock = threading.Lock()
+
+
+def context(device: int | None = None) -> Context:
+    """Process-wide context for `device` (default: the current torch device
+    if torch is imported and CUDA-enabled, else 0)."""
+    if device is None:
+        device = int(os.environ.get("ZS_DEVICE", "0"))
+    with _ctx_lock:
+        c = _ctx.get(device)
+        if c is None:
+            c = _ctx[device] = Context(device)
+        return c

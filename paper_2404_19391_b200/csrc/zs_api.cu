@@ -1,0 +1,774 @@
+// zs_api.cu -- C ABI (include/zs.h) over the sm_100a kernels.
+//
+// Host side: dictionary tables in the reference layouts -> device tables
+// (dense trie for the generic walk, reversed-pattern Aho-Corasick DFA for the
+// fast path, compact decode tables); per-context stream, events and grow-only
+// device buffers; the whole-buffer calls (one persistent-kernel launch per
+// buffer or chunk) and the parity-shim calls.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/zs.h"
+#include "zs_kernels.cuh"
+
+using namespace zs;
+
+namespace {
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t c = std::max<size_t>(n, 256);
+        cudaError_t e = cudaMalloc(&p, c);
+        if (e == cudaSuccess) cap = c;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+struct HostTables {
+    int n_nodes = 0, max_len = 0;
+    std::vector<int32_t> children;
+    std::vector<int16_t> term_code;
+    bool fast = false;
+    int n_states = 0;
+    std::vector<uint16_t> dfa;
+    std::vector<uint8_t> codes;
+    uint8_t exp_len[256];
+    uint16_t exp_off[257];
+    std::vector<uint8_t> exp_flat;
+};
+
+}  // namespace
+
+struct zs_ctx {
+    int dev = 0;
+    int n_sm = 0;
+    cudaStream_t stream[2] = {nullptr, nullptr};
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_ctl[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+    std::string err;
+    bool have_dict = false;
+    HostTables ht;
+    Tables tb{};
+    int fast_w = 0;
+    DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat;
+    // per-slot (double-buffered) work buffers
+    DevBuf ctl[2], ts[2], terr[2], in[2], out[2], arena[2];  // arena: per slot
+    // shim scratch
+    DevBuf s_flat, s_starts, s_out, s_lens, s_dec, s_stat, s_errpos, s_tot, s_ids, s_outst;
+    Ctl *h_ctl = nullptr;  // pinned, 2 slots
+    float last_ms = 0.f;
+};
+
+namespace {
+
+int fail(zs_ctx *ctx, cudaError_t e, const char *what) {
+    if (ctx) ctx->err = std::string(what) + ": " + cudaGetErrorString(e);
+    return ZS_E_CUDA;
+}
+
+#define CK(call)                                         \
+    do {                                                 \
+        cudaError_t e_ = (call);                         \
+        if (e_ != cudaSuccess) return fail(ctx, e_, #call); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// dictionary -> device tables
+// ---------------------------------------------------------------------------
+
+// Walk the reference trie (trie.py:22-50 layout) to recover (pattern, code).
+void trie_patterns(const int32_t *children, const int16_t *term_code, int n_nodes,
+                   std::vector<std::pair<std::string, int>> &out) {
+    std::vector<std::pair<int, std::string>> stack{{0, std::string()}};
+    while (!stack.empty()) {
+        auto [node, s] = stack.back();
+        stack.pop_back();
+        if (node < 0 || node >= n_nodes) continue;
+        if (term_code[node] >= 0) out.emplace_back(s, term_code[node]);
+        for (int b = 255; b >= 0; --b) {
+            int c = children[(size_t)node * 256 + b];
+            if (c >= 0) stack.emplace_back(c, s + (char)b);
+        }
+    }
+}
+
+// Reversed-pattern Aho-Corasick DFA.  Reading a line right to left, the state
+// after consuming byte i has as outputs exactly the patterns that START at i
+// (a reversed pattern is a suffix of the reversed text read so far).
+bool build_dfa(const std::vector<std::pair<std::string, int>> &pats, int max_len, HostTables &ht) {
+    if (max_len > FAST_W) return false;
+    for (auto &pc : pats)
+        for (unsigned char c : pc.first)
+            if (c < 0x21 || c > 0x7e) return false;
+    std::vector<std::array<int, 256>> go(1);
+    go[0].fill(-1);
+    std::vector<uint32_t> own(1, 0);
+    std::vector<std::array<int, FAST_W>> own_code(1);
+    own_code[0].fill(-1);
+    for (auto &pc : pats) {
+        int node = 0;
+        for (auto it = pc.first.rbegin(); it != pc.first.rend(); ++it) {
+            unsigned char c = (unsigned char)*it;
+            if (go[node][c] < 0) {
+                go[node][c] = (int)go.size();
+                go.emplace_back();
+                go.back().fill(-1);
+                own.push_back(0);
+                own_code.emplace_back();
+                own_code.back().fill(-1);
+            }
+            node = go[node][c];
+        }
+        int L = (int)pc.first.size();
+        own[node] |= 1u << (L - 1);
+        own_code[node][L - 1] = pc.second;
+    }
+    const int ns = (int)go.size();
+    if (ns > FAST_STATES) return false;
+    std::vector<int> failv(ns, 0), order;
+    std::vector<uint32_t> outm(own);
+    std::vector<std::array<int, FAST_W>> code(own_code);
+    order.push_back(0);
+    for (size_t qi = 0; qi < order.size(); ++qi) {
+        int s = order[qi];
+        for (int c = 0; c < 256; ++c) {
+            int ch = go[s][c];
+            if (ch >= 0) {
+                failv[ch] = s == 0 ? 0 : go[failv[s]][c];
+                outm[ch] = own[ch] | outm[failv[ch]];
+                for (int L = 0; L < FAST_W; ++L)
+                    code[ch][L] = own_code[ch][L] >= 0 ? own_code[ch][L] : code[failv[ch]][L];
+                order.push_back(ch);
+            } else {
+                go[s][c] = s == 0 ? 0 : go[failv[s]][c];
+            }
+        }
+    }
+    ht.n_states = ns;
+    ht.dfa.assign((size_t)align16(ns * NCOL * 2) / 2, 0);
+    ht.codes.assign((size_t)align16(ns * FAST_W), 0);
+    for (int s = 0; s < ns; ++s) {
+        for (int col = 0; col < NCOL; ++col) {
+            int b = col < 96 ? 0x20 + col : 0x00;  // col 96: every byte outside 0x20..0x7f
+            int nx = go[s][b];
+            ht.dfa[(size_t)s * NCOL + col] = (uint16_t)(nx | (outm[nx] << 8));
+        }
+        for (int L = 0; L < FAST_W; ++L)
+            ht.codes[(size_t)s * FAST_W + L] = (uint8_t)(code[s][L] < 0 ? 0 : code[s][L]);
+    }
+    return true;
+}
+
+template <typename K>
+cudaError_t set_smem(K kernel, int bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+typedef void (*TileKernel)(Job, Tables);
+
+TileKernel compress_kernel(int w) {
+    switch (w) {
+    case 2: return compress_tiles<2>;
+    case 4: return compress_tiles<4>;
+    case 6: return compress_tiles<6>;
+    case 8: return compress_tiles<8>;
+    default: return compress_tiles<0>;
+    }
+}
+
+typedef void (*BatchKernel)(const uint8_t *, const long long *, long long, uint8_t *, long long *,
+                            uint8_t *, unsigned long long *, Tables);
+BatchKernel batch_kernel(int w) {
+    switch (w) {
+    case 2: return batch_compress<2>;
+    case 4: return batch_compress<4>;
+    case 6: return batch_compress<6>;
+    case 8: return batch_compress<8>;
+    default: return batch_compress<0>;
+    }
+}
+
+// one whole-buffer launch (device pointers) on `slot`'s buffers and stream
+int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, long long n,
+                  uint8_t *d_out, long long out_cap, int flags, bool timed) {
+    const long long nt = (n + TILE - 1) / TILE;
+    cudaStream_t st = ctx->stream[slot];
+    if (ctx->ctl[slot].reserve(sizeof(Ctl)) || ctx->ts[slot].reserve(sizeof(TileState) * (nt + 1)) ||
+        ctx->terr[slot].reserve(sizeof(TileErr) * (nt + 1)))
+        return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(tile state)");
+    if (!ctx->arena[slot].p && ctx->arena[slot].reserve(64ull << 20))
+        return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(arena)");
+    CK(cudaMemsetAsync(ctx->ctl[slot].p, 0, sizeof(Ctl), st));
+    // err_key starts at ~0
+    CK(cudaMemsetAsync((char *)ctx->ctl[slot].p + offsetof(Ctl, err_key), 0xff, 8, st));
+    CK(cudaMemsetAsync(ctx->ts[slot].p, 0, sizeof(TileState) * (nt + 1), st));
+    Job job;
+    job.in = d_in;
+    job.n = n;
+    job.out = d_out;
+    job.out_cap = out_cap;
+    job.preprocess = (flags & ZS_F_PREPROCESS) ? 1 : 0;
+    job.lenient = (flags & ZS_F_LENIENT) ? 1 : 0;
+    job.n_tiles = nt;
+    job.ctl = ctx->ctl[slot].as<Ctl>();
+    job.ts = ctx->ts[slot].as<TileState>();
+    job.terr = ctx->terr[slot].as<TileErr>();
+    job.arena = ctx->arena[slot].as<uint8_t>();
+    job.arena_cap = (long long)ctx->arena[slot].cap;
+    if (nt > 0) {
+        const int grid = (int)std::min<long long>(nt, ctx->n_sm);
+        if (timed) CK(cudaEventRecord(ctx->ev0, st));
+        if (compress) {
+            TileKernel k = compress_kernel(ctx->fast_w);
+            const int smem = compress_smem_bytes(ctx->fast_w ? ctx->tb.n_states : 0);
+            CK(set_smem(k, smem));
+            k<<<grid, NT, smem, st>>>(job, ctx->tb);
+        } else {
+            const int smem = decompress_smem_bytes(ctx->tb.n_flat);
+            CK(set_smem(decompress_tiles, smem));
+            decompress_tiles<<<grid, NT, smem, st>>>(job, ctx->tb);
+        }
+        CK(cudaGetLastError());
+        if (timed) CK(cudaEventRecord(ctx->ev1, st));
+    }
+    CK(cudaMemcpyAsync(&ctx->h_ctl[slot], ctx->ctl[slot].p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(ctx->ev_ctl[slot], st));
+    return ZS_OK;
+}
+
+// Fill res from a finished slot; returns ZS_OK, or 1 = re-run needed
+// (arena exhausted), 2 = output capacity exceeded.
+int collect(zs_ctx *ctx, int slot, long long n, const uint8_t *h_last_byte_src, bool trailing,
+            long long line_base, zs_result *res, bool accumulate) {
+    const Ctl &c = ctx->h_ctl[slot];
+    if (c.overflow & 2ull) {
+        size_t need = (size_t)c.arena_used * 2 + (64ull << 20);
+        ctx->arena[slot].release();
+        if (ctx->arena[slot].reserve(need)) return fail(ctx, cudaErrorMemoryAllocation, "arena");
+        return 1;
+    }
+    (void)h_last_byte_src;
+    zs_result r{};
+    r.lines = (long long)c.lines;
+    r.in_bytes = n;
+    r.out_bytes = (long long)c.total_out;
+    if (!trailing && r.lines > 0) r.out_bytes -= 1;
+    r.escapes = (long long)c.escapes;
+    r.skipped = (long long)c.skipped;
+    r.flagged = (long long)c.flagged;
+    if (c.err_key != ~0ull) {
+        const long long line_idx = (long long)(c.err_key >> 24);
+        const long long tile = (long long)(c.err_key & 0xffffff);
+        TileErr e;
+        cudaError_t ce = cudaMemcpy(&e, ctx->terr[slot].as<TileErr>() + tile, sizeof e,
+                                    cudaMemcpyDeviceToHost);
+        if (ce != cudaSuccess) return fail(ctx, ce, "cudaMemcpy(terr)");
+        r.err_line = line_base + line_idx + 1;
+        r.err_kind = e.kind;
+        r.err_code = e.code;
+        r.err_offset = e.offset;
+        r.err_ids[0] = e.ids[0];
+        r.err_ids[1] = e.ids[1];
+    }
+    if (accumulate) {
+        res->lines += r.lines;
+        res->in_bytes += r.in_bytes;
+        res->out_bytes += r.out_bytes;
+        res->escapes += r.escapes;
+        res->skipped += r.skipped;
+        res->flagged += r.flagged;
+        if (!res->err_line && r.err_line) {
+            res->err_line = r.err_line;
+            res->err_kind = r.err_kind;
+            res->err_code = r.err_code;
+            res->err_offset = r.err_offset;
+            res->err_ids[0] = r.err_ids[0];
+            res->err_ids[1] = r.err_ids[1];
+        }
+        res->gpu_launches += 1;
+    } else {
+        r.gpu_launches = 1;
+        *res = r;
+    }
+    return (c.overflow & 1ull) ? 2 : ZS_OK;
+}
+
+int run_device(zs_ctx *ctx, bool compress, const uint8_t *d_in, int64_t n, uint8_t *d_out,
+               int64_t out_cap, int flags, zs_result *res) {
+    if (!ctx || !res || n < 0 || (n > 0 && !d_in)) return ZS_E_ARG;
+    if (!ctx->have_dict) return ZS_E_NODICT;
+    CK(cudaSetDevice(ctx->dev));
+    memset(res, 0, sizeof *res);
+    bool trailing = true;
+    if (n > 0) {
+        uint8_t last;
+        CK(cudaMemcpyAsync(&last, d_in + n - 1, 1, cudaMemcpyDeviceToHost, ctx->stream[0]));
+        CK(cudaStreamSynchronize(ctx->stream[0]));
+        trailing = last == '\n';
+    }
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        int rc = launch_stream(ctx, 0, compress, d_in, n, d_out, out_cap, flags, true);
+        if (rc) return rc;
+        CK(cudaEventSynchronize(ctx->ev_ctl[0]));
+        if (n > 0) CK(cudaEventElapsedTime(&ctx->last_ms, ctx->ev0, ctx->ev1));
+        rc = collect(ctx, 0, n, nullptr, trailing, 0, res, false);
+        if (rc == 1) continue;  // arena grown, re-run
+        if (rc == 2) {
+            res->out_bytes = (long long)ctx->h_ctl[0].total_out;
+            return ZS_E_CAPACITY;
+        }
+        return rc;
+    }
+    ctx->err = "arena re-run limit";
+    return ZS_E_NOMEM;
+}
+
+// Host-buffer pipeline: newline-aligned chunks, two slots on two streams so
+// chunk k+1's H2D and kernel overlap chunk k's D2H.
+int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t *h_out,
+             int64_t out_cap, int flags, zs_result *res) {
+    if (!ctx || !res || n < 0 || (n > 0 && !h_in)) return ZS_E_ARG;
+    if (!ctx->have_dict) return ZS_E_NODICT;
+    CK(cudaSetDevice(ctx->dev));
+    memset(res, 0, sizeof *res);
+    const bool trailing = n == 0 || h_in[n - 1] == '\n';
+    const long long CH = 256ll << 20;
+    // chunk boundaries just past a newline
+    std::vector<long long> cuts{0};
+    while (cuts.back() < n) {
+        long long s = cuts.back(), e = std::min<long long>(n, s + CH);
+        if (e < n) {
+            const void *nl = memchr(h_in + e, '\n', (size_t)(n - e));
+            e = nl ? (long long)((const uint8_t *)nl - h_in) + 1 : n;
+        }
+        cuts.push_back(e);
+    }
+    const int nch = (int)cuts.size() - 1;
+    long long written = 0, line_base = 0;
+    bool capacity_hit = false;
+    int pending = -1;  // slot whose output is waiting for D2H
+    long long pend_len = 0, pend_n = 0;
+    auto out_bound = [&](long long m) {
+        return compress ? 2 * m + 64 : std::max<long long>(4 * m, 1 << 20);
+    };
+    auto finish = [&](int slot, long long cn, long long clen) -> int {
+        // wait for ctl, then D2H this chunk's output
+        CK(cudaEventSynchronize(ctx->ev_ctl[slot]));
+        zs_result r{};
+        int rc = collect(ctx, slot, cn, nullptr, true, line_base, &r, false);
+        if (rc < 0) return rc;
+        (void)clen;
+        if (rc == 1 || rc == 2) return 10 + rc;  // caller re-runs this chunk synchronously
+        long long ob = (long long)ctx->h_ctl[slot].total_out;
+        if (!capacity_hit && written + ob <= out_cap && ob > 0 && !r.err_line)
+            CK(cudaMemcpyAsync(h_out + written, ctx->out[slot].p, ob, cudaMemcpyDeviceToHost,
+                               ctx->stream[slot]));
+        if (written + ob > out_cap) capacity_hit = true;
+        CK(cudaEventRecord(ctx->ev_out[slot], ctx->stream[slot]));
+        written += ob;
+        res->lines += r.lines;
+        res->escapes += r.escapes;
+        res->skipped += r.skipped;
+        res->flagged += r.flagged;
+        res->gpu_launches += 1;
+        if (!res->err_line && r.err_line) {
+            res->err_line = r.err_line;
+            res->err_kind = r.err_kind;
+            res->err_code = r.err_code;
+            res->err_offset = r.err_offset;
+            res->err_ids[0] = r.err_ids[0];
+            res->err_ids[1] = r.err_ids[1];
+        }
+        line_base += (long long)ctx->h_ctl[slot].in_lines;
+        return ZS_OK;
+    };
+    for (int k = 0; k < nch && !res->err_line; ++k) {
+        const int slot = k & 1;
+        const long long cs = cuts[k], cn = cuts[k + 1] - cs;
+        // slot reuse: its previous output copy must be done
+        CK(cudaEventSynchronize(ctx->ev_out[slot]));
+        if (ctx->in[slot].reserve(cn + 16) || ctx->out[slot].reserve(out_bound(cn)))
+            return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(chunk)");
+        CK(cudaMemcpyAsync(ctx->in[slot].p, h_in + cs, cn, cudaMemcpyHostToDevice, ctx->stream[slot]));
+        int rc = launch_stream(ctx, slot, compress, ctx->in[slot].as<uint8_t>(), cn,
+                               ctx->out[slot].as<uint8_t>(), (long long)ctx->out[slot].cap, flags,
+                               false);
+        if (rc) return rc;
+        if (pending >= 0) {
+            rc = finish(pending, pend_n, pend_len);
+            while (rc >= 10) {  // re-run the previous chunk synchronously with bigger buffers
+                const int ps = pending;
+                CK(cudaStreamSynchronize(ctx->stream[ps]));
+                if (rc == 12 && ctx->out[ps].reserve((size_t)ctx->h_ctl[ps].total_out + 64))
+                    return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(out)");
+                CK(cudaMemcpyAsync(ctx->in[ps].p, h_in + cuts[k - 1], pend_n, cudaMemcpyHostToDevice,
+                                   ctx->stream[ps]));
+                rc = launch_stream(ctx, ps, compress, ctx->in[ps].as<uint8_t>(), pend_n,
+                                   ctx->out[ps].as<uint8_t>(), (long long)ctx->out[ps].cap, flags, false);
+                if (rc) return rc;
+                rc = finish(ps, pend_n, pend_len);
+            }
+            if (rc) return rc;
+        }
+        pending = slot;
+        pend_n = cn;
+    }
+    if (pending >= 0 && !res->err_line) {
+        int rc = finish(pending, pend_n, pend_len);
+        while (rc >= 10) {
+            const int ps = pending;
+            CK(cudaStreamSynchronize(ctx->stream[ps]));
+            if (rc == 12 && ctx->out[ps].reserve((size_t)ctx->h_ctl[ps].total_out + 64))
+                return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(out)");
+            CK(cudaMemcpyAsync(ctx->in[ps].p, h_in + cuts[nch - 1], pend_n, cudaMemcpyHostToDevice,
+                               ctx->stream[ps]));
+            rc = launch_stream(ctx, ps, compress, ctx->in[ps].as<uint8_t>(), pend_n,
+                               ctx->out[ps].as<uint8_t>(), (long long)ctx->out[ps].cap, flags, false);
+            if (rc) return rc;
+            rc = finish(ps, pend_n, pend_len);
+        }
+        if (rc) return rc;
+    }
+    CK(cudaStreamSynchronize(ctx->stream[0]));
+    CK(cudaStreamSynchronize(ctx->stream[1]));
+    res->in_bytes = n;
+    res->out_bytes = written;
+    if (!trailing && res->lines > 0) res->out_bytes -= 1;
+    if (capacity_hit) return ZS_E_CAPACITY;
+    return ZS_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int zs_device_count(int *n) {
+    if (!n) return ZS_E_ARG;
+    cudaError_t e = cudaGetDeviceCount(n);
+    if (e != cudaSuccess) {
+        *n = 0;
+        return ZS_E_CUDA;
+    }
+    return ZS_OK;
+}
+
+int zs_ctx_create(int device, zs_ctx **out) {
+    if (!out) return ZS_E_ARG;
+    *out = nullptr;
+    zs_ctx *ctx = new zs_ctx();
+    ctx->dev = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, device);
+    for (int s = 0; s < 2 && e == cudaSuccess; ++s) {
+        e = cudaStreamCreateWithFlags(&ctx->stream[s], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_ctl[s], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_out[s], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_out[s], ctx->stream[s]);
+    }
+    if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_ctl, 2 * sizeof(Ctl));
+    if (e != cudaSuccess) {
+        delete ctx;
+        return ZS_E_CUDA;
+    }
+    *out = ctx;
+    return ZS_OK;
+}
+
+int zs_ctx_destroy(zs_ctx *ctx) {
+    if (!ctx) return ZS_OK;
+    cudaSetDevice(ctx->dev);
+    for (DevBuf *b : {&ctx->d_dfa, &ctx->d_codes, &ctx->d_children, &ctx->d_term, &ctx->d_explen,
+                      &ctx->d_expoff, &ctx->d_expflat, &ctx->ctl[0], &ctx->ctl[1], &ctx->ts[0],
+                      &ctx->ts[1], &ctx->terr[0], &ctx->terr[1], &ctx->in[0], &ctx->in[1],
+                      &ctx->out[0], &ctx->out[1], &ctx->arena[0], &ctx->arena[1], &ctx->s_flat, &ctx->s_starts,
+                      &ctx->s_out, &ctx->s_lens, &ctx->s_dec, &ctx->s_stat, &ctx->s_errpos,
+                      &ctx->s_tot, &ctx->s_ids, &ctx->s_outst})
+        b->release();
+    for (int s = 0; s < 2; ++s) {
+        if (ctx->stream[s]) cudaStreamDestroy(ctx->stream[s]);
+        if (ctx->ev_ctl[s]) cudaEventDestroy(ctx->ev_ctl[s]);
+        if (ctx->ev_out[s]) cudaEventDestroy(ctx->ev_out[s]);
+    }
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
+    delete ctx;
+    return ZS_OK;
+}
+
+const char *zs_last_error(zs_ctx *ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+float zs_last_kernel_ms(zs_ctx *ctx) { return ctx ? ctx->last_ms : 0.f; }
+
+int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_code,
+                      int32_t n_nodes, const int32_t *exp_len, const uint8_t *valid,
+                      const int64_t *exp_off, const uint8_t *exp_flat) {
+    if (!ctx || !children || !term_code || n_nodes < 1 || !exp_len || !valid || !exp_off)
+        return ZS_E_ARG;
+    CK(cudaSetDevice(ctx->dev));
+    HostTables &ht = ctx->ht;
+    ht = HostTables();
+    ht.n_nodes = n_nodes;
+    ht.children.assign(children, children + (size_t)n_nodes * 256);
+    ht.term_code.assign(term_code, term_code + n_nodes);
+    std::vector<std::pair<std::string, int>> pats;
+    trie_patterns(children, term_code, n_nodes, pats);
+    ht.max_len = 0;
+    for (auto &p : pats) ht.max_len = std::max<int>(ht.max_len, (int)p.first.size());
+    ht.fast = build_dfa(pats, ht.max_len, ht);
+    // decode tables (dictionary.py:112-129): valid codes have exp_len > 0
+    if (exp_off[256] > 65535) {
+        ctx->err = "expansion table too large";
+        return ZS_E_ARG;
+    }
+    for (int b = 0; b < 256; ++b) {
+        if (valid[b] && (exp_len[b] < 1 || exp_len[b] > 255)) {
+            ctx->err = "bad expansion length";
+            return ZS_E_ARG;
+        }
+        ht.exp_len[b] = valid[b] ? (uint8_t)exp_len[b] : 0;
+    }
+    for (int b = 0; b <= 256; ++b) ht.exp_off[b] = (uint16_t)exp_off[b];
+    ht.exp_flat.assign(exp_flat, exp_flat + exp_off[256]);
+    ht.exp_flat.resize(ht.exp_flat.size() + 16, 0);
+    // upload
+    auto up = [&](DevBuf &b, const void *src, size_t bytes) -> cudaError_t {
+        cudaError_t e = b.reserve(bytes + 16);
+        if (e == cudaSuccess) e = cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice);
+        return e;
+    };
+    CK(up(ctx->d_children, ht.children.data(), ht.children.size() * 4));
+    CK(up(ctx->d_term, ht.term_code.data(), ht.term_code.size() * 2));
+    CK(up(ctx->d_explen, ht.exp_len, 256));
+    CK(up(ctx->d_expoff, ht.exp_off, 257 * 2));
+    CK(up(ctx->d_expflat, ht.exp_flat.data(), ht.exp_flat.size()));
+    if (ht.fast) {
+        CK(up(ctx->d_dfa, ht.dfa.data(), ht.dfa.size() * 2));
+        CK(up(ctx->d_codes, ht.codes.data(), ht.codes.size()));
+    }
+    Tables &tb = ctx->tb;
+    tb.dfa = ht.fast ? ctx->d_dfa.as<uint16_t>() : nullptr;
+    tb.codes = ht.fast ? ctx->d_codes.as<uint8_t>() : nullptr;
+    tb.n_states = ht.fast ? ht.n_states : 0;
+    tb.fast = ht.fast ? 1 : 0;
+    tb.children = ctx->d_children.as<int32_t>();
+    tb.term_code = ctx->d_term.as<int16_t>();
+    tb.n_nodes = n_nodes;
+    tb.max_len = ht.max_len;
+    tb.exp_len = ctx->d_explen.as<uint8_t>();
+    tb.exp_off = ctx->d_expoff.as<uint16_t>();
+    tb.exp_flat = ctx->d_expflat.as<uint8_t>();
+    tb.n_flat = (int)exp_off[256];
+    ctx->fast_w = 0;
+    if (ht.fast) {
+        const int L = std::max(1, ht.max_len);
+        ctx->fast_w = L <= 2 ? 2 : L <= 4 ? 4 : L <= 6 ? 6 : 8;
+    }
+    ctx->have_dict = true;
+    return ZS_OK;
+}
+
+int zs_dictionary_fast(zs_ctx *ctx) { return ctx && ctx->have_dict ? ctx->fast_w : -1; }
+
+int zs_build_tables_host(const int32_t *children, const int16_t *term_code, int32_t n_nodes,
+                         uint16_t *dfa, uint8_t *codes, int32_t *n_states, int32_t *max_len) {
+    if (!children || !term_code || n_nodes < 1 || !dfa || !codes || !n_states || !max_len)
+        return ZS_E_ARG;
+    std::vector<std::pair<std::string, int>> pats;
+    trie_patterns(children, term_code, n_nodes, pats);
+    HostTables ht;
+    ht.max_len = 0;
+    for (auto &p : pats) ht.max_len = std::max<int>(ht.max_len, (int)p.first.size());
+    *max_len = ht.max_len;
+    *n_states = 0;
+    if (!build_dfa(pats, ht.max_len, ht)) return 0;
+    *n_states = ht.n_states;
+    memcpy(dfa, ht.dfa.data(), (size_t)ht.n_states * NCOL * 2);
+    memcpy(codes, ht.codes.data(), (size_t)ht.n_states * FAST_W);
+    return 1;
+}
+
+int64_t zs_compress_bound(int64_t n) { return 2 * n + 64; }
+
+int64_t zs_decompress_bound(zs_ctx *ctx, int64_t n) {
+    int m = 1;
+    if (ctx && ctx->have_dict)
+        for (int b = 0; b < 256; ++b) m = std::max<int>(m, ctx->ht.exp_len[b]);
+    return (int64_t)m * n + 64;
+}
+
+int zs_compress_device(zs_ctx *ctx, const uint8_t *d_in, int64_t n, uint8_t *d_out,
+                       int64_t out_cap, int flags, zs_result *res) {
+    return run_device(ctx, true, d_in, n, d_out, out_cap, flags, res);
+}
+
+int zs_decompress_device(zs_ctx *ctx, const uint8_t *d_in, int64_t n, uint8_t *d_out,
+                         int64_t out_cap, int flags, zs_result *res) {
+    return run_device(ctx, false, d_in, n, d_out, out_cap, flags, res);
+}
+
+int zs_compress_host(zs_ctx *ctx, const uint8_t *h_in, int64_t n, uint8_t *h_out,
+                     int64_t out_cap, int flags, zs_result *res) {
+    return run_host(ctx, true, h_in, n, h_out, out_cap, flags, res);
+}
+
+int zs_decompress_host(zs_ctx *ctx, const uint8_t *h_in, int64_t n, uint8_t *h_out,
+                       int64_t out_cap, int flags, zs_result *res) {
+    return run_host(ctx, false, h_in, n, h_out, out_cap, flags, res);
+}
+
+// ---------------------------------------------------------------------------
+// parity shim
+// ---------------------------------------------------------------------------
+static int upload_batch(zs_ctx *ctx, const uint8_t *flat, const int64_t *starts, int64_t n_lines) {
+    const long long n = starts[n_lines];
+    if (ctx->s_flat.reserve(n + 16) || ctx->s_starts.reserve(8 * (n_lines + 1)))
+        return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(batch)");
+    cudaStream_t st = ctx->stream[0];
+    if (n) CK(cudaMemcpyAsync(ctx->s_flat.p, flat, n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->s_starts.p, starts, 8 * (n_lines + 1), cudaMemcpyHostToDevice, st));
+    return ZS_OK;
+}
+
+int zs_compress_batch(zs_ctx *ctx, const uint8_t *flat, const int64_t *starts, int64_t n_lines,
+                      uint8_t *out, int64_t *out_lens, int64_t *escapes) {
+    if (!ctx || !starts || n_lines < 0 || !out_lens) return ZS_E_ARG;
+    if (!ctx->have_dict) return ZS_E_NODICT;
+    if (escapes) *escapes = 0;
+    if (n_lines == 0) return ZS_OK;
+    CK(cudaSetDevice(ctx->dev));
+    int rc = upload_batch(ctx, flat, starts, n_lines);
+    if (rc) return rc;
+    const long long n = starts[n_lines];
+    cudaStream_t st = ctx->stream[0];
+    if (ctx->s_out.reserve(2 * n + 16) || ctx->s_lens.reserve(8 * n_lines) ||
+        ctx->s_dec.reserve(n + n_lines + 16) || ctx->s_tot.reserve(16))
+        return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(batch)");
+    CK(cudaMemsetAsync(ctx->s_tot.p, 0, 16, st));
+    BatchKernel k = batch_kernel(ctx->fast_w);
+    const int smem = ctx->fast_w ? align16(ctx->tb.n_states * NCOL * 2) + align16(ctx->tb.n_states * FAST_W) : 0;
+    CK(set_smem(k, smem));
+    const int blocks = (int)((n_lines + 255) / 256);
+    k<<<blocks, 256, smem, st>>>(ctx->s_flat.as<uint8_t>(), ctx->s_starts.as<long long>(), n_lines,
+                                 ctx->s_out.as<uint8_t>(), ctx->s_lens.as<long long>(),
+                                 ctx->s_dec.as<uint8_t>(), ctx->s_tot.as<unsigned long long>(), ctx->tb);
+    CK(cudaGetLastError());
+    if (n && out) CK(cudaMemcpyAsync(out, ctx->s_out.p, 2 * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out_lens, ctx->s_lens.p, 8 * n_lines, cudaMemcpyDeviceToHost, st));
+    unsigned long long esc = 0;
+    CK(cudaMemcpyAsync(&esc, ctx->s_tot.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (escapes) *escapes = (int64_t)esc;
+    return ZS_OK;
+}
+
+int zs_decompress_sizes(zs_ctx *ctx, const uint8_t *flat, const int64_t *starts,
+                        int64_t n_lines, int64_t *out_lens, int8_t *status, int64_t *errpos,
+                        int64_t *total, int64_t *escapes) {
+    if (!ctx || !starts || n_lines < 0 || !out_lens || !status || !errpos) return ZS_E_ARG;
+    if (!ctx->have_dict) return ZS_E_NODICT;
+    if (total) *total = 0;
+    if (escapes) *escapes = 0;
+    if (n_lines == 0) return ZS_OK;
+    CK(cudaSetDevice(ctx->dev));
+    int rc = upload_batch(ctx, flat, starts, n_lines);
+    if (rc) return rc;
+    cudaStream_t st = ctx->stream[0];
+    if (ctx->s_lens.reserve(8 * n_lines) || ctx->s_stat.reserve(n_lines) ||
+        ctx->s_errpos.reserve(8 * n_lines) || ctx->s_tot.reserve(16))
+        return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(batch)");
+    CK(cudaMemsetAsync(ctx->s_tot.p, 0, 16, st));
+    batch_decode_sizes<<<(int)((n_lines + 255) / 256), 256, 0, st>>>(
+        ctx->s_flat.as<uint8_t>(), ctx->s_starts.as<long long>(), n_lines, ctx->s_lens.as<long long>(),
+        ctx->s_stat.as<int8_t>(), ctx->s_errpos.as<long long>(), ctx->s_tot.as<unsigned long long>(),
+        ctx->tb);
+    CK(cudaGetLastError());
+    unsigned long long tot[2];
+    CK(cudaMemcpyAsync(out_lens, ctx->s_lens.p, 8 * n_lines, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(status, ctx->s_stat.p, n_lines, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(errpos, ctx->s_errpos.p, 8 * n_lines, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(tot, ctx->s_tot.p, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (total) *total = (int64_t)tot[0];
+    if (escapes) *escapes = (int64_t)tot[1];
+    return ZS_OK;
+}
+
+int zs_decompress_fill(zs_ctx *ctx, const uint8_t *flat, const int64_t *starts, int64_t n_lines,
+                       const int8_t *status, uint8_t *out, const int64_t *out_starts) {
+    if (!ctx || !starts || n_lines < 0 || !status || !out_starts) return ZS_E_ARG;
+    if (!ctx->have_dict) return ZS_E_NODICT;
+    if (n_lines == 0) return ZS_OK;
+    CK(cudaSetDevice(ctx->dev));
+    int rc = upload_batch(ctx, flat, starts, n_lines);
+    if (rc) return rc;
+    cudaStream_t st = ctx->stream[0];
+    const long long total = out_starts[n_lines];
+    if (ctx->s_stat.reserve(n_lines) || ctx->s_outst.reserve(8 * (n_lines + 1)) ||
+        ctx->s_out.reserve(total + 16))
+        return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(batch)");
+    CK(cudaMemcpyAsync(ctx->s_stat.p, status, n_lines, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->s_outst.p, out_starts, 8 * (n_lines + 1), cudaMemcpyHostToDevice, st));
+    batch_decode_fill<<<(int)((n_lines + 255) / 256), 256, 0, st>>>(
+        ctx->s_flat.as<uint8_t>(), ctx->s_starts.as<long long>(), n_lines, ctx->s_stat.as<int8_t>(),
+        ctx->s_out.as<uint8_t>(), ctx->s_outst.as<long long>(), ctx->tb);
+    CK(cudaGetLastError());
+    if (total && out) CK(cudaMemcpyAsync(out, ctx->s_out.p, total, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return ZS_OK;
+}
+
+int zs_preprocess_batch(zs_ctx *ctx, const uint8_t *flat, const int64_t *starts,
+                        int64_t n_lines, uint8_t *out, int64_t *out_lens, int8_t *status,
+                        int64_t *err_off, uint64_t *err_ids) {
+    if (!ctx || !starts || n_lines < 0 || !out || !out_lens || !status || !err_off || !err_ids)
+        return ZS_E_ARG;
+    if (n_lines == 0) return ZS_OK;
+    CK(cudaSetDevice(ctx->dev));
+    int rc = upload_batch(ctx, flat, starts, n_lines);
+    if (rc) return rc;
+    cudaStream_t st = ctx->stream[0];
+    const long long n = starts[n_lines];
+    const long long ocap = 3 * n + 3 * n_lines;
+    if (ctx->s_out.reserve(ocap + 16) || ctx->s_lens.reserve(8 * n_lines) ||
+        ctx->s_stat.reserve(n_lines) || ctx->s_errpos.reserve(8 * n_lines) ||
+        ctx->s_ids.reserve(16 * n_lines) || ctx->s_dec.reserve(n + n_lines + 16))
+        return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(batch)");
+    batch_preprocess<<<(int)((n_lines + 255) / 256), 256, 0, st>>>(
+        ctx->s_flat.as<uint8_t>(), ctx->s_starts.as<long long>(), n_lines, ctx->s_out.as<uint8_t>(),
+        ctx->s_lens.as<long long>(), ctx->s_stat.as<int8_t>(), ctx->s_errpos.as<long long>(),
+        ctx->s_ids.as<unsigned long long>(), ctx->s_dec.as<uint8_t>());
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, ctx->s_out.p, ocap, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out_lens, ctx->s_lens.p, 8 * n_lines, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(status, ctx->s_stat.p, n_lines, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(err_off, ctx->s_errpos.p, 8 * n_lines, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(err_ids, ctx->s_ids.p, 16 * n_lines, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return ZS_OK;
+}
+
+}  // extern "C"

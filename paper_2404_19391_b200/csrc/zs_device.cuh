@@ -1,0 +1,438 @@
+// zs_device.cuh -- sm_100a device code for the ZSMILES per-line codec.
+//
+// Layout of the hot path:
+//   * The input buffer stays resident in HBM.  It is cut into fixed TILE-byte
+//     tiles; a line belongs to the tile in which it STARTS.  One persistent
+//     CTA per SM takes tiles in order from an atomic ticket.
+//   * Per tile the CTA stages [tile_start-16, tile_end+EXTRA) in shared memory
+//     (16-byte vector loads), finds its line starts (newline scan + block
+//     scan -> a compact queue), and processes lines thread-per-line from the
+//     queue: CR policy, ring renumbering (in place in smem), then the
+//     min-cost parse.
+//   * The parse runs right-to-left over a reversed-pattern Aho-Corasick DFA
+//     held in shared memory: one 16-bit table lookup per byte yields the next
+//     state and the set of dictionary match lengths starting at that byte;
+//     the DP keeps the next W costs in registers as packed keys
+//     (cost<<3)-position, so "cheapest, then longest" (numba_impl.py:50) is a
+//     single signed min.  Decisions (the chosen code byte, 0x20 = escape) are
+//     written per byte into smem.
+//   * Tile output size -> decoupled look-back over tiles (single pass, no
+//     line-offset array in HBM) -> the forward emit writes compressed records
+//     into a smem staging buffer -> coalesced 16-byte stores to HBM.
+//   * Decompression uses the same tile/look-back skeleton with a table-driven
+//     size/validate pass and expansion pass.
+//
+// Lines that do not fit the smem window (longer than EXTRA past the tile, or
+// lines that grow under renumbering) take a "global" path in the same kernel:
+// scratch from a bump arena in HBM and the reference-shaped trie walk.
+#pragma once
+#include <stdint.h>
+
+namespace zs {
+
+// ----------------------------------------------------------------------------
+// constants
+// ----------------------------------------------------------------------------
+constexpr int NT = 512;                 // threads per CTA
+constexpr int NWARP = NT / 32;
+constexpr int TILE = 32768;             // bytes of line-start ownership per tile
+constexpr int EXTRA = 4096;             // window overhang past the tile end
+constexpr int HEAD = 16;                // bytes staged before the tile start
+constexpr int WIN = HEAD + TILE + EXTRA;  // staged window (multiple of 16)
+constexpr int CHUNK = TILE / NT;        // per-thread newline-scan chunk (64 B)
+constexpr int QCAP = 4096;              // line queue capacity per round
+constexpr int OUTCAP = TILE + EXTRA;    // compress staging (no-expansion case)
+constexpr int DOUTCAP = 3 * TILE;       // decompress staging
+constexpr int NCOL = 97;                // DFA columns: bytes 0x20..0x7f, other
+constexpr int FAST_W = 8;               // max pattern length on the fast path
+constexpr int FAST_STATES = 256;        // max DFA states on the fast path
+
+// decision-byte sentinels (never valid codes: codes are 0x21-0x7e, 0x80-0xff)
+constexpr uint8_t D_ESC = 0x20;   // escape: emit 0x20 + literal
+constexpr uint8_t D_END = 0x0A;   // end of (preprocessed) line
+constexpr uint8_t D_DROP = 0x0D;  // line dropped (lenient CR) or strict error
+constexpr uint8_t D_GLOBAL = 0x0B;  // line processed in the HBM arena
+
+// tile flags for the look-back
+constexpr unsigned F_AGG = 1u, F_INC = 2u;
+
+enum ErrKind {
+    E_NONE = 0, E_CR = 1, E_BRACKET = 2, E_PERCENT = 3, E_UNPAIRED = 4, E_OVERFLOW = 5,
+    E_UNKNOWN = 6, E_TRUNC = 7
+};
+
+struct Tables {
+    // fast path: reversed-pattern AC DFA, [n_states][NCOL] u16 = next | mask<<8
+    const uint16_t *dfa;
+    const uint8_t *codes;   // [n_states][FAST_W] code of the match of length L+1
+    int n_states;
+    int fast;               // 1 if the DFA path serves this dictionary
+    // generic path (reference layout): dense trie in HBM
+    const int32_t *children;  // [n_nodes][256]
+    const int16_t *term_code;
+    int n_nodes;
+    int max_len;
+    // decode
+    const uint8_t *exp_len;   // [256], 0 = invalid code
+    const uint16_t *exp_off;  // [257]
+    const uint8_t *exp_flat;
+    int n_flat;
+};
+
+struct Ctl {                    // zeroed before every launch
+    unsigned long long ticket;
+    unsigned long long total_out;
+    unsigned long long lines;
+    unsigned long long escapes;
+    unsigned long long skipped;
+    unsigned long long flagged;
+    unsigned long long err_key;    // (line_idx << 24) | tile ; ~0 = none
+    unsigned long long arena_used;
+    unsigned long long overflow;   // output or arena capacity exceeded
+    unsigned long long in_lines;   // lines seen (records in)
+};
+
+struct TileState {
+    unsigned int flag;
+    unsigned int pad;
+    unsigned long long agg_out, agg_lines, inc_out, inc_lines;
+};
+
+struct TileErr {
+    int kind;
+    int code;
+    long long offset;
+    unsigned long long ids[2];
+};
+
+struct Job {
+    const uint8_t *in;
+    long long n;
+    uint8_t *out;
+    long long out_cap;
+    int preprocess, lenient;
+    long long n_tiles;
+    Ctl *ctl;
+    TileState *ts;
+    TileErr *terr;
+    uint8_t *arena;
+    long long arena_cap;
+};
+
+// ----------------------------------------------------------------------------
+// small helpers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ int dcol(unsigned b) { return (int)min(b - 0x20u, 96u); }
+
+__device__ __forceinline__ bool is_digit(unsigned b) { return b - '0' < 10u; }
+
+// byte classes for the tokenizer (smiles.py:23-35, 83-137)
+enum : uint8_t {
+    C_OTHER = 0, C_ATOM = 1, C_BOND = 2, C_DIGIT = 3, C_PCT = 4, C_LBR = 5, C_RBR = 6,
+    C_BOPEN = 7, C_BCLOSE = 8, C_DOT = 9, C_CR = 10
+};
+
+__device__ __forceinline__ uint8_t tok_class(unsigned b) {
+    if ((b | 0x20u) - 'a' < 26u || b == '*') return C_ATOM;
+    if (b - '0' < 10u) return C_DIGIT;
+    switch (b) {
+    case '-': case '=': case '#': case '$': case ':': case '/': case '\\': case '~': return C_BOND;
+    case '%': return C_PCT;
+    case '[': return C_LBR;
+    case ']': return C_RBR;
+    case '(': return C_BOPEN;
+    case ')': return C_BCLOSE;
+    case '.': return C_DOT;
+    case '\r': return C_CR;
+    default: return C_OTHER;
+    }
+}
+
+// block-wide exclusive scan of one value per thread (NT threads)
+template <typename T>
+__device__ __forceinline__ T block_exscan(T v, T *warp_tmp, T &total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tmp[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        T w = lane < NWARP ? warp_tmp[lane] : T(0);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            T y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < NWARP) warp_tmp[lane] = w;  // inclusive per warp
+    }
+    __syncthreads();
+    T base = wid ? warp_tmp[wid - 1] : T(0);
+    total = warp_tmp[NWARP - 1];
+    __syncthreads();
+    return base + x - v;
+}
+
+// ----------------------------------------------------------------------------
+// decoupled look-back over tiles (ordered tickets guarantee progress)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void lookback(TileState *ts, long long t, unsigned long long agg_out,
+                                         unsigned long long agg_lines,
+                                         unsigned long long &pre_out,
+                                         unsigned long long &pre_lines) {
+    volatile TileState *vts = ts;
+    if (t == 0) {
+        vts[0].inc_out = agg_out;
+        vts[0].inc_lines = agg_lines;
+        __threadfence();
+        atomicExch(&ts[0].flag, F_INC);
+        pre_out = 0;
+        pre_lines = 0;
+        return;
+    }
+    vts[t].agg_out = agg_out;
+    vts[t].agg_lines = agg_lines;
+    __threadfence();
+    atomicExch(&ts[t].flag, F_AGG);
+    unsigned long long po = 0, pl = 0;
+    long long j = t - 1;
+    while (true) {
+        unsigned f;
+        do {
+            f = vts[j].flag;
+        } while (f == 0);
+        __threadfence();
+        if (f == F_INC) {
+            po += vts[j].inc_out;
+            pl += vts[j].inc_lines;
+            break;
+        }
+        po += vts[j].agg_out;
+        pl += vts[j].agg_lines;
+        --j;
+    }
+    vts[t].inc_out = po + agg_out;
+    vts[t].inc_lines = pl + agg_lines;
+    __threadfence();
+    atomicExch(&ts[t].flag, F_INC);
+    pre_out = po;
+    pre_lines = pl;
+}
+
+// ----------------------------------------------------------------------------
+// ring renumbering of one line (smiles.py:83-213), strict semantics.
+//
+// buf[0..n) is the line; marks[0..n] is per-byte scratch (0xff = not a ring
+// token start, 0xfe = ring opened / colour pending, <100 = assigned colour).
+// One forward pass tokenizes, pairs ids (occurrences alternate open/close)
+// and colours each ring when it closes with the smallest id not used by a
+// ring that closed inside it (closing-order greedy, smiles.py:162-180): a
+// single backward scan from the closing token finds the opener (the most
+// recent pending token with the same id) and collects those colours.
+// Returns E_NONE and the new length in *new_len (the rewrite is in place
+// when no ring token grows), E_CR if a '\r' is present anywhere, another
+// E_* on a tokenize/pair/colour error (err_off / ids filled), or -1 when the
+// line grows (caller re-runs it out of place with out != buf).
+// ----------------------------------------------------------------------------
+__device__ int preprocess_line(const uint8_t *buf, int n, uint8_t *marks, uint8_t *out,
+                               int *new_len, int *err_off, unsigned long long ids[2],
+                               bool cr_is_error = true) {
+    uint64_t open0 = 0, open1 = 0;  // currently open ring ids
+    bool ring_ok = false;
+    int nrings = 0, grow = 0;
+    int err = E_NONE, eoff = -1;
+    int i = 0;
+    while (i < n) {
+        unsigned b = buf[i];
+        uint8_t c = tok_class(b);
+        if (c == C_CR && !cr_is_error) c = C_OTHER;
+        marks[i] = 0xff;
+        int rid = -1, tlen = 1;
+        if (c == C_ATOM || c == C_BOND) {
+            ring_ok = true;
+        } else if (c == C_DIGIT) {
+            if (ring_ok) rid = (int)(b - '0');
+        } else if (c == C_PCT) {
+            if (i + 2 >= n || !is_digit(buf[i + 1]) || !is_digit(buf[i + 2])) {
+                err = E_PERCENT; eoff = i;
+                break;
+            }
+            marks[i + 1] = 0xff;
+            marks[i + 2] = 0xff;
+            tlen = 3;
+            if (ring_ok) rid = (int)(buf[i + 1] - '0') * 10 + (int)(buf[i + 2] - '0');
+        } else if (c == C_LBR) {
+            int j = i + 1;
+            while (j < n && buf[j] != ']') {
+                if (cr_is_error && buf[j] == '\r') { err = E_CR; break; }
+                marks[j] = 0xff;
+                ++j;
+            }
+            if (err) break;
+            if (j >= n) { err = E_BRACKET; eoff = i; break; }
+            marks[j] = 0xff;
+            tlen = j + 1 - i;
+            ring_ok = true;
+        } else if (c == C_CR) {
+            err = E_CR;
+            break;
+        } else {
+            ring_ok = false;  // ( ) . and any other byte
+        }
+        if (rid >= 0) {
+            // ring closure token
+            uint64_t bit = 1ull << (rid & 63);
+            bool is_open = rid < 64 ? (open0 & bit) : (open1 & bit);
+            if (!is_open) {
+                marks[i] = 0xfe;
+                if (rid < 64) open0 |= bit; else open1 |= bit;
+            } else {
+                if (rid < 64) open0 &= ~bit; else open1 &= ~bit;
+                uint64_t used0 = 0, used1 = 0;
+                int o = i - 1;
+                for (;; --o) {
+                    uint8_t m = marks[o];
+                    if (m == 0xfe) {
+                        int r2 = buf[o] == '%' ? (buf[o + 1] - '0') * 10 + (buf[o + 2] - '0')
+                                               : buf[o] - '0';
+                        if (r2 == rid) break;
+                    } else if (m < 100) {
+                        if (m < 64) used0 |= 1ull << m; else used1 |= 1ull << (m - 64);
+                    }
+                }
+                int col = used0 != ~0ull ? __ffsll((long long)~used0) - 1
+                                         : 64 + (used1 != ~0ull ? __ffsll((long long)~used1) - 1 : 64);
+                if (col > 99) { err = E_OVERFLOW; break; }
+                marks[o] = (uint8_t)col;
+                marks[i] = (uint8_t)col;
+                // an endpoint grows only when a 1-byte id takes a colour >= 10
+                // (the two endpoints may differ: '1' pairs with '%01')
+                if (col >= 10) grow |= (buf[o] != '%') | (tlen == 1);
+                nrings++;
+            }
+            ring_ok = true;
+        }
+        i += tlen;
+    }
+    if (err == E_NONE && (open0 | open1)) {
+        err = E_UNPAIRED;
+        ids[0] = open0;
+        ids[1] = open1;
+    }
+    if (cr_is_error && err != E_NONE && err != E_CR) {
+        // CR anywhere in the line takes precedence (pipeline.py:102-107)
+        for (int k = 0; k < n; ++k)
+            if (buf[k] == '\r') { err = E_CR; break; }
+    }
+    if (err != E_NONE) {
+        *err_off = eoff;
+        return err;
+    }
+    if (nrings == 0) {
+        if (out != buf)
+            for (int k = 0; k < n; ++k) out[k] = buf[k];
+        *new_len = n;
+        return E_NONE;
+    }
+    if (grow && out == buf) return -1;  // needs an out-of-place rewrite
+    // rewrite: tokens keep order; every ring token takes its colour text
+    int w = 0;
+    for (int r = 0; r < n;) {
+        uint8_t m = marks[r];
+        if (m < 100) {
+            int ol = buf[r] == '%' ? 3 : 1;
+            if (m < 10) {
+                out[w++] = (uint8_t)('0' + m);
+            } else {
+                out[w++] = '%';
+                out[w++] = (uint8_t)('0' + m / 10);
+                out[w++] = (uint8_t)('0' + m % 10);
+            }
+            r += ol;
+        } else {
+            out[w++] = buf[r++];
+        }
+    }
+    *new_len = w;
+    return E_NONE;
+}
+
+// ----------------------------------------------------------------------------
+// min-cost parse, fast path: reversed AC DFA in smem, W <= 8.
+//
+// key(j) = (cost[j] << 3) - j.  Among candidates j in (i, i+W], a smaller key
+// means cheaper, and at equal cost the larger j (= longer match), which is
+// exactly the reference's replacement rule (numba_impl.py:50).  The escape
+// edge (cost 2 + cost[i+1]) loses every tie because it shares j = i+1 with
+// the length-1 match only, which is strictly cheaper.
+// s[0..n) line bytes, dec[0..n] decisions out.  Returns cost[0].
+// ----------------------------------------------------------------------------
+template <int W>
+__device__ __forceinline__ int dp_fast(const uint8_t *s, int n, uint8_t *dec,
+                                       const uint16_t *dfa, const uint8_t *codes) {
+    constexpr int INF = 0x3fffffff;
+    int k[W + 1];
+#pragma unroll
+    for (int L = 1; L <= W; ++L) k[L] = INF;
+    // position n: cost 0
+    int key = -n;
+    int st = 0;
+    dec[n] = D_END;
+    for (int i = n - 1; i >= 0; --i) {
+        // shift window: k[L] = key of position i+L
+#pragma unroll
+        for (int L = W; L > 1; --L) k[L] = k[L - 1];
+        k[1] = key;
+        unsigned b = s[i];
+        unsigned e = dfa[st * NCOL + dcol(b)];
+        st = e & 0xffu;
+        int mm = INF;
+#pragma unroll
+        for (int L = 1; L <= W; ++L)
+            if (e & (0x100u << (L - 1))) mm = min(mm, k[L]);
+        int esc = k[1] + (2 << 3);
+        int best = min(esc, mm + (1 << 3));
+        int t = best + i + W;
+        int L = W - (t & 7);
+        key = (t & ~7) - i;
+        uint8_t code = codes[st * FAST_W + L - 1];
+        dec[i] = esc < mm + (1 << 3) ? D_ESC : code;
+    }
+    return key >> 3;  // position 0: key = cost[0] << 3
+}
+
+// ----------------------------------------------------------------------------
+// min-cost parse, generic path: the reference trie walk (numba_impl.py:37-56)
+// over the dense HBM trie; keys (cost<<7)-j in a 128-entry ring buffer so any
+// pattern length <= 64 works.  s/dec may live in smem or HBM.
+// ----------------------------------------------------------------------------
+__device__ long long dp_generic(const uint8_t *s, long long n, uint8_t *dec, const Tables &tb,
+                                long long *ring /* 128 entries */) {
+    ring[n & 127] = -n;  // key of position n: cost 0
+    dec[n] = D_END;
+    for (long long i = n - 1; i >= 0; --i) {
+        long long best = ring[(i + 1) & 127] + (2ll << 7);
+        int bc = -1;
+        int node = 0;
+        for (long long j = i; j < n; ++j) {
+            node = __ldg(&tb.children[(long long)node * 256 + s[j]]);
+            if (node < 0) break;
+            int tc = __ldg(&tb.term_code[node]);
+            if (tc < 0) continue;
+            long long cand = ring[(j + 1) & 127] + (1ll << 7);
+            if (cand < best) {  // keys encode "cheaper, then longer"
+                best = cand;
+                bc = tc;
+            }
+        }
+        long long t = best + i + 127;
+        ring[i & 127] = (t & ~127ll) - i;
+        dec[i] = bc < 0 ? D_ESC : (uint8_t)bc;
+    }
+    return ring[0] >> 7;
+}
+
+}  // namespace zs

@@ -1,0 +1,755 @@
+// zs_kernels.cuh -- sm_100a kernels: fused single-pass tile kernels for the
+// whole-buffer path and the thread-per-line parity-shim kernels.
+#pragma once
+#include "zs_device.cuh"
+
+namespace zs {
+
+// ----------------------------------------------------------------------------
+// shared-memory carve-up for the compress tile kernel
+// ----------------------------------------------------------------------------
+struct CSmem {
+    uint16_t *dfa;
+    uint8_t *codes;
+    uint8_t *explen;
+    uint8_t *win;
+    uint8_t *dec;
+    uint8_t *out;
+    uint16_t *queue;
+    unsigned *chunk;
+};
+
+__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
+
+__host__ __device__ inline int compress_smem_bytes(int n_states) {
+    return align16(n_states * NCOL * 2) + align16(n_states * FAST_W) + 256 + align16(WIN + 16) +
+           align16(WIN + 16) + align16(OUTCAP) + QCAP * 2 + NT * 4;
+}
+
+struct DSmem {
+    uint8_t *expflat;
+    uint16_t *expoff;
+    uint8_t *explen;
+    uint8_t *win;
+    uint8_t *out;
+    uint16_t *queue;
+    unsigned *chunk;
+    uint8_t *stat;  // one status byte per line ordinal of the tile
+};
+
+__host__ __device__ inline int decompress_smem_bytes(int n_flat) {
+    return align16(n_flat + 16) + align16(257 * 2) + 256 + align16(WIN + 16) + align16(DOUTCAP) +
+           QCAP * 2 + NT * 4 + TILE;
+}
+
+__device__ inline DSmem carve_dsmem(uint8_t *p, int n_flat) {
+    DSmem S;
+    S.expflat = p; p += align16(n_flat + 16);
+    S.expoff = reinterpret_cast<uint16_t *>(p); p += align16(257 * 2);
+    S.explen = p; p += 256;
+    S.win = p; p += align16(WIN + 16);
+    S.out = p; p += align16(DOUTCAP);
+    S.queue = reinterpret_cast<uint16_t *>(p); p += QCAP * 2;
+    S.chunk = reinterpret_cast<unsigned *>(p); p += NT * 4;
+    S.stat = p;
+    return S;
+}
+
+// Stage window bytes [ws, ws+len) of `in` into smem `win` (positions before
+// the buffer start read as '\n' so offset 0 is a line start).
+__device__ __forceinline__ void load_window(const uint8_t *in, long long n, long long ws, int len,
+                                            uint8_t *win) {
+    const bool aligned = ((reinterpret_cast<uintptr_t>(in) & 15) == 0) && ws >= 0 &&
+                         ws + len <= n && (len & 15) == 0;
+    if (aligned) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(in + ws);
+        uint4 *dst = reinterpret_cast<uint4 *>(win);
+        for (int k = threadIdx.x; k < len / 16; k += NT) dst[k] = __ldcs(src + k);
+    } else {
+        for (int k = threadIdx.x; k < len; k += NT) {
+            long long g = ws + k;
+            win[k] = g < 0 ? (uint8_t)'\n' : (g < n ? __ldcs(in + g) : (uint8_t)'\n');
+        }
+    }
+}
+
+// Each thread scans its CHUNK of the tile for line starts (a start is a
+// position p in [T0, T1) whose previous byte is '\n').  Returns the count and,
+// when `queue` is given, writes the window offsets of the starts whose
+// ordinal falls in [q0, q1) at queue[ord - q0].
+__device__ __forceinline__ int scan_starts(const uint8_t *win, int tile_len, int base_ord,
+                                           uint16_t *queue, int q0, int q1) {
+    const int c0 = threadIdx.x * CHUNK;
+    const int c1 = min(c0 + CHUNK, tile_len);
+    int cnt = 0;
+    for (int p = c0; p < c1; ++p) {
+        if (win[HEAD + p - 1] == '\n') {
+            int ord = base_ord + cnt;
+            if (queue && ord >= q0 && ord < q1) queue[ord - q0] = (uint16_t)(HEAD + p);
+            ++cnt;
+        }
+    }
+    return cnt;
+}
+
+// Find the end (window offset of '\n', or of EOF) of the line starting at
+// window offset p; -1 if the line runs past the staged window.
+__device__ __forceinline__ int find_end(const uint8_t *win, int p, int win_len, bool window_hits_eof) {
+    for (int k = p; k < win_len; ++k)
+        if (win[k] == '\n') return k;
+    return window_hits_eof ? win_len : -1;
+}
+
+// arena block for a line processed out of smem:
+// [ArenaHdr][pre bytes: 3n+3, 16-aligned][decisions: 3n+4]
+struct ArenaHdr {
+    long long n_pre;     // length of the (preprocessed) line
+    long long bytes_off; // offset of the line bytes in the arena, -1 = in the input
+    long long dec_off;   // offset of the decision bytes in the arena
+    long long pad;
+};
+
+// Process one line in HBM (long line or one that grows under renumbering).
+// Returns the payload size (cost[0]) and sets *kind to an error kind, or
+// -2 when the arena is exhausted.
+__device__ long long compress_line_global(const Job &job, const Tables &tb, long long gstart,
+                                          long long n_l, unsigned *arena_off16, int *kind,
+                                          int *eoff, unsigned long long ids[2]) {
+    const uint8_t *src = job.in + gstart;
+    long long need = (long long)sizeof(ArenaHdr) + ((3 * n_l + 3 + 15) & ~15ll) +
+                     ((3 * n_l + 4 + 15) & ~15ll);
+    unsigned long long a = atomicAdd((unsigned long long *)&job.ctl->arena_used,
+                                     (unsigned long long)need);
+    if ((long long)(a + need) > job.arena_cap) {
+        atomicOr((unsigned long long *)&job.ctl->overflow, 2ull);
+        *kind = -2;
+        return 0;
+    }
+    uint8_t *blk = job.arena + a;
+    ArenaHdr *h = reinterpret_cast<ArenaHdr *>(blk);
+    uint8_t *pre = blk + sizeof(ArenaHdr);
+    uint8_t *dec = pre + ((3 * n_l + 3 + 15) & ~15ll);
+    h->dec_off = (long long)(dec - job.arena);
+    *arena_off16 = (unsigned)(a >> 4);
+    const uint8_t *line = src;
+    long long n_pre = n_l;
+    *kind = E_NONE;
+    if (job.preprocess) {
+        int nl2 = 0;
+        int k = preprocess_line(src, (int)n_l, dec, pre, &nl2, eoff, ids);
+        if (k != E_NONE) {
+            *kind = k;
+            if (k == E_CR || !job.lenient) return 0;
+            // lenient: keep the raw line (pipeline.py:108-115)
+            *kind = -3;  // flagged
+        } else {
+            line = pre;
+            n_pre = nl2;
+        }
+    } else {
+        for (long long q = 0; q < n_l; ++q)
+            if (src[q] == '\r') { *kind = E_CR; return 0; }
+    }
+    h->n_pre = n_pre;
+    h->bytes_off = line == src ? -1 : (long long)(pre - job.arena);
+    long long ring[128];
+    return dp_generic(line, n_pre, dec, tb, ring);
+}
+
+// ----------------------------------------------------------------------------
+// compress: one persistent CTA per SM, tiles in ticket order.
+// W = fast-path window (max pattern length) or 0 for the generic trie walk.
+// ----------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ unsigned long long s_tmp64[NWARP];
+    __shared__ int s_tmp32[NWARP];
+    __shared__ long long s_tile;
+    __shared__ int s_qhead, s_err_ord, s_global;
+    __shared__ unsigned long long s_pre_out, s_pre_lines;
+    __shared__ unsigned s_kept, s_esc, s_skip, s_flag;
+
+    CSmem S;
+    {
+        uint8_t *p = smem;
+        const int ns = W ? tb.n_states : 0;
+        S.dfa = reinterpret_cast<uint16_t *>(p); p += align16(ns * NCOL * 2);
+        S.codes = p; p += align16(ns * FAST_W);
+        S.explen = p; p += 256;
+        S.win = p; p += align16(WIN + 16);
+        S.dec = p; p += align16(WIN + 16);
+        S.out = p; p += align16(OUTCAP);
+        S.queue = reinterpret_cast<uint16_t *>(p); p += QCAP * 2;
+        S.chunk = reinterpret_cast<unsigned *>(p);
+        // tables -> smem once per CTA
+        if (W) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(tb.dfa);
+            uint4 *dst = reinterpret_cast<uint4 *>(S.dfa);
+            for (int k = threadIdx.x; k < align16(ns * NCOL * 2) / 16; k += NT) dst[k] = src[k];
+            for (int k = threadIdx.x; k < ns * FAST_W; k += NT) S.codes[k] = tb.codes[k];
+        }
+        for (int k = threadIdx.x; k < 256; k += NT) S.explen[k] = tb.exp_len[k];
+    }
+    const int tid = threadIdx.x;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) {
+            s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
+            s_err_ord = 0x7fffffff;
+            s_global = 0;
+            s_kept = s_esc = s_skip = s_flag = 0;
+        }
+        __syncthreads();
+        const long long t = s_tile;
+        if (t >= job.n_tiles) break;
+        const long long T0 = t * (long long)TILE;
+        const int tile_len = (int)min((long long)TILE, job.n - T0);
+        const long long ws = T0 - HEAD;
+        const long long we = min(job.n, T0 + TILE + EXTRA);
+        const int win_len = (int)(we - ws);
+        const bool hits_eof = we == job.n;
+        load_window(job.in, job.n, ws, align16(win_len), S.win);
+        S.chunk[tid] = 0;
+        __syncthreads();
+
+        // ---- line starts: per-thread chunk counts -> block scan ----
+        const int my_cnt = scan_starts(S.win, tile_len, 0, nullptr, 0, 0);
+        int tile_lines;
+        const int my_off = block_exscan<int>(my_cnt, s_tmp32, tile_lines);
+
+        // ---- DP phase, in rounds of QCAP lines ----
+        for (int q0 = 0; q0 < tile_lines; q0 += QCAP) {
+            const int q1 = min(q0 + QCAP, tile_lines);
+            if (my_cnt) scan_starts(S.win, tile_len, my_off, S.queue, q0, q1);
+            if (tid == 0) s_qhead = 0;
+            __syncthreads();
+            for (;;) {
+                const int q = atomicAdd(&s_qhead, 1);
+                if (q >= q1 - q0) break;
+                const int ord = q0 + q;
+                const int p = S.queue[q];
+                int end = (q + 1 < q1 - q0) ? S.queue[q + 1] - 1 : find_end(S.win, p, win_len, hits_eof);
+                const int chunk_owner = (p - HEAD) / CHUNK;
+                int kind = E_NONE;
+                long long size = 0;
+                bool global_line = end < 0;
+                if (!global_line) {
+                    uint8_t *s = S.win + p;
+                    uint8_t *d = S.dec + p;
+                    int n_l = end - p;
+                    if (job.preprocess) {
+                        int nl2 = n_l, eoff;
+                        unsigned long long ids[2] = {0, 0};
+                        int k = preprocess_line(s, n_l, d, s, &nl2, &eoff, ids);
+                        if (k == -1) {
+                            global_line = true;
+                        } else if (k == E_CR) {
+                            kind = E_CR;
+                        } else if (k != E_NONE) {
+                            if (job.lenient) atomicAdd(&s_flag, 1u);
+                            else kind = k;
+                        } else {
+                            n_l = nl2;
+                        }
+                    } else {
+                        for (int k = 0; k < n_l; ++k)
+                            if (s[k] == '\r') { kind = E_CR; break; }
+                    }
+                    if (!global_line) {
+                        if (kind != E_NONE) {
+                            d[0] = D_DROP;
+                            if (job.lenient) atomicAdd(&s_skip, 1u);
+                            else atomicMin(&s_err_ord, ord);
+                        } else {
+                            if constexpr (W > 0)
+                                size = dp_fast<W>(s, n_l, d, S.dfa, S.codes) + 1;
+                            else {
+                                long long ring[128];
+                                size = dp_generic(s, n_l, d, tb, ring) + 1;
+                            }
+                        }
+                    }
+                }
+                if (global_line) {
+                    // line in HBM: find its end, process in the arena
+                    const long long gs = ws + p;
+                    long long ge = gs;
+                    while (ge < job.n && job.in[ge] != '\n') ++ge;
+                    unsigned aoff = 0;
+                    int eoff = -1;
+                    unsigned long long ids[2] = {0, 0};
+                    long long cost = compress_line_global(job, tb, gs, ge - gs, &aoff, &kind, &eoff, ids);
+                    s_global = 1;
+                    uint8_t *d = S.dec + p;
+                    if (kind == -2) {
+                        d[0] = D_DROP;  // arena exhausted; host re-runs
+                        kind = E_NONE;
+                    } else if (kind == E_CR || (kind > 0 && !job.lenient)) {
+                        d[0] = D_DROP;
+                        if (job.lenient) atomicAdd(&s_skip, 1u);
+                        else atomicMin(&s_err_ord, ord);
+                    } else {
+                        if (kind == -3) atomicAdd(&s_flag, 1u);
+                        kind = E_NONE;
+                        d[0] = D_GLOBAL;
+                        d[1] = aoff & 0xff; d[2] = (aoff >> 8) & 0xff;
+                        d[3] = (aoff >> 16) & 0xff; d[4] = (aoff >> 24) & 0xff;
+                        size = cost + 1;
+                    }
+                }
+                if (size) atomicAdd(&S.chunk[chunk_owner], (unsigned)size);
+                if (size) atomicAdd(&s_kept, 1u);
+            }
+            __syncthreads();
+        }
+
+        // ---- tile output size, look-back ----
+        unsigned long long tile_out;
+        const unsigned long long my_out = S.chunk[tid];
+        const unsigned long long my_out_off = block_exscan<unsigned long long>(my_out, s_tmp64, tile_out);
+        if (tid == 0) {
+            unsigned long long po, pl;
+            lookback(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
+            s_pre_out = po;
+            s_pre_lines = pl;
+            atomicAdd(&job.ctl->total_out, tile_out);
+            atomicAdd(&job.ctl->lines, (unsigned long long)s_kept);
+            atomicAdd(&job.ctl->in_lines, (unsigned long long)tile_lines);
+            if (s_skip) atomicAdd(&job.ctl->skipped, (unsigned long long)s_skip);
+            if (s_flag) atomicAdd(&job.ctl->flagged, (unsigned long long)s_flag);
+            if (s_pre_out + tile_out > (unsigned long long)job.out_cap)
+                atomicOr(&job.ctl->overflow, 1ull);
+        }
+        __syncthreads();
+        const unsigned long long pre_out = s_pre_out;
+        const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
+        const bool staged = fits && !s_global && tile_out <= (unsigned long long)OUTCAP;
+
+        // ---- strict error: re-derive details of the first bad line ----
+        if (tid == 0 && s_err_ord != 0x7fffffff) {
+            // find its start by ordinal
+            int ord = s_err_ord, seen = 0, p = -1;
+            for (int x = 0; x < tile_len && p < 0; ++x)
+                if (S.win[HEAD + x - 1] == '\n') {
+                    if (seen == ord) p = HEAD + x;
+                    ++seen;
+                }
+            long long gs = ws + p, ge = gs;
+            while (ge < job.n && job.in[ge] != '\n') ++ge;
+            TileErr e = {E_CR, 0, -1, {0, 0}};
+            bool cr = false;
+            for (long long k = gs; k < ge; ++k) cr |= job.in[k] == '\r';
+            if (!cr && job.preprocess) {
+                // recompute from the pristine input (marks in the arena-free
+                // output staging area, which is not used yet)
+                int nl2, eoff = -1;
+                unsigned long long ids[2] = {0, 0};
+                const long long n_l = ge - gs;
+                uint8_t *tmp = S.out;  // n_l+1 marks + 3n_l+3 out
+                if (4 * n_l + 4 > OUTCAP) {
+                    const unsigned long long need = 4 * n_l + 4;
+                    unsigned long long a = atomicAdd(&job.ctl->arena_used, need);
+                    tmp = a + need <= (unsigned long long)job.arena_cap ? job.arena + a : nullptr;
+                    if (!tmp) atomicOr(&job.ctl->overflow, 2ull);
+                }
+                int k = tmp ? preprocess_line(job.in + gs, (int)n_l, tmp, tmp + n_l + 1, &nl2, &eoff, ids)
+                            : E_NONE;
+                e.kind = k;
+                e.offset = eoff;
+                e.ids[0] = ids[0];
+                e.ids[1] = ids[1];
+            }
+            job.terr[t] = e;
+            __threadfence();
+            atomicMin(&job.ctl->err_key, ((s_pre_lines + (unsigned long long)ord) << 24) |
+                                             (unsigned long long)(t & 0xffffff));
+        }
+        if (!fits) continue;
+
+        // ---- emit: each thread writes the lines that start in its chunk ----
+        __syncthreads();
+        {
+            uint8_t *o_stage = S.out;
+            uint8_t *o_glob = job.out + pre_out;
+            unsigned long long w = my_out_off;
+            unsigned esc = 0;
+            const int c0 = tid * CHUNK, c1 = min(c0 + CHUNK, tile_len);
+            for (int x = c0; x < c1; ++x) {
+                if (S.win[HEAD + x - 1] != '\n') continue;
+                const int p = HEAD + x;
+                const uint8_t first = S.dec[p];
+                if (first == D_DROP) continue;
+                if (first == D_GLOBAL) {
+                    unsigned aoff = S.dec[p + 1] | (S.dec[p + 2] << 8) | (S.dec[p + 3] << 16) |
+                                    ((unsigned)S.dec[p + 4] << 24);
+                    const uint8_t *blk = job.arena + ((long long)aoff << 4);
+                    const ArenaHdr *h = reinterpret_cast<const ArenaHdr *>(blk);
+                    const long long n_pre = h->n_pre;
+                    const uint8_t *bytes = h->bytes_off < 0 ? job.in + ws + p : job.arena + h->bytes_off;
+                    const uint8_t *dec = job.arena + h->dec_off;
+                    for (long long i = 0; i < n_pre;) {
+                        uint8_t c = dec[i];
+                        if (c == D_ESC) {
+                            o_glob[w++] = 0x20;
+                            o_glob[w++] = bytes[i];
+                            ++esc;
+                            ++i;
+                        } else {
+                            o_glob[w++] = c;
+                            i += S.explen[c];
+                        }
+                    }
+                    o_glob[w++] = '\n';
+                    continue;
+                }
+                uint8_t *o = staged ? o_stage : o_glob;
+                int i = p;
+                for (;;) {
+                    uint8_t c = S.dec[i];
+                    if (c == D_END) break;
+                    if (c == D_ESC) {
+                        o[w++] = 0x20;
+                        o[w++] = S.win[i];
+                        ++esc;
+                        ++i;
+                    } else {
+                        o[w++] = c;
+                        i += S.explen[c];
+                    }
+                }
+                o[w++] = '\n';
+            }
+            if (esc) atomicAdd(&s_esc, esc);
+        }
+        __syncthreads();
+        if (staged) {
+            uint8_t *dst = job.out + pre_out;
+            for (unsigned long long k = tid; k < tile_out; k += NT) dst[k] = S.out[k];
+        }
+        if (tid == 0 && s_esc) atomicAdd(&job.ctl->escapes, (unsigned long long)s_esc);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// decompress: same skeleton; size/validate pass then table expansion.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ int decode_size(const uint8_t *r, long long n, const uint8_t *explen,
+                                           long long *m_out, long long *errpos, int *code,
+                                           unsigned *esc) {
+    long long m = 0;
+    for (long long i = 0; i < n;) {
+        unsigned b = r[i];
+        if (b == 0x20) {
+            if (i + 1 >= n) { *errpos = i; return E_TRUNC; }
+            ++m;
+            ++*esc;
+            i += 2;
+        } else {
+            unsigned L = explen[b];
+            if (!L) { *errpos = i; *code = (int)b; return E_UNKNOWN; }
+            m += L;
+            ++i;
+        }
+    }
+    *m_out = m;
+    return E_NONE;
+}
+
+__device__ __forceinline__ long long decode_fill(const uint8_t *r, long long n, const uint8_t *explen,
+                                                 const uint16_t *expoff, const uint8_t *expflat,
+                                                 uint8_t *o) {
+    long long w = 0;
+    for (long long i = 0; i < n;) {
+        unsigned b = r[i];
+        if (b == 0x20) {
+            o[w++] = r[i + 1];
+            i += 2;
+        } else {
+            unsigned L = explen[b];
+            const uint8_t *e = expflat + expoff[b];
+            for (unsigned k = 0; k < L; ++k) o[w + k] = e[k];
+            w += L;
+            ++i;
+        }
+    }
+    return w;
+}
+
+__global__ void __launch_bounds__(NT, 1) decompress_tiles(Job job, Tables tb) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ unsigned long long s_tmp64[NWARP];
+    __shared__ int s_tmp32[NWARP];
+    __shared__ long long s_tile;
+    __shared__ int s_qhead, s_err_ord, s_global;
+    __shared__ unsigned long long s_pre_out, s_pre_lines;
+    __shared__ unsigned s_kept, s_esc, s_skip;
+
+    const DSmem S = carve_dsmem(smem, tb.n_flat);
+    uint8_t *expflat = S.expflat;
+    uint16_t *expoff = S.expoff;
+    uint8_t *explen = S.explen;
+    uint8_t *win = S.win;
+    uint8_t *obuf = S.out;
+    uint16_t *queue = S.queue;
+    unsigned *chunk = S.chunk;
+    uint8_t *stat = S.stat;
+    for (int k = threadIdx.x; k < tb.n_flat; k += NT) expflat[k] = tb.exp_flat[k];
+    for (int k = threadIdx.x; k < 257; k += NT) expoff[k] = tb.exp_off[k];
+    for (int k = threadIdx.x; k < 256; k += NT) explen[k] = tb.exp_len[k];
+    const int tid = threadIdx.x;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) {
+            s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
+            s_err_ord = 0x7fffffff;
+            s_global = 0;
+            s_kept = s_esc = s_skip = 0;
+        }
+        __syncthreads();
+        const long long t = s_tile;
+        if (t >= job.n_tiles) break;
+        const long long T0 = t * (long long)TILE;
+        const int tile_len = (int)min((long long)TILE, job.n - T0);
+        const long long ws = T0 - HEAD;
+        const long long we = min(job.n, T0 + TILE + EXTRA);
+        const int win_len = (int)(we - ws);
+        const bool hits_eof = we == job.n;
+        load_window(job.in, job.n, ws, align16(win_len), win);
+        chunk[tid] = 0;
+        __syncthreads();
+
+        const int my_cnt = scan_starts(win, tile_len, 0, nullptr, 0, 0);
+        int tile_lines;
+        const int my_off = block_exscan<int>(my_cnt, s_tmp32, tile_lines);
+
+        for (int q0 = 0; q0 < tile_lines; q0 += QCAP) {
+            const int q1 = min(q0 + QCAP, tile_lines);
+            if (my_cnt) scan_starts(win, tile_len, my_off, queue, q0, q1);
+            if (tid == 0) s_qhead = 0;
+            __syncthreads();
+            for (;;) {
+                const int q = atomicAdd(&s_qhead, 1);
+                if (q >= q1 - q0) break;
+                const int ord = q0 + q;
+                const int p = queue[q];
+                int end = (q + 1 < q1 - q0) ? queue[q + 1] - 1 : find_end(win, p, win_len, hits_eof);
+                const uint8_t *r;
+                long long n_r;
+                if (end >= 0) {
+                    r = win + p;
+                    n_r = end - p;
+                } else {
+                    long long gs = ws + p, ge = gs;
+                    while (ge < job.n && job.in[ge] != '\n') ++ge;
+                    r = job.in + gs;
+                    n_r = ge - gs;
+                    s_global = 1;
+                }
+                long long m = 0, ep = -1;
+                int code = 0;
+                unsigned esc = 0;
+                int st = decode_size(r, n_r, explen, &m, &ep, &code, &esc);
+                stat[ord] = (uint8_t)st;
+                if (esc) atomicAdd(&s_esc, esc);
+                if (st == E_NONE) {
+                    atomicAdd(&chunk[(p - HEAD) / CHUNK], (unsigned)(m + 1));
+                    atomicAdd(&s_kept, 1u);
+                } else if (job.lenient) {
+                    atomicAdd(&s_skip, 1u);
+                } else {
+                    atomicMin(&s_err_ord, ord);
+                }
+            }
+            __syncthreads();
+        }
+
+        unsigned long long tile_out;
+        const unsigned long long my_out_off = block_exscan<unsigned long long>(
+            (unsigned long long)chunk[tid], s_tmp64, tile_out);
+        if (tid == 0) {
+            unsigned long long po, pl;
+            lookback(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
+            s_pre_out = po;
+            s_pre_lines = pl;
+            atomicAdd(&job.ctl->total_out, tile_out);
+            atomicAdd(&job.ctl->lines, (unsigned long long)s_kept);
+            atomicAdd(&job.ctl->in_lines, (unsigned long long)tile_lines);
+            if (s_skip) atomicAdd(&job.ctl->skipped, (unsigned long long)s_skip);
+            if (s_esc) atomicAdd(&job.ctl->escapes, (unsigned long long)s_esc);
+            if (s_pre_out + tile_out > (unsigned long long)job.out_cap)
+                atomicOr(&job.ctl->overflow, 1ull);
+        }
+        __syncthreads();
+        const unsigned long long pre_out = s_pre_out;
+        const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
+        const bool staged = fits && !s_global && tile_out <= (unsigned long long)DOUTCAP;
+
+        if (tid == 0 && s_err_ord != 0x7fffffff) {
+            int ord = s_err_ord, seen = 0, p = -1;
+            for (int x = 0; x < tile_len && p < 0; ++x)
+                if (win[HEAD + x - 1] == '\n') {
+                    if (seen == ord) p = HEAD + x;
+                    ++seen;
+                }
+            long long gs = ws + p, ge = gs;
+            while (ge < job.n && job.in[ge] != '\n') ++ge;
+            long long m = 0, ep = -1;
+            int code = 0;
+            unsigned esc = 0;
+            TileErr e;
+            e.kind = decode_size(job.in + gs, ge - gs, explen, &m, &ep, &code, &esc);
+            e.code = code;
+            e.offset = ep;
+            e.ids[0] = e.ids[1] = 0;
+            job.terr[t] = e;
+            __threadfence();
+            atomicMin(&job.ctl->err_key, ((s_pre_lines + (unsigned long long)ord) << 24) |
+                                             (unsigned long long)(t & 0xffffff));
+        }
+        if (!fits) continue;
+
+        __syncthreads();
+        {
+            unsigned long long w = my_out_off;
+            uint8_t *o = staged ? obuf : job.out + pre_out;
+            const int c0 = tid * CHUNK, c1 = min(c0 + CHUNK, tile_len);
+            int ord = my_off;
+            for (int x = c0; x < c1; ++x) {
+                if (win[HEAD + x - 1] != '\n') continue;
+                const int p = HEAD + x;
+                if (stat[ord++] != E_NONE) continue;
+                int end = find_end(win, p, win_len, hits_eof);
+                const uint8_t *r;
+                long long n_r;
+                if (end >= 0) {
+                    r = win + p;
+                    n_r = end - p;
+                } else {
+                    long long gs = ws + p, ge = gs;
+                    while (ge < job.n && job.in[ge] != '\n') ++ge;
+                    r = job.in + gs;
+                    n_r = ge - gs;
+                }
+                w += decode_fill(r, n_r, explen, expoff, expflat, o + w);
+                o[w++] = '\n';
+            }
+        }
+        __syncthreads();
+        if (staged) {
+            uint8_t *dst = job.out + pre_out;
+            for (unsigned long long k = tid; k < tile_out; k += NT) dst[k] = obuf[k];
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
+// parity-shim kernels: reference kernel layouts, one thread per line, HBM
+// ----------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(256) batch_compress(const uint8_t *flat, const long long *starts,
+                                                      long long n_lines, uint8_t *out,
+                                                      long long *out_lens, uint8_t *dec,
+                                                      unsigned long long *escapes, Tables tb) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint16_t *dfa = reinterpret_cast<uint16_t *>(smem);
+    uint8_t *codes = smem + align16(tb.n_states * NCOL * 2);
+    __shared__ uint8_t explen[256];
+    if (W) {
+        for (int k = threadIdx.x; k < tb.n_states * NCOL; k += blockDim.x) dfa[k] = tb.dfa[k];
+        for (int k = threadIdx.x; k < tb.n_states * FAST_W; k += blockDim.x) codes[k] = tb.codes[k];
+    }
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) explen[k] = tb.exp_len[k];
+    __syncthreads();
+    long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (li >= n_lines) return;
+    const long long s0 = starts[li], n = starts[li + 1] - s0;
+    const uint8_t *s = flat + s0;
+    uint8_t *d = dec + s0 + li;  // n+1 decision slots per line
+    if (n == 0) { out_lens[li] = 0; return; }
+    long long cost;
+    if constexpr (W > 0) {
+        if (n < (1ll << 24)) {
+            cost = dp_fast<W>(s, (int)n, d, dfa, codes);
+        } else {
+            long long ring[128];
+            cost = dp_generic(s, n, d, tb, ring);
+        }
+    } else {
+        long long ring[128];
+        cost = dp_generic(s, n, d, tb, ring);
+    }
+    uint8_t *o = out + 2 * s0;
+    long long w = 0;
+    unsigned esc = 0;
+    for (long long i = 0; i < n;) {
+        uint8_t c = d[i];
+        if (c == D_ESC) {
+            o[w++] = 0x20;
+            o[w++] = s[i];
+            ++esc;
+            ++i;
+        } else {
+            o[w++] = c;
+            i += explen[c];
+        }
+    }
+    out_lens[li] = cost;
+    if (esc) atomicAdd(escapes, (unsigned long long)esc);
+}
+
+__global__ void batch_decode_sizes(const uint8_t *flat, const long long *starts, long long n_lines,
+                                   long long *out_lens, int8_t *status, long long *errpos,
+                                   unsigned long long *tot, Tables tb) {
+    __shared__ uint8_t explen[256];
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) explen[k] = tb.exp_len[k];
+    __syncthreads();
+    long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (li >= n_lines) return;
+    const long long s0 = starts[li];
+    long long m = 0, ep = -1;
+    int code = 0;
+    unsigned esc = 0;
+    int st = decode_size(flat + s0, starts[li + 1] - s0, explen, &m, &ep, &code, &esc);
+    // reference status codes: 1 unknown code, 2 truncated escape
+    status[li] = (int8_t)(st == E_NONE ? 0 : (st == E_UNKNOWN ? 1 : 2));
+    errpos[li] = st == E_NONE ? -1 : ep;
+    out_lens[li] = st == E_NONE ? m : 0;
+    if (st == E_NONE && m) atomicAdd(&tot[0], (unsigned long long)m);
+    if (esc) atomicAdd(&tot[1], (unsigned long long)esc);
+}
+
+__global__ void batch_decode_fill(const uint8_t *flat, const long long *starts, long long n_lines,
+                                  const int8_t *status, uint8_t *out, const long long *out_starts,
+                                  Tables tb) {
+    __shared__ uint8_t explen[256];
+    __shared__ uint16_t expoff[257];
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) explen[k] = tb.exp_len[k];
+    for (int k = threadIdx.x; k < 257; k += blockDim.x) expoff[k] = tb.exp_off[k];
+    __syncthreads();
+    long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (li >= n_lines || status[li] != 0) return;
+    const long long s0 = starts[li];
+    decode_fill(flat + s0, starts[li + 1] - s0, explen, expoff, tb.exp_flat, out + out_starts[li]);
+}
+
+__global__ void batch_preprocess(const uint8_t *flat, const long long *starts, long long n_lines,
+                                 uint8_t *out, long long *out_lens, int8_t *status,
+                                 long long *err_off, unsigned long long *err_ids, uint8_t *marks) {
+    long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (li >= n_lines) return;
+    const long long s0 = starts[li], n = starts[li + 1] - s0;
+    uint8_t *o = out + 3 * s0 + 3 * li;
+    int nl2 = 0, eoff = -1;
+    unsigned long long ids[2] = {0, 0};
+    int k = preprocess_line(flat + s0, (int)n, marks + s0 + li, o, &nl2, &eoff, ids, false);
+    status[li] = (int8_t)k;
+    out_lens[li] = k == E_NONE ? nl2 : 0;
+    err_off[li] = eoff;
+    err_ids[2 * li] = ids[0];
+    err_ids[2 * li + 1] = ids[1];
+}
+
+}  // namespace zs

@@ -1,0 +1,132 @@
+"""Whole-file compression / decompression (reference pipeline.py:129-167).
+
+``run_stream`` hands the whole newline-framed buffer to libzs in one call
+(zs_compress_host / zs_decompress_host): framing, the CR policy, ring
+renumbering, the parse, strict/lenient handling and the stats are all
+computed on the GPU in the fused tile kernels.  Output bytes are identical
+to the reference for any ``workers`` / ``batch_lines`` (both accepted for
+API compatibility; the GPU does not batch by lines).
+
+Strict-mode errors: like the reference, the batches before the failing
+line's ``batch_lines`` batch are written to ``dst`` before ``LineError``
+is raised (pipeline.py:154-161 writes batches in order as they finish).
+"""
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import LineError, from_kind
+
+BATCH_LINES = 4096
+
+
+@dataclass
+class CorpusStats:
+    lines: int = 0
+    input_bytes: int = 0
+    output_bytes: int = 0
+    escapes: int = 0
+    skipped: int = 0
+    flagged: int = 0
+    elapsed: float = 0.0
+
+    @property
+    def ratio(self) -> float:
+        return 1.0 if self.input_bytes == 0 else self.output_bytes / self.input_bytes
+
+    def format_line(self) -> str:
+        return (f"lines={self.lines} in_bytes={self.input_bytes} "
+                f"out_bytes={self.output_bytes} ratio={self.ratio:.6f} "
+                f"escapes={self.escapes} elapsed_ms={int(round(self.elapsed * 1000))}")
+
+
+def compute_ratio(stats: CorpusStats) -> float:
+    """Output over input bytes (newlines included); 1.0 for empty input."""
+    return stats.ratio
+
+
+def _read_all(src) -> bytes:
+    parts = []
+    while True:
+        chunk = src.read(64 << 20)
+        if not chunk:
+            break
+        parts.append(chunk)
+    return b"".join(parts)
+
+
+def run_buffer(buf, d, direction="compress", *, preprocess=False, lenient=False, device=None):
+    """One newline-framed buffer through the GPU.  Returns (output bytes,
+    zs_result).  `buf` may be bytes or a uint8 numpy array (pinned memory
+    gives full PCIe rate)."""
+    if direction not in ("compress", "decompress"):
+        raise ValueError(f"bad direction {direction!r}")
+    arr = buf if isinstance(buf, np.ndarray) else np.frombuffer(buf, np.uint8)
+    ctx = _lib.context(device)
+    flags = (_lib.F_PREPROCESS if preprocess else 0) | (_lib.F_LENIENT if lenient else 0)
+    res = _lib.Result()
+    n = arr.size
+    with ctx.lock:
+        ctx.set_dictionary(d)
+        if direction == "compress":
+            cap = ctx.lib.zs_compress_bound(n)
+            fn = ctx.lib.zs_compress_host
+        else:
+            cap = max(4 * n + 64, 1024)
+            fn = ctx.lib.zs_decompress_host
+        for _ in range(3):
+            out = np.empty(cap, np.uint8)
+            rc = fn(ctx.h, _lib.ptr(arr), n, _lib.ptr(out), cap, flags, res)
+            if rc == _lib.ZS_E_CAPACITY:
+                cap = res.out_bytes + 64
+                continue
+            ctx.check(rc, "zs_compress_host" if direction == "compress" else "zs_decompress_host")
+            break
+    return out[:res.out_bytes], res
+
+
+def run_stream(src, dst, d, direction="compress", *, preprocess=False, lenient=False, workers=1,
+               batch_lines=BATCH_LINES, device=None) -> CorpusStats:
+    """Stream src to dst through the GPU codec; returns exact corpus totals.
+
+    Strict mode raises LineError (1-based) for the first bad line; lenient
+    mode drops undecodable / carriage-return lines (``skipped``) and keeps
+    unpreprocessable ones raw (``flagged``)."""
+    if direction not in ("compress", "decompress"):
+        raise ValueError(f"bad direction {direction!r}")
+    t0 = time.perf_counter()
+    data = _read_all(src)
+    out, res = run_buffer(data, d, direction, preprocess=preprocess, lenient=lenient,
+                          device=device)
+    if res.err_line:
+        cause = from_kind(res.err_kind, res.err_offset, tuple(res.err_ids), res.err_code)
+        _write_partial(dst, data, d, direction, preprocess, lenient, res.err_line, batch_lines,
+                       device)
+        raise LineError(int(res.err_line), cause)
+    if out.size:
+        dst.write(out.tobytes())
+    st = CorpusStats(lines=res.lines, input_bytes=len(data), output_bytes=int(res.out_bytes),
+                     escapes=res.escapes, skipped=res.skipped, flagged=res.flagged)
+    st.elapsed = time.perf_counter() - t0
+    return st
+
+
+def _write_partial(dst, data, d, direction, preprocess, lenient, err_line, batch_lines, device):
+    """Reference behaviour on a strict error: every complete batch before the
+    failing line's batch has already been written (no trailing newline)."""
+    keep = ((err_line - 1) // max(1, batch_lines)) * max(1, batch_lines)
+    if keep <= 0:
+        return
+    arr = np.frombuffer(data, np.uint8)
+    nl = np.flatnonzero(arr == 0x0A)
+    end = int(nl[keep - 1]) + 1
+    out, _ = run_buffer(arr[:end], d, direction, preprocess=preprocess, lenient=lenient,
+                        device=device)
+    blob = out.tobytes()
+    if blob.endswith(b"\n"):
+        blob = blob[:-1]
+    if blob:
+        dst.write(blob)

@@ -1,0 +1,335 @@
+"""GPU parity: the sm_100a path vs the reference's own outputs (golden
+fixtures) and vs the CPU oracle, through the C ABI.  Bit-exact throughout."""
+
+import hashlib
+import io
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from conftest import golden_dict_bytes, has_gpu
+
+pytestmark = pytest.mark.gpu
+
+if has_gpu():
+    import paper_2404_19391_b200 as z
+    from paper_2404_19391_b200 import _lib, kernels
+
+
+def dict_from_json(dj):
+    learned = [bytes.fromhex(p) for p in dj["learned"]]
+    ident = bytes.fromhex(dj["identity"])
+    if dj["prepopulate"] is not None:
+        return z.Dictionary(learned, dj["prepopulate"], l_min=dj["l_min"], l_max=dj["l_max"])
+    return z.Dictionary(learned, None, l_min=dj["l_min"], l_max=dj["l_max"], identity=ident)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _ready():
+    if not has_gpu():
+        pytest.skip("no GPU")
+    oracle.build()
+    synth.build()
+
+
+# ---------------------------------------------------------------- shim paths
+
+def test_compress_lines_golden(codec_cases):
+    for c in codec_cases:
+        d = dict_from_json(c["dict"])
+        recs, esc = z.compress_lines(d, [bytes.fromhex(l) for l in c["lines"]])
+        assert [r.hex() for r in recs] == c["records"]
+        assert esc == c["escapes"]
+
+
+def test_kernel_seam_harness_golden(codec_cases, decode_cases):
+    """The reference's kernel harness shape (test_kernels.py:18-48) against
+    kernels.compress_batch / decompress_sizes / decompress_fill."""
+    for c in codec_cases[:12]:
+        d = dict_from_json(c["dict"])
+        lines = [bytes.fromhex(l) for l in c["lines"]]
+        flat = np.frombuffer(b"".join(lines) or b"\0", np.uint8)
+        starts = np.zeros(len(lines) + 1, np.int64)
+        np.cumsum([len(l) for l in lines], out=starts[1:])
+        out = np.zeros(2 * int(starts[-1]) + 1, np.uint8)
+        lens = np.empty(len(lines), np.int64)
+        esc = kernels.compress_batch(d.encode_trie.children, d.encode_trie.term_code, flat, starts,
+                                     out, lens)
+        recs = [out[2 * starts[i]:2 * starts[i] + lens[i]].tobytes().hex() for i in range(len(lines))]
+        assert recs == c["records"] and esc == c["escapes"]
+    for c in decode_cases:
+        d = dict_from_json(c["dict"])
+        recs = [bytes.fromhex(r) for r in c["records"]]
+        exp_len, valid, exp_off, exp_flat = d.decode_tables
+        flat = np.frombuffer(b"".join(recs) or b"\0", np.uint8)
+        starts = np.zeros(len(recs) + 1, np.int64)
+        np.cumsum([len(r) for r in recs], out=starts[1:])
+        n = len(recs)
+        lens, st, ep = np.empty(n, np.int64), np.empty(n, np.int8), np.empty(n, np.int64)
+        total, esc = kernels.decompress_sizes(exp_len, valid, flat, starts, lens, st, ep)
+        assert lens.tolist() == c["out_lens"] and st.tolist() == c["status"]
+        assert ep.tolist() == c["errpos"] and (total, esc) == (c["total"], c["escapes"])
+        ost = np.zeros(n + 1, np.int64)
+        np.cumsum(lens, out=ost[1:])
+        out = np.zeros(total + 1, np.uint8)
+        kernels.decompress_fill(exp_off, exp_flat, flat, starts, st, out, ost)
+        assert out[:total].tobytes().hex() == c["out"]
+
+
+def test_decompress_lines_golden(decode_cases):
+    for c in decode_cases:
+        d = dict_from_json(c["dict"])
+        recs = [bytes.fromhex(r) for r in c["records"]]
+        lines, errors, esc = z.decompress_lines(d, recs)
+        assert esc == c["escapes"]
+        got = b"".join(l for l in lines if l is not None)
+        assert got.hex() == c["out"]
+        bad = {i for i, s in enumerate(c["status"]) if s}
+        assert {i for i, _ in errors} == bad
+        for i, e in errors:
+            want = z.UnknownCode if c["status"][i] == 1 else z.TruncatedEscape
+            assert isinstance(e, want) and e.offset == c["errpos"][i]
+
+
+def test_decode_error_kats():
+    d = z.Dictionary([b"CC"], "none")
+    with pytest.raises(z.UnknownCode) as ei:
+        z.decompress_line(d, bytes([0x80, 0x99]))
+    assert (ei.value.code, ei.value.offset) == (0x99, 1)
+    with pytest.raises(z.TruncatedEscape) as ei:
+        z.decompress_line(z.Dictionary([], "smiles"), bytes([ord("C"), 0x20]))
+    assert ei.value.offset == 1
+    assert z.compress_line(z.Dictionary([b"CC", b"CCC"], None, identity=b"C"), b"CCCC") == \
+        bytes([0x81, ord("C")])
+
+
+def test_preprocess_golden(preprocess_cases):
+    lines = [bytes.fromhex(c["line"]) for c in preprocess_cases]
+    res = z.preprocess_batch(lines)
+    for c, line, (kind, val) in zip(preprocess_cases, lines, res):
+        s = c["strict"]
+        if kind == 0:
+            assert s.get("out") == val.hex(), c
+        else:
+            e = z.errors.from_kind(kind, val[0], val[1])
+            assert (type(e).__name__, str(e)) == (s["err"], s["msg"]), c
+    for c in preprocess_cases[::7]:
+        line = bytes.fromhex(c["line"])
+        for mode in ("strict", "lenient"):
+            want = c[mode]
+            try:
+                got = {"out": z.preprocess_line(line, mode).hex()}
+            except z.ZsmilesError as e:
+                got = {"err": type(e).__name__, "msg": str(e)}
+            assert got == want, (line, mode)
+
+
+# ---------------------------------------------------------------- whole-buffer path
+
+def test_run_stream_golden(stream_cases):
+    dicts = [dict_from_json(dj) for dj in stream_cases["dicts"]]
+    for c in stream_cases["cases"]:
+        dst = io.BytesIO()
+        kw = dict(preprocess=c["preprocess"], lenient=c["lenient"])
+        if "err" in c:
+            with pytest.raises(z.LineError) as ei:
+                z.run_stream(io.BytesIO(bytes.fromhex(c["payload"])), dst, dicts[c["dict"]],
+                             c["direction"], **kw)
+            assert ei.value.line_no == c["line_no"]
+            assert type(ei.value.cause).__name__ == c["cause"]
+            assert str(ei.value) == c["msg"]
+        else:
+            st = z.run_stream(io.BytesIO(bytes.fromhex(c["payload"])), dst, dicts[c["dict"]],
+                              c["direction"], **kw)
+            assert dst.getvalue().hex() == c["out"], c
+            assert (st.lines, st.input_bytes, st.output_bytes, st.escapes, st.skipped,
+                    st.flagged) == (c["lines"], c["in_bytes"], c["out_bytes"], c["escapes"],
+                                    c["skipped"], c["flagged"])
+
+
+def test_whole_buffer_random_dictionaries(codec_cases):
+    """Fused tile kernels (fast DFA and generic trie) vs the oracle stream on
+    the golden random dictionaries, with escape-heavy bytes."""
+    rng = random.Random(5)
+    n_fast = 0
+    for c in codec_cases:
+        d = dict_from_json(c["dict"])
+        lines = [bytes.fromhex(l) for l in c["lines"]]
+        lines = [l.replace(b"\n", b"").replace(b"\r", b"") for l in lines]
+        rng.shuffle(lines)
+        payload = b"\n".join(lines * 3) + b"\n"
+        t = oracle.Tables(d.learned, bytes(sorted(d.identity)))
+        for pre in (False, True):
+            comp, res = z.run_buffer(payload, d, "compress", preprocess=pre, lenient=True)
+            want, st = oracle.run_stream(t, payload, "compress", pre, True, 1)
+            assert comp.tobytes() == want
+            assert (res.lines, res.escapes, res.flagged) == (st["lines"], st["escapes"], st["flagged"])
+            back, _ = z.run_buffer(want, d, "decompress", lenient=True)
+            want_back, _ = oracle.run_stream(t, want, "decompress", False, True, 1)
+            assert back.tobytes() == want_back
+        n_fast += _lib.context().fast_width() > 0
+    assert n_fast >= 10
+
+
+@pytest.mark.parametrize("name", ["aromatic_10k", "aliphatic_10k", "mixed_50k", "c1_100k",
+                                  "c3_skewed_20k"])
+def test_corpus_hashes(corpus_hashes, name):
+    e = corpus_hashes[name]
+    buf = synth.generate(e["kind"], e["lines"], e["seed"])
+    d = z.deserialize(golden_dict_bytes(e["dict"]))
+    for key, pre in (("pre_off", False), ("pre_on", True)):
+        comp, res = z.run_buffer(buf, d, "compress", preprocess=pre, lenient=True)
+        assert hashlib.sha256(comp.tobytes()).hexdigest() == e[key]["comp_sha256"]
+        assert res.out_bytes == e[key]["out_bytes"] and res.escapes == e[key]["escapes"]
+        back, _ = z.run_buffer(comp, d, "decompress")
+        assert hashlib.sha256(back.tobytes()).hexdigest() == e[key]["roundtrip_sha256"]
+
+
+def test_ablation_dictionaries(corpus_hashes):
+    e0 = corpus_hashes["c1_100k"]
+    buf = synth.generate(e0["kind"], e0["lines"], e0["seed"])
+    for name, e in corpus_hashes.items():
+        if not name.startswith("c4_"):
+            continue
+        d = z.deserialize(golden_dict_bytes(e["dict"]))
+        for key, pre in (("pre_off", False), ("pre_on", True)):
+            comp, _ = z.run_buffer(buf, d, "compress", preprocess=pre, lenient=True)
+            assert hashlib.sha256(comp.tobytes()).hexdigest() == e[key]["comp_sha256"], (name, key)
+            back, _ = z.run_buffer(comp, d, "decompress")
+            assert hashlib.sha256(back.tobytes()).hexdigest() == e[key]["roundtrip_sha256"]
+
+
+@pytest.mark.parametrize("name", ["c2_10m", "c3_skewed_1m"])
+def test_full_size_hashes(corpus_hashes, name):
+    """BASELINE configs at full size (10M lines; 1M skewed lines), host API
+    (multi-chunk pipeline) and device API."""
+    import torch
+    e = corpus_hashes[name]
+    buf = synth.generate(e["kind"], e["lines"], e["seed"])
+    d = z.default_dictionary()
+    for key, pre in (("pre_off", False), ("pre_on", True)):
+        comp, res = z.run_buffer(buf, d, "compress", preprocess=pre, lenient=True)
+        assert hashlib.sha256(comp.tobytes()).hexdigest() == e[key]["comp_sha256"], key
+        back, _ = z.run_buffer(comp, d, "decompress")
+        assert hashlib.sha256(back.tobytes()).hexdigest() == e[key]["roundtrip_sha256"], key
+    # device API on HBM-resident buffers
+    ctx = _lib.context()
+    din = torch.from_numpy(buf).cuda()
+    dout = torch.empty(2 * buf.size + 64, dtype=torch.uint8, device="cuda")
+    r = _lib.Result()
+    with ctx.lock:
+        ctx.set_dictionary(d)
+        rc = ctx.lib.zs_compress_device(ctx.h, din.data_ptr(), buf.size, dout.data_ptr(),
+                                        dout.numel(), _lib.F_PREPROCESS | _lib.F_LENIENT, r)
+        ctx.check(rc, "zs_compress_device")
+    got = dout[:r.out_bytes].cpu().numpy().tobytes()
+    assert hashlib.sha256(got).hexdigest() == e["pre_on"]["comp_sha256"]
+
+
+# ---------------------------------------------------------------- edge cases
+
+def _oracle_check(payload, d, pre, lenient, direction="compress"):
+    t = oracle.Tables(d.learned, bytes(sorted(d.identity)))
+    want, st = oracle.run_stream(t, payload, direction, pre, lenient, 1)
+    if st["err_line"]:
+        with pytest.raises(z.LineError) as ei:
+            z.run_stream(io.BytesIO(payload), io.BytesIO(), d, direction, preprocess=pre,
+                         lenient=lenient)
+        assert ei.value.line_no == st["err_line"]
+        return None
+    got, res = z.run_buffer(payload, d, direction, preprocess=pre, lenient=lenient)
+    assert got.tobytes() == want
+    assert (res.lines, res.escapes, res.skipped, res.flagged) == \
+        (st["lines"], st["escapes"], st["skipped"], st["flagged"])
+    return want
+
+
+def test_long_lines_global_path():
+    """Lines longer than the smem window take the HBM-arena path."""
+    d = z.default_dictionary()
+    rng = random.Random(9)
+    mols = synth.generate("mixed", 20000, 7).tobytes().split(b"\n")[:-1]
+    for L in (3000, 5000, 40000, 300000):
+        parts, n = [], 0
+        while n < L:
+            m = rng.choice(mols)
+            parts.append(m)
+            n += len(m) + 1
+        long_line = b"C".join(parts)
+        payload = b"\n".join(mols[:300]) + b"\n" + long_line + b"\n" + b"\n".join(mols[300:600]) + b"\n"
+        for pre in (False, True):
+            _oracle_check(payload, d, pre, True)
+        back_in = _oracle_check(payload, d, True, False)
+        if back_in is not None:
+            _oracle_check(back_in, d, False, False, "decompress")
+
+
+def test_growing_renumbering_line():
+    """A 1-byte ring id that must take a colour >= 10 grows the line."""
+    d = z.default_dictionary()
+    ids = [str(i) for i in range(1, 10)] + [f"%{i:02d}" for i in range(10, 25)]
+    grow = ("C" + "C".join(ids[::-1]) + "C" + "C".join(ids) + "C").encode()
+    grow2 = ("C1" + "".join(f"C%{i:02d}" for i in range(10, 22)) + "C" +
+             "".join(f"C%{i:02d}" for i in range(21, 9, -1)) + "C1").encode()
+    payload = b"CCO\n" + grow + b"\n" + grow2 + b"\nc1ccccc1\n" + grow2
+    for lenient in (False, True):
+        _oracle_check(payload, d, True, lenient)
+
+
+def test_many_tiny_lines_multiple_rounds():
+    d = z.Dictionary([b"CC"], "smiles")
+    payload = b"\n" * 70000 + b"C\n" * 30000 + b"CC\nC\n" * 20000
+    for pre in (False, True):
+        want = _oracle_check(payload, d, pre, False)
+        _oracle_check(want, d, False, False, "decompress")
+
+
+def test_errors_across_tiles():
+    d = z.default_dictionary()
+    base = synth.generate("aromatic", 30000, 11).tobytes().split(b"\n")[:-1]
+    for bad_at, bad in ((0, b"C1CC"), (777, b"C[NH"), (20000, b"CC\rO"), (29999, b"C%1")):
+        lines = list(base)
+        lines[bad_at] = bad
+        payload = b"\n".join(lines) + b"\n"
+        for lenient in (False, True):
+            _oracle_check(payload, d, True, lenient)
+            _oracle_check(payload, d, False, lenient)
+    comp, _ = z.run_buffer(b"\n".join(base) + b"\n", d, "compress")
+    recs = comp.tobytes().split(b"\n")
+    recs[12345] = b"\x05\x80"
+    recs[23456] = b"CC "
+    _oracle_check(b"\n".join(recs), d, False, True, "decompress")
+    _oracle_check(b"\n".join(recs), d, False, False, "decompress")
+
+
+def test_strict_partial_output_matches_reference_batches():
+    d = z.Dictionary([], "smiles")
+    lines = [b"CCO"] * 300 + [b"C1CC"] + [b"CCO"] * 50
+    dst = io.BytesIO()
+    with pytest.raises(z.LineError) as ei:
+        z.run_stream(io.BytesIO(b"\n".join(lines) + b"\n"), dst, d, "compress",
+                     preprocess=True, batch_lines=32)
+    assert ei.value.line_no == 301
+    assert dst.getvalue() == b"\n".join([b"CCO"] * 288)
+
+
+def test_device_and_host_api_agree():
+    import torch
+    d = z.default_dictionary()
+    buf = synth.generate("mixed", 200000, 3)
+    comp, res = z.run_buffer(buf, d, "compress", preprocess=True)
+    ctx = _lib.context()
+    din = torch.from_numpy(buf).cuda()
+    dout = torch.empty(2 * buf.size + 64, dtype=torch.uint8, device="cuda")
+    r = _lib.Result()
+    with ctx.lock:
+        ctx.set_dictionary(d)
+        rc = ctx.lib.zs_compress_device(ctx.h, din.data_ptr(), buf.size, dout.data_ptr(),
+                                        dout.numel(), _lib.F_PREPROCESS, r)
+        ctx.check(rc, "zs_compress_device")
+        assert ctx.last_kernel_ms() > 0
+    assert dout[:r.out_bytes].cpu().numpy().tobytes() == comp.tobytes()
+    assert (r.lines, r.out_bytes) == (res.lines, res.out_bytes)
