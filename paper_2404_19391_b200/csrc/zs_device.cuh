@@ -54,7 +54,7 @@ constexpr uint8_t D_DROP = 0x0D;  // line dropped (lenient CR) or strict error
 constexpr uint8_t D_GLOBAL = 0x0B;  // line processed in the HBM arena
 
 // tile flags for the look-back
-constexpr unsigned F_AGG = 1u, F_INC = 2u;
+enum : unsigned { F_AGG = 1u, F_INC = 2u };
 
 enum ErrKind {
     E_NONE = 0, E_CR = 1, E_BRACKET = 2, E_PERCENT = 3, E_UNPAIRED = 4, E_OVERFLOW = 5,
@@ -177,47 +177,71 @@ __device__ __forceinline__ T block_exscan(T v, T *warp_tmp, T &total) {
 }
 
 // ----------------------------------------------------------------------------
-// decoupled look-back over tiles (ordered tickets guarantee progress)
+// decoupled look-back over tiles, one warp (ordered tickets guarantee
+// progress).  Lanes inspect 32 predecessors per round trip: the nearest one
+// with an inclusive prefix ends the walk, the aggregates before it are summed
+// with a warp reduction.  Must be called by all 32 lanes of one warp.
 // ----------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 __device__ __forceinline__ void lookback(TileState *ts, long long t, unsigned long long agg_out,
                                          unsigned long long agg_lines,
                                          unsigned long long &pre_out,
                                          unsigned long long &pre_lines) {
     volatile TileState *vts = ts;
+    const int lane = threadIdx.x & 31;
     if (t == 0) {
-        vts[0].inc_out = agg_out;
-        vts[0].inc_lines = agg_lines;
-        __threadfence();
-        atomicExch(&ts[0].flag, F_INC);
+        if (lane == 0) {
+            vts[0].inc_out = agg_out;
+            vts[0].inc_lines = agg_lines;
+            __threadfence();
+            atomicExch(&ts[0].flag, F_INC);
+        }
         pre_out = 0;
         pre_lines = 0;
         return;
     }
-    vts[t].agg_out = agg_out;
-    vts[t].agg_lines = agg_lines;
-    __threadfence();
-    atomicExch(&ts[t].flag, F_AGG);
+    if (lane == 0) {
+        vts[t].agg_out = agg_out;
+        vts[t].agg_lines = agg_lines;
+        __threadfence();
+        atomicExch(&ts[t].flag, F_AGG);
+    }
     unsigned long long po = 0, pl = 0;
     long long j = t - 1;
-    while (true) {
-        unsigned f;
-        do {
-            f = vts[j].flag;
-        } while (f == 0);
+    for (;;) {
+        const long long idx = j - lane;
+        unsigned f = idx >= 0 ? vts[idx].flag : F_INC;
+        while (__any_sync(0xffffffffu, f == 0u))
+            if (f == 0u) f = vts[idx].flag;
         __threadfence();
-        if (f == F_INC) {
-            po += vts[j].inc_out;
-            pl += vts[j].inc_lines;
-            break;
+        const unsigned inc = __ballot_sync(0xffffffffu, f == F_INC);
+        const int stop = inc ? __ffs(inc) - 1 : 32;  // lanes < stop: AGG; lane == stop: INC
+        unsigned long long vo = 0, vl = 0;
+        if (idx >= 0 && lane <= stop) {
+            if (lane == stop) {
+                vo = vts[idx].inc_out;
+                vl = vts[idx].inc_lines;
+            } else {
+                vo = vts[idx].agg_out;
+                vl = vts[idx].agg_lines;
+            }
         }
-        po += vts[j].agg_out;
-        pl += vts[j].agg_lines;
-        --j;
+        po += warp_sum(vo);
+        pl += warp_sum(vl);
+        if (inc) break;
+        j -= 32;
     }
-    vts[t].inc_out = po + agg_out;
-    vts[t].inc_lines = pl + agg_lines;
-    __threadfence();
-    atomicExch(&ts[t].flag, F_INC);
+    if (lane == 0) {
+        vts[t].inc_out = po + agg_out;
+        vts[t].inc_lines = pl + agg_lines;
+        __threadfence();
+        atomicExch(&ts[t].flag, F_INC);
+    }
     pre_out = po;
     pre_lines = pl;
 }
@@ -357,6 +381,112 @@ __device__ int preprocess_line(const uint8_t *buf, int n, uint8_t *marks, uint8_
         }
     }
     *new_len = w;
+    return E_NONE;
+}
+
+// ----------------------------------------------------------------------------
+// ring renumbering, fast path (the common case, one byte per loop trip).
+//
+// Same semantics as preprocess_line, restricted to lines whose ring tokens
+// are single digits, with at most 4 rings open at once and colours < 8 (so
+// every token keeps its width and the rewrite is in place at close time).
+// Open rings live in 4 register slots (id, position); the smallest free
+// colour is found from lc[k] = position where colour k last closed: colour k
+// is taken by a ring closed inside (o, c) iff lc[k] > o.  Anything else
+// returns RN_FALLBACK and the caller re-runs the line through
+// preprocess_line on pristine bytes.  On any return other than E_NONE the
+// line bytes may be partially rewritten (callers restore them from HBM).
+// ----------------------------------------------------------------------------
+constexpr int RN_FALLBACK = -4;
+enum : uint8_t { K_OKP = 1, K_DIG = 2, K_PCT = 4, K_LBR = 8, K_CR = 16 };
+
+__device__ __forceinline__ uint8_t tok_bits(unsigned b) {
+    uint8_t c = tok_class(b);
+    return c == C_ATOM || c == C_BOND ? K_OKP : c == C_DIGIT ? K_DIG : c == C_PCT ? K_PCT
+         : c == C_LBR ? K_LBR : c == C_CR ? K_CR : 0;
+}
+
+__device__ __forceinline__ int renumber_fast(uint8_t *s, int n, const uint8_t *lut, int *err_off,
+                                             unsigned long long ids[2]) {
+    unsigned oid = 0xffffffffu;  // 4 slots: open ring id per byte, 0xff = free
+    int opos[4] = {0, 0, 0, 0};
+    int lc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) lc[k] = -1;
+    bool ring_ok = false, in_br = false;
+    int br = 0;
+    for (int i = 0; i < n; ++i) {
+        const unsigned b = s[i];
+        const unsigned c = lut[b];
+        if (in_br) {
+            if (b == ']') { in_br = false; ring_ok = true; }
+            else if (c & K_CR) return E_CR;
+            continue;
+        }
+        if (!(c & (K_DIG | K_PCT | K_LBR | K_CR))) {
+            ring_ok = c & K_OKP;
+            continue;
+        }
+        if (c & K_LBR) { in_br = true; br = i; continue; }
+        if (c & K_CR) return E_CR;
+        if (c & K_PCT) {
+            if (i + 2 >= n || !is_digit(s[i + 1]) || !is_digit(s[i + 2])) {
+                for (int k = i; k < n; ++k)
+                    if (s[k] == '\r') return E_CR;
+                *err_off = i;
+                return E_PERCENT;
+            }
+            if (ring_ok) return RN_FALLBACK;  // %nn ring id: width may change
+            i += 2;                           // '%nn' as an Other token
+            continue;
+        }
+        if (!ring_ok) continue;  // digit after a non-atom: Other, ring_ok stays false
+        const unsigned rid = b - '0';
+        int slot = -1, free_slot = -1;
+#pragma unroll
+        for (int k = 3; k >= 0; --k) {
+            const unsigned v = (oid >> (8 * k)) & 0xffu;
+            if (v == rid) slot = k;
+            if (v == 0xffu) free_slot = k;
+        }
+        if (slot < 0) {
+            if (free_slot < 0) return RN_FALLBACK;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k == free_slot) opos[k] = i;
+            oid = (oid & ~(0xffu << (8 * free_slot))) | (rid << (8 * free_slot));
+        } else {
+            int o = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k == slot) o = opos[k];
+            oid |= 0xffu << (8 * slot);
+            int col = 8;
+#pragma unroll
+            for (int k = 7; k >= 0; --k)
+                if (lc[k] <= o) col = k;
+            if (col == 8) return RN_FALLBACK;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k == col) lc[k] = i;
+            s[o] = (uint8_t)('0' + col);
+            s[i] = (uint8_t)('0' + col);
+        }
+        ring_ok = true;
+    }
+    if (in_br) {
+        *err_off = br;
+        return E_BRACKET;
+    }
+    if (oid != 0xffffffffu) {
+        ids[0] = ids[1] = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned v = (oid >> (8 * k)) & 0xffu;
+            if (v != 0xffu) ids[0] |= 1ull << v;
+        }
+        return E_UNPAIRED;
+    }
     return E_NONE;
 }
 

@@ -15,15 +15,51 @@ struct CSmem {
     uint8_t *win;
     uint8_t *dec;
     uint8_t *out;
-    uint16_t *queue;
-    unsigned *chunk;
+    uint16_t *queue;  // line starts (window offsets) of the current round
+    uint16_t *qlen;   // their lengths (0xffff = runs past the window)
+    uint16_t *qsort;  // queue indices sorted by length, longest first
+    unsigned *chunk;  // per-thread-chunk output byte sums
 };
 
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
 __host__ __device__ inline int compress_smem_bytes(int n_states) {
     return align16(n_states * NCOL * 2) + align16(n_states * FAST_W) + 256 + align16(WIN + 16) +
-           align16(WIN + 16) + align16(OUTCAP) + QCAP * 2 + NT * 4;
+           align16(WIN + 16) + align16(OUTCAP) + 3 * QCAP * 2 + NT * 4;
+}
+
+__device__ inline CSmem carve_csmem(uint8_t *p, int ns) {
+    CSmem S;
+    S.dfa = reinterpret_cast<uint16_t *>(p); p += align16(ns * NCOL * 2);
+    S.codes = p; p += align16(ns * FAST_W);
+    S.explen = p; p += 256;
+    S.win = p; p += align16(WIN + 16);
+    S.dec = p; p += align16(WIN + 16);
+    S.out = p; p += align16(OUTCAP);
+    S.queue = reinterpret_cast<uint16_t *>(p); p += QCAP * 2;
+    S.qlen = reinterpret_cast<uint16_t *>(p); p += QCAP * 2;
+    S.qsort = reinterpret_cast<uint16_t *>(p); p += QCAP * 2;
+    S.chunk = reinterpret_cast<unsigned *>(p);
+    return S;
+}
+
+// Copy the staged tile output to HBM: byte stores until dst is 16-byte
+// aligned, then 16-byte vector stores assembled from smem bytes.
+__device__ __forceinline__ void store_out(uint8_t *dst, const uint8_t *src, int len) {
+    const int head = min(len, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
+    if ((int)threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
+    const int nvec = (len - head) >> 4;
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst + head);
+    for (int k = threadIdx.x; k < nvec; k += NT) {
+        const uint8_t *q = src + head + 16 * k;
+        uint4 v;
+        v.x = q[0] | (q[1] << 8) | (q[2] << 16) | ((unsigned)q[3] << 24);
+        v.y = q[4] | (q[5] << 8) | (q[6] << 16) | ((unsigned)q[7] << 24);
+        v.z = q[8] | (q[9] << 8) | (q[10] << 16) | ((unsigned)q[11] << 24);
+        v.w = q[12] | (q[13] << 8) | (q[14] << 16) | ((unsigned)q[15] << 24);
+        d4[k] = v;
+    }
+    for (int k = head + (nvec << 4) + threadIdx.x; k < len; k += NT) dst[k] = src[k];
 }
 
 struct DSmem {
@@ -157,6 +193,71 @@ __device__ long long compress_line_global(const Job &job, const Tables &tb, long
 }
 
 // ----------------------------------------------------------------------------
+// compress emit: one thread walks the positions of its CHUNK in a single flat
+// loop (uniform trip structure across the warp).  At a line start the walk
+// arms `nxt` at the line's first decision; every position equal to `nxt`
+// emits its code (or escape + literal) and advances nxt by the code length;
+// D_END emits the record separator.  Lines that started in the chunk are
+// finished past the chunk end.
+// ----------------------------------------------------------------------------
+template <bool STAGED>
+__device__ __forceinline__ unsigned emit_chunk(const Job &job, const CSmem &S, long long ws,
+                                               int tile_len, unsigned long long w, uint8_t *o) {
+    const int c0 = threadIdx.x * CHUNK;
+    const int c1 = min(c0 + CHUNK, tile_len);
+    unsigned esc = 0;
+    int nxt = -1;
+    for (int x = c0; x < c1 || nxt >= 0; ++x) {
+        const int p = HEAD + x;
+        if (x < c1 && S.win[p - 1] == '\n') {
+            const uint8_t first = S.dec[p];
+            if (first == D_GLOBAL) {
+                // out-of-smem line: its decisions live in the HBM arena
+                const unsigned aoff = S.dec[p + 1] | (S.dec[p + 2] << 8) | (S.dec[p + 3] << 16) |
+                                      ((unsigned)S.dec[p + 4] << 24);
+                const uint8_t *blk = job.arena + ((long long)aoff << 4);
+                const ArenaHdr *h = reinterpret_cast<const ArenaHdr *>(blk);
+                const uint8_t *bytes = h->bytes_off < 0 ? job.in + ws + p : job.arena + h->bytes_off;
+                const uint8_t *dec = job.arena + h->dec_off;
+                uint8_t *og = job.out;  // direct mode is forced for such tiles
+                for (long long i = 0; i < h->n_pre;) {
+                    const uint8_t c = dec[i];
+                    if (c == D_ESC) {
+                        og[w++] = 0x20;
+                        og[w++] = bytes[i];
+                        ++esc;
+                        ++i;
+                    } else {
+                        og[w++] = c;
+                        i += S.explen[c];
+                    }
+                }
+                og[w++] = '\n';
+                nxt = -1;
+                continue;
+            }
+            nxt = first == D_DROP ? -1 : p;
+        }
+        if (p == nxt) {
+            const uint8_t c = S.dec[p];
+            if (c == D_END) {
+                o[w++] = '\n';
+                nxt = -1;
+            } else if (c == D_ESC) {
+                o[w++] = 0x20;
+                o[w++] = S.win[p];
+                ++esc;
+                ++nxt;
+            } else {
+                o[w++] = c;
+                nxt += S.explen[c];
+            }
+        }
+    }
+    return esc;
+}
+
+// ----------------------------------------------------------------------------
 // compress: one persistent CTA per SM, tiles in ticket order.
 // W = fast-path window (max pattern length) or 0 for the generic trie walk.
 // ----------------------------------------------------------------------------
@@ -165,31 +266,26 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ unsigned long long s_tmp64[NWARP];
     __shared__ int s_tmp32[NWARP];
+    __shared__ unsigned s_hist[256];
+    __shared__ uint8_t s_lut[256];
     __shared__ long long s_tile;
-    __shared__ int s_qhead, s_err_ord, s_global;
+    __shared__ int s_err_ord, s_global;
     __shared__ unsigned long long s_pre_out, s_pre_lines;
     __shared__ unsigned s_kept, s_esc, s_skip, s_flag;
 
-    CSmem S;
+    const CSmem S = carve_csmem(smem, W ? tb.n_states : 0);
     {
-        uint8_t *p = smem;
         const int ns = W ? tb.n_states : 0;
-        S.dfa = reinterpret_cast<uint16_t *>(p); p += align16(ns * NCOL * 2);
-        S.codes = p; p += align16(ns * FAST_W);
-        S.explen = p; p += 256;
-        S.win = p; p += align16(WIN + 16);
-        S.dec = p; p += align16(WIN + 16);
-        S.out = p; p += align16(OUTCAP);
-        S.queue = reinterpret_cast<uint16_t *>(p); p += QCAP * 2;
-        S.chunk = reinterpret_cast<unsigned *>(p);
-        // tables -> smem once per CTA
         if (W) {
             const uint4 *src = reinterpret_cast<const uint4 *>(tb.dfa);
             uint4 *dst = reinterpret_cast<uint4 *>(S.dfa);
             for (int k = threadIdx.x; k < align16(ns * NCOL * 2) / 16; k += NT) dst[k] = src[k];
             for (int k = threadIdx.x; k < ns * FAST_W; k += NT) S.codes[k] = tb.codes[k];
         }
-        for (int k = threadIdx.x; k < 256; k += NT) S.explen[k] = tb.exp_len[k];
+        for (int k = threadIdx.x; k < 256; k += NT) {
+            S.explen[k] = tb.exp_len[k];
+            s_lut[k] = tok_bits(k);
+        }
     }
     const int tid = threadIdx.x;
 
@@ -219,43 +315,77 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
         int tile_lines;
         const int my_off = block_exscan<int>(my_cnt, s_tmp32, tile_lines);
 
-        // ---- DP phase, in rounds of QCAP lines ----
+        // ---- parse phase, in rounds of QCAP lines ----
         for (int q0 = 0; q0 < tile_lines; q0 += QCAP) {
-            const int q1 = min(q0 + QCAP, tile_lines);
-            if (my_cnt) scan_starts(S.win, tile_len, my_off, S.queue, q0, q1);
-            if (tid == 0) s_qhead = 0;
+            const int nq = min(QCAP, tile_lines - q0);
+            if (my_cnt) scan_starts(S.win, tile_len, my_off, S.queue, q0, q0 + nq);
+            for (int k = tid; k < 256; k += NT) s_hist[k] = 0;
             __syncthreads();
-            for (;;) {
-                const int q = atomicAdd(&s_qhead, 1);
-                if (q >= q1 - q0) break;
+            // line lengths and a counting sort by length (longest first) so
+            // the 32 lines a warp parses together have similar lengths
+            for (int q = tid; q < nq; q += NT) {
+                const int p = S.queue[q];
+                const int end = (q + 1 < nq) ? S.queue[q + 1] - 1 : find_end(S.win, p, win_len, hits_eof);
+                const int len = end < 0 ? 0xffff : end - p;
+                S.qlen[q] = (uint16_t)len;
+                atomicAdd(&s_hist[255 - min(len, 255)], 1u);
+            }
+            __syncthreads();
+            {
+                unsigned h = tid < 256 ? s_hist[tid] : 0u;
+                unsigned tot;
+                const unsigned ex = block_exscan<unsigned>(h, reinterpret_cast<unsigned *>(s_tmp32), tot);
+                if (tid < 256) s_hist[tid] = ex;
+            }
+            __syncthreads();
+            for (int q = tid; q < nq; q += NT) {
+                const int len = S.qlen[q];
+                const unsigned r = atomicAdd(&s_hist[255 - min(len, 255)], 1u);
+                S.qsort[r] = (uint16_t)q;
+            }
+            __syncthreads();
+            for (int r = tid; r < nq; r += NT) {
+                const int q = S.qsort[r];
                 const int ord = q0 + q;
                 const int p = S.queue[q];
-                int end = (q + 1 < q1 - q0) ? S.queue[q + 1] - 1 : find_end(S.win, p, win_len, hits_eof);
+                const int qlen = S.qlen[q];
                 const int chunk_owner = (p - HEAD) / CHUNK;
                 int kind = E_NONE;
                 long long size = 0;
-                bool global_line = end < 0;
+                bool global_line = qlen == 0xffff;
                 if (!global_line) {
                     uint8_t *s = S.win + p;
                     uint8_t *d = S.dec + p;
-                    int n_l = end - p;
+                    int n_l = qlen;
                     if (job.preprocess) {
-                        int nl2 = n_l, eoff;
+                        int eoff = -1;
                         unsigned long long ids[2] = {0, 0};
-                        int k = preprocess_line(s, n_l, d, s, &nl2, &eoff, ids);
+                        int k = renumber_fast(s, n_l, s_lut, &eoff, ids);
+                        if (k == RN_FALLBACK) {
+                            // pristine bytes, then the general routine
+                            const uint8_t *g = job.in + ws + p;
+                            for (int j = 0; j < n_l; ++j) s[j] = g[j];
+                            int nl2 = n_l;
+                            k = preprocess_line(s, n_l, d, s, &nl2, &eoff, ids);
+                            if (k == E_NONE) n_l = nl2;
+                        }
                         if (k == -1) {
                             global_line = true;
-                        } else if (k == E_CR) {
-                            kind = E_CR;
                         } else if (k != E_NONE) {
-                            if (job.lenient) atomicAdd(&s_flag, 1u);
-                            else kind = k;
-                        } else {
-                            n_l = nl2;
+                            if (k == E_CR) {
+                                kind = E_CR;
+                            } else if (job.lenient) {
+                                // keep the raw line (pipeline.py:108-115)
+                                const uint8_t *g = job.in + ws + p;
+                                for (int j = 0; j < n_l; ++j) s[j] = g[j];
+                                atomicAdd(&s_flag, 1u);
+                            } else {
+                                kind = k;
+                            }
                         }
                     } else {
-                        for (int k = 0; k < n_l; ++k)
-                            if (s[k] == '\r') { kind = E_CR; break; }
+                        for (int j = 0; j < n_l; ++j)
+                            if (s[j] == '\r') { kind = E_CR; break; }
                     }
                     if (!global_line) {
                         if (kind != E_NONE) {
@@ -299,8 +429,10 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                         size = cost + 1;
                     }
                 }
-                if (size) atomicAdd(&S.chunk[chunk_owner], (unsigned)size);
-                if (size) atomicAdd(&s_kept, 1u);
+                if (size) {
+                    atomicAdd(&S.chunk[chunk_owner], (unsigned)size);
+                    atomicAdd(&s_kept, 1u);
+                }
             }
             __syncthreads();
         }
@@ -309,11 +441,15 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
         unsigned long long tile_out;
         const unsigned long long my_out = S.chunk[tid];
         const unsigned long long my_out_off = block_exscan<unsigned long long>(my_out, s_tmp64, tile_out);
-        if (tid == 0) {
+        if (tid < 32) {
             unsigned long long po, pl;
             lookback(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
-            s_pre_out = po;
-            s_pre_lines = pl;
+            if (tid == 0) {
+                s_pre_out = po;
+                s_pre_lines = pl;
+            }
+        }
+        if (tid == 0) {
             atomicAdd(&job.ctl->total_out, tile_out);
             atomicAdd(&job.ctl->lines, (unsigned long long)s_kept);
             atomicAdd(&job.ctl->in_lines, (unsigned long long)tile_lines);
@@ -329,7 +465,6 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
 
         // ---- strict error: re-derive details of the first bad line ----
         if (tid == 0 && s_err_ord != 0x7fffffff) {
-            // find its start by ordinal
             int ord = s_err_ord, seen = 0, p = -1;
             for (int x = 0; x < tile_len && p < 0; ++x)
                 if (S.win[HEAD + x - 1] == '\n') {
@@ -342,8 +477,8 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
             bool cr = false;
             for (long long k = gs; k < ge; ++k) cr |= job.in[k] == '\r';
             if (!cr && job.preprocess) {
-                // recompute from the pristine input (marks in the arena-free
-                // output staging area, which is not used yet)
+                // recompute from the pristine input (marks + output in the
+                // staging area, unused until the emit)
                 int nl2, eoff = -1;
                 unsigned long long ids[2] = {0, 0};
                 const long long n_l = ge - gs;
@@ -368,66 +503,16 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
         }
         if (!fits) continue;
 
-        // ---- emit: each thread writes the lines that start in its chunk ----
+        // ---- emit ----
         __syncthreads();
         {
-            uint8_t *o_stage = S.out;
-            uint8_t *o_glob = job.out + pre_out;
-            unsigned long long w = my_out_off;
-            unsigned esc = 0;
-            const int c0 = tid * CHUNK, c1 = min(c0 + CHUNK, tile_len);
-            for (int x = c0; x < c1; ++x) {
-                if (S.win[HEAD + x - 1] != '\n') continue;
-                const int p = HEAD + x;
-                const uint8_t first = S.dec[p];
-                if (first == D_DROP) continue;
-                if (first == D_GLOBAL) {
-                    unsigned aoff = S.dec[p + 1] | (S.dec[p + 2] << 8) | (S.dec[p + 3] << 16) |
-                                    ((unsigned)S.dec[p + 4] << 24);
-                    const uint8_t *blk = job.arena + ((long long)aoff << 4);
-                    const ArenaHdr *h = reinterpret_cast<const ArenaHdr *>(blk);
-                    const long long n_pre = h->n_pre;
-                    const uint8_t *bytes = h->bytes_off < 0 ? job.in + ws + p : job.arena + h->bytes_off;
-                    const uint8_t *dec = job.arena + h->dec_off;
-                    for (long long i = 0; i < n_pre;) {
-                        uint8_t c = dec[i];
-                        if (c == D_ESC) {
-                            o_glob[w++] = 0x20;
-                            o_glob[w++] = bytes[i];
-                            ++esc;
-                            ++i;
-                        } else {
-                            o_glob[w++] = c;
-                            i += S.explen[c];
-                        }
-                    }
-                    o_glob[w++] = '\n';
-                    continue;
-                }
-                uint8_t *o = staged ? o_stage : o_glob;
-                int i = p;
-                for (;;) {
-                    uint8_t c = S.dec[i];
-                    if (c == D_END) break;
-                    if (c == D_ESC) {
-                        o[w++] = 0x20;
-                        o[w++] = S.win[i];
-                        ++esc;
-                        ++i;
-                    } else {
-                        o[w++] = c;
-                        i += S.explen[c];
-                    }
-                }
-                o[w++] = '\n';
-            }
+            unsigned esc;
+            if (staged) esc = emit_chunk<true>(job, S, ws, tile_len, my_out_off, S.out);
+            else esc = emit_chunk<false>(job, S, ws, tile_len, pre_out + my_out_off, job.out);
             if (esc) atomicAdd(&s_esc, esc);
         }
         __syncthreads();
-        if (staged) {
-            uint8_t *dst = job.out + pre_out;
-            for (unsigned long long k = tid; k < tile_out; k += NT) dst[k] = S.out[k];
-        }
+        if (staged) store_out(job.out + pre_out, S.out, (int)tile_out);
         if (tid == 0 && s_esc) atomicAdd(&job.ctl->escapes, (unsigned long long)s_esc);
     }
 }
@@ -477,6 +562,53 @@ __device__ __forceinline__ long long decode_fill(const uint8_t *r, long long n, 
     return w;
 }
 
+// Decompress emit: one flat walk over the positions of the thread's chunk
+// (records that start in it are finished past its end).  ST_LONG marks a
+// good record that runs past the staged window; it is expanded from HBM
+// (tiles holding one are never staged).
+constexpr uint8_t ST_LONG = 0xfe;
+
+template <bool STAGED>
+__device__ __forceinline__ void dec_emit_chunk(const Job &job, const DSmem &S, long long ws,
+                                               int tile_len, int ord, unsigned long long w,
+                                               uint8_t *o) {
+    const int c0 = threadIdx.x * CHUNK;
+    const int c1 = min(c0 + CHUNK, tile_len);
+    bool in = false, esc_next = false;
+    for (int x = c0; x < c1 || in; ++x) {
+        const int p = HEAD + x;
+        if (x < c1 && S.win[p - 1] == '\n') {
+            const uint8_t st = S.stat[ord++];
+            in = st == E_NONE;
+            esc_next = false;
+            if (st == ST_LONG) {
+                const long long gs = ws + p;
+                long long ge = gs;
+                while (ge < job.n && job.in[ge] != '\n') ++ge;
+                w += decode_fill(job.in + gs, ge - gs, S.explen, S.expoff, S.expflat, job.out + w);
+                job.out[w++] = '\n';
+                continue;
+            }
+        }
+        if (!in) continue;
+        const unsigned b = S.win[p];
+        if (esc_next) {
+            o[w++] = (uint8_t)b;
+            esc_next = false;
+        } else if (b == '\n') {
+            o[w++] = '\n';
+            in = false;
+        } else if (b == 0x20) {
+            esc_next = true;
+        } else {
+            const unsigned L = S.explen[b];
+            const uint8_t *e = S.expflat + S.expoff[b];
+            for (unsigned k = 0; k < L; ++k) o[w + k] = e[k];
+            w += L;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(NT, 1) decompress_tiles(Job job, Tables tb) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ unsigned long long s_tmp64[NWARP];
@@ -520,6 +652,8 @@ __global__ void __launch_bounds__(NT, 1) decompress_tiles(Job job, Tables tb) {
         load_window(job.in, job.n, ws, align16(win_len), win);
         chunk[tid] = 0;
         __syncthreads();
+        if (tid == 0 && hits_eof) win[win_len] = '\n';  // virtual newline after a final partial record
+        __syncthreads();
 
         const int my_cnt = scan_starts(win, tile_len, 0, nullptr, 0, 0);
         int tile_lines;
@@ -552,7 +686,7 @@ __global__ void __launch_bounds__(NT, 1) decompress_tiles(Job job, Tables tb) {
                 int code = 0;
                 unsigned esc = 0;
                 int st = decode_size(r, n_r, explen, &m, &ep, &code, &esc);
-                stat[ord] = (uint8_t)st;
+                stat[ord] = (uint8_t)(st == E_NONE && end < 0 ? ST_LONG : st);
                 if (esc) atomicAdd(&s_esc, esc);
                 if (st == E_NONE) {
                     atomicAdd(&chunk[(p - HEAD) / CHUNK], (unsigned)(m + 1));
@@ -569,11 +703,15 @@ __global__ void __launch_bounds__(NT, 1) decompress_tiles(Job job, Tables tb) {
         unsigned long long tile_out;
         const unsigned long long my_out_off = block_exscan<unsigned long long>(
             (unsigned long long)chunk[tid], s_tmp64, tile_out);
-        if (tid == 0) {
+        if (tid < 32) {
             unsigned long long po, pl;
             lookback(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
-            s_pre_out = po;
-            s_pre_lines = pl;
+            if (tid == 0) {
+                s_pre_out = po;
+                s_pre_lines = pl;
+            }
+        }
+        if (tid == 0) {
             atomicAdd(&job.ctl->total_out, tile_out);
             atomicAdd(&job.ctl->lines, (unsigned long long)s_kept);
             atomicAdd(&job.ctl->in_lines, (unsigned long long)tile_lines);
@@ -612,36 +750,10 @@ __global__ void __launch_bounds__(NT, 1) decompress_tiles(Job job, Tables tb) {
         if (!fits) continue;
 
         __syncthreads();
-        {
-            unsigned long long w = my_out_off;
-            uint8_t *o = staged ? obuf : job.out + pre_out;
-            const int c0 = tid * CHUNK, c1 = min(c0 + CHUNK, tile_len);
-            int ord = my_off;
-            for (int x = c0; x < c1; ++x) {
-                if (win[HEAD + x - 1] != '\n') continue;
-                const int p = HEAD + x;
-                if (stat[ord++] != E_NONE) continue;
-                int end = find_end(win, p, win_len, hits_eof);
-                const uint8_t *r;
-                long long n_r;
-                if (end >= 0) {
-                    r = win + p;
-                    n_r = end - p;
-                } else {
-                    long long gs = ws + p, ge = gs;
-                    while (ge < job.n && job.in[ge] != '\n') ++ge;
-                    r = job.in + gs;
-                    n_r = ge - gs;
-                }
-                w += decode_fill(r, n_r, explen, expoff, expflat, o + w);
-                o[w++] = '\n';
-            }
-        }
+        if (staged) dec_emit_chunk<true>(job, S, ws, tile_len, my_off, my_out_off, obuf);
+        else dec_emit_chunk<false>(job, S, ws, tile_len, my_off, pre_out + my_out_off, job.out);
         __syncthreads();
-        if (staged) {
-            uint8_t *dst = job.out + pre_out;
-            for (unsigned long long k = tid; k < tile_out; k += NT) dst[k] = obuf[k];
-        }
+        if (staged) store_out(job.out + pre_out, obuf, (int)tile_out);
     }
 }
 
