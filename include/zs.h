@@ -100,6 +100,12 @@ int zs_dictionary_fast(zs_ctx *ctx);
  * the fast path applies, 0 if not, <0 on bad arguments. */
 int zs_build_tables_host(const int32_t *children, const int16_t *term_code, int32_t n_nodes,
                          uint16_t *dfa, uint8_t *codes, int32_t *n_states, int32_t *max_len);
+/* Host-only inspection of the cost-window transducer: dfa2 uint16[256*97],
+ * t2 uint32[1024*16].  Returns 1 if built, 0 if the dictionary does not fit. */
+int zs_build_t2_host(const int32_t *children, const int16_t *term_code, int32_t n_nodes,
+                     uint16_t *dfa2, uint32_t *t2, int32_t *n_windows, int32_t *n_masks);
+/* debug/ablation: 0 forces the key-window DP instead of the transducer */
+int zs_set_transducer(zs_ctx *ctx, int on);
 
 /* ---- fine-grained parity shim (reference kernel layouts, host memory) ---- */
 /* out must hold 2*starts[n_lines] bytes; record i lands at out[2*starts[i]] */
@@ -137,6 +143,11 @@ int64_t zs_decompress_bound(zs_ctx *ctx, int64_t n);
 /* timing of the last whole-buffer call's main kernel (CUDA events on the
  * launching stream), milliseconds */
 float zs_last_kernel_ms(zs_ctx *ctx);
+
+/* profiling aid: per-phase SM cycles of the tile kernels (summed over CTAs,
+ * thread 0's view) for the last device-API call; off by default */
+int zs_set_phase_timing(zs_ctx *ctx, int on);
+int zs_last_phase_cycles(zs_ctx *ctx, uint64_t *cycles8);
 
 #ifdef __cplusplus
 }

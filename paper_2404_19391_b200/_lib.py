@@ -24,7 +24,8 @@ EXPORTS = (
     "zs_dictionary_fast", "zs_compress_batch", "zs_decompress_sizes", "zs_decompress_fill",
     "zs_preprocess_batch", "zs_compress_device", "zs_decompress_device", "zs_compress_host",
     "zs_decompress_host", "zs_compress_bound", "zs_decompress_bound", "zs_last_kernel_ms",
-    "zs_build_tables_host",
+    "zs_build_tables_host", "zs_set_phase_timing", "zs_last_phase_cycles", "zs_build_t2_host",
+    "zs_set_transducer",
 )
 
 
@@ -77,6 +78,10 @@ def load():
             "zs_decompress_bound": (I64, [P, I64]),
             "zs_last_kernel_ms": (ctypes.c_float, [P]),
             "zs_build_tables_host": (ctypes.c_int, [P, P, I32, P, P, P, P]),
+            "zs_set_phase_timing": (ctypes.c_int, [P, ctypes.c_int]),
+            "zs_build_t2_host": (ctypes.c_int, [P, P, I32, P, P, P, P]),
+            "zs_set_transducer": (ctypes.c_int, [P, ctypes.c_int]),
+            "zs_last_phase_cycles": (ctypes.c_int, [P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

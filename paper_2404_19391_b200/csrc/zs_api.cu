@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <array>
+#include <map>
+#include <set>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -50,6 +52,11 @@ struct HostTables {
     int n_states = 0;
     std::vector<uint16_t> dfa;
     std::vector<uint8_t> codes;
+    // cost-window transducer (see build_t2): dfa2 = dfa with a mask *index*
+    bool t2_ok = false;
+    int n_windows = 0, n_masks = 0;
+    std::vector<uint16_t> dfa2;
+    std::vector<uint32_t> t2;
     uint8_t exp_len[256];
     uint16_t exp_off[257];
     std::vector<uint8_t> exp_flat;
@@ -68,13 +75,15 @@ struct zs_ctx {
     HostTables ht;
     Tables tb{};
     int fast_w = 0;
-    DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat;
+    DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2;
+    int no_t2 = 0;  // debug: force the key-window DP
     // per-slot (double-buffered) work buffers
     DevBuf ctl[2], ts[2], terr[2], in[2], out[2], arena[2];  // arena: per slot
     // shim scratch
     DevBuf s_flat, s_starts, s_out, s_lens, s_dec, s_stat, s_errpos, s_tot, s_ids, s_outst;
     Ctl *h_ctl = nullptr;  // pinned, 2 slots
     float last_ms = 0.f;
+    int timing = 0;
 };
 
 namespace {
@@ -177,6 +186,95 @@ bool build_dfa(const std::vector<std::pair<std::string, int>> &pats, int max_len
     return true;
 }
 
+// Cost-window transducer for the parse.  The parse decision at byte i is a
+// function of the AC match mask M(i) and of the window of suffix costs of
+// positions i+1..i+W relative to cost[i+1] (plus INF past the line end).
+// Those windows come from a small closed set, so the DP step becomes
+//   (window, mask) -> (next window, chosen length L (0 = escape), cost delta)
+// precomputed here by BFS over the joint (AC state, window) states reachable
+// from the line-end state under every byte.  Built only if it fits smem.
+bool build_t2(HostTables &ht, int W) {
+    constexpr int8_t INF = 127;
+    const int ns = ht.n_states;
+    // distinct masks -> indices (stored in the DFA entry's high byte)
+    std::vector<int> mask_id(256, -1);
+    std::vector<unsigned> masks;
+    for (int s = 0; s < ns; ++s)
+        for (int col = 0; col < NCOL; ++col) {
+            unsigned m = ht.dfa[(size_t)s * NCOL + col] >> 8;
+            if (mask_id[m] < 0) {
+                mask_id[m] = (int)masks.size();
+                masks.push_back(m);
+            }
+        }
+    if (masks.size() > (size_t)T2_MASKS) return false;
+    typedef std::array<int8_t, FAST_W> Win;  // w[L-1] = cost[i+L] - cost[i+1]
+    std::map<Win, int> win_id;
+    std::vector<Win> wins;
+    auto wid = [&](const Win &w) {
+        auto it = win_id.find(w);
+        if (it != win_id.end()) return it->second;
+        int id = (int)wins.size();
+        win_id.emplace(w, id);
+        wins.push_back(w);
+        return id;
+    };
+    Win w0;
+    w0.fill(INF);
+    w0[0] = 0;
+    wid(w0);
+    std::map<std::pair<int, int>, uint32_t> step;  // (window, mask index) -> entry
+    auto transition = [&](int wi, int mi) -> uint32_t {
+        auto key = std::make_pair(wi, mi);
+        auto it = step.find(key);
+        if (it != step.end()) return it->second;
+        const Win w = wins[wi];
+        const unsigned M = masks[mi];
+        int bc = 2, bl = 1, L_sel = 0;  // escape: 0x20 + literal, cost 2
+        for (int L = 1; L <= W; ++L) {
+            if (!((M >> (L - 1)) & 1) || w[L - 1] == INF) continue;
+            int c = w[L - 1] + 1;
+            if (c < bc || (c == bc && L > bl)) {  // numba_impl.py:50
+                bc = c;
+                bl = L;
+                L_sel = L;
+            }
+        }
+        Win nw;
+        nw.fill(INF);
+        nw[0] = 0;
+        for (int L = 1; L < W; ++L) nw[L] = w[L - 1] == INF ? INF : (int8_t)(w[L - 1] - bc);
+        int nwi = wid(nw);
+        uint32_t e = (uint32_t)nwi | ((uint32_t)L_sel << 12) | ((uint32_t)(bc + 16) << 16);
+        step.emplace(key, e);
+        return e;
+    };
+    // BFS over joint states
+    std::set<std::pair<int, int>> seen;
+    std::vector<std::pair<int, int>> q{{0, 0}};
+    seen.insert({0, 0});
+    for (size_t qi = 0; qi < q.size(); ++qi) {
+        const int st = q[qi].first, wi = q[qi].second;
+        for (int col = 0; col < NCOL; ++col) {
+            const uint16_t e = ht.dfa[(size_t)st * NCOL + col];
+            const int s2 = e & 0xff, mi = mask_id[e >> 8];
+            const uint32_t x = transition(wi, mi);
+            std::pair<int, int> nxt{s2, (int)(x & 0xfff)};
+            if (seen.insert(nxt).second) q.push_back(nxt);
+            if (wins.size() > (size_t)T2_WINDOWS || q.size() > 400000) return false;
+        }
+    }
+    ht.n_windows = (int)wins.size();
+    ht.n_masks = (int)masks.size();
+    ht.t2.assign((size_t)ht.n_windows * T2_MASKS, 0xffffffffu);
+    for (auto &kv : step) ht.t2[(size_t)kv.first.first * T2_MASKS + kv.first.second] = kv.second;
+    ht.dfa2 = ht.dfa;
+    for (size_t k = 0; k < (size_t)ns * NCOL; ++k)
+        ht.dfa2[k] = (uint16_t)((ht.dfa[k] & 0xff) | (mask_id[ht.dfa[k] >> 8] << 8));
+    ht.t2_ok = true;
+    return true;
+}
+
 template <typename K>
 cudaError_t set_smem(K kernel, int bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -184,13 +282,14 @@ cudaError_t set_smem(K kernel, int bytes) {
 
 typedef void (*TileKernel)(Job, Tables);
 
-TileKernel compress_kernel(int w) {
+TileKernel compress_kernel(int w, bool t2) {
+    if (t2) return compress_tiles<8, true>;  // W only sizes the (unused) key window
     switch (w) {
-    case 2: return compress_tiles<2>;
-    case 4: return compress_tiles<4>;
-    case 6: return compress_tiles<6>;
-    case 8: return compress_tiles<8>;
-    default: return compress_tiles<0>;
+    case 2: return compress_tiles<2, false>;
+    case 4: return compress_tiles<4, false>;
+    case 6: return compress_tiles<6, false>;
+    case 8: return compress_tiles<8, false>;
+    default: return compress_tiles<0, false>;
     }
 }
 
@@ -233,12 +332,15 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
     job.terr = ctx->terr[slot].as<TileErr>();
     job.arena = ctx->arena[slot].as<uint8_t>();
     job.arena_cap = (long long)ctx->arena[slot].cap;
+    job.timing = ctx->timing;
     if (nt > 0) {
         const int grid = (int)std::min<long long>(nt, ctx->n_sm);
         if (timed) CK(cudaEventRecord(ctx->ev0, st));
         if (compress) {
-            TileKernel k = compress_kernel(ctx->fast_w);
-            const int smem = compress_smem_bytes(ctx->fast_w ? ctx->tb.n_states : 0);
+            const bool t2 = ctx->fast_w && ctx->ht.t2_ok && !ctx->no_t2;
+            TileKernel k = compress_kernel(ctx->fast_w, t2);
+            const int smem = compress_smem_bytes(ctx->fast_w ? ctx->tb.n_states : 0,
+                                                 t2 ? ctx->ht.n_windows : 0);
             CK(set_smem(k, smem));
             k<<<grid, NT, smem, st>>>(job, ctx->tb);
         } else {
@@ -500,7 +602,7 @@ int zs_ctx_create(int device, zs_ctx **out) {
 int zs_ctx_destroy(zs_ctx *ctx) {
     if (!ctx) return ZS_OK;
     cudaSetDevice(ctx->dev);
-    for (DevBuf *b : {&ctx->d_dfa, &ctx->d_codes, &ctx->d_children, &ctx->d_term, &ctx->d_explen,
+    for (DevBuf *b : {&ctx->d_dfa2, &ctx->d_t2, &ctx->d_dfa, &ctx->d_codes, &ctx->d_children, &ctx->d_term, &ctx->d_explen,
                       &ctx->d_expoff, &ctx->d_expflat, &ctx->ctl[0], &ctx->ctl[1], &ctx->ts[0],
                       &ctx->ts[1], &ctx->terr[0], &ctx->terr[1], &ctx->in[0], &ctx->in[1],
                       &ctx->out[0], &ctx->out[1], &ctx->arena[0], &ctx->arena[1], &ctx->s_flat, &ctx->s_starts,
@@ -523,6 +625,18 @@ const char *zs_last_error(zs_ctx *ctx) { return ctx ? ctx->err.c_str() : "no con
 
 float zs_last_kernel_ms(zs_ctx *ctx) { return ctx ? ctx->last_ms : 0.f; }
 
+int zs_set_phase_timing(zs_ctx *ctx, int on) {
+    if (!ctx) return ZS_E_ARG;
+    ctx->timing = on ? 1 : 0;
+    return ZS_OK;
+}
+
+int zs_last_phase_cycles(zs_ctx *ctx, uint64_t *cycles8) {
+    if (!ctx || !cycles8) return ZS_E_ARG;
+    for (int k = 0; k < 8; ++k) cycles8[k] = ctx->h_ctl[0].phase[k];
+    return ZS_OK;
+}
+
 int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_code,
                       int32_t n_nodes, const int32_t *exp_len, const uint8_t *valid,
                       const int64_t *exp_off, const uint8_t *exp_flat) {
@@ -539,6 +653,7 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
     ht.max_len = 0;
     for (auto &p : pats) ht.max_len = std::max<int>(ht.max_len, (int)p.first.size());
     ht.fast = build_dfa(pats, ht.max_len, ht);
+    if (ht.fast) build_t2(ht, std::max(1, ht.max_len));
     // decode tables (dictionary.py:112-129): valid codes have exp_len > 0
     if (exp_off[256] > 65535) {
         ctx->err = "expansion table too large";
@@ -569,11 +684,18 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
         CK(up(ctx->d_dfa, ht.dfa.data(), ht.dfa.size() * 2));
         CK(up(ctx->d_codes, ht.codes.data(), ht.codes.size()));
     }
+    if (ht.t2_ok) {
+        CK(up(ctx->d_dfa2, ht.dfa2.data(), ht.dfa2.size() * 2));
+        CK(up(ctx->d_t2, ht.t2.data(), ht.t2.size() * 4));
+    }
     Tables &tb = ctx->tb;
     tb.dfa = ht.fast ? ctx->d_dfa.as<uint16_t>() : nullptr;
     tb.codes = ht.fast ? ctx->d_codes.as<uint8_t>() : nullptr;
     tb.n_states = ht.fast ? ht.n_states : 0;
     tb.fast = ht.fast ? 1 : 0;
+    tb.dfa2 = ht.t2_ok ? ctx->d_dfa2.as<uint16_t>() : nullptr;
+    tb.t2 = ht.t2_ok ? ctx->d_t2.as<uint32_t>() : nullptr;
+    tb.n_windows = ht.t2_ok ? ht.n_windows : 0;
     tb.children = ctx->d_children.as<int32_t>();
     tb.term_code = ctx->d_term.as<int16_t>();
     tb.n_nodes = n_nodes;
@@ -592,6 +714,29 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
 }
 
 int zs_dictionary_fast(zs_ctx *ctx) { return ctx && ctx->have_dict ? ctx->fast_w : -1; }
+
+int zs_build_t2_host(const int32_t *children, const int16_t *term_code, int32_t n_nodes,
+                     uint16_t *dfa2, uint32_t *t2, int32_t *n_windows, int32_t *n_masks) {
+    if (!children || !term_code || n_nodes < 1 || !dfa2 || !t2 || !n_windows || !n_masks)
+        return ZS_E_ARG;
+    std::vector<std::pair<std::string, int>> pats;
+    trie_patterns(children, term_code, n_nodes, pats);
+    HostTables ht;
+    for (auto &p : pats) ht.max_len = std::max<int>(ht.max_len, (int)p.first.size());
+    *n_windows = *n_masks = 0;
+    if (!build_dfa(pats, ht.max_len, ht) || !build_t2(ht, std::max(1, ht.max_len))) return 0;
+    *n_windows = ht.n_windows;
+    *n_masks = ht.n_masks;
+    memcpy(dfa2, ht.dfa2.data(), (size_t)ht.n_states * NCOL * 2);
+    memcpy(t2, ht.t2.data(), ht.t2.size() * 4);
+    return 1;
+}
+
+int zs_set_transducer(zs_ctx *ctx, int on) {
+    if (!ctx) return ZS_E_ARG;
+    ctx->no_t2 = on ? 0 : 1;
+    return ZS_OK;
+}
 
 int zs_build_tables_host(const int32_t *children, const int16_t *term_code, int32_t n_nodes,
                          uint16_t *dfa, uint8_t *codes, int32_t *n_states, int32_t *max_len) {

@@ -35,17 +35,22 @@ namespace zs {
 // ----------------------------------------------------------------------------
 constexpr int NT = 512;                 // threads per CTA
 constexpr int NWARP = NT / 32;
-constexpr int TILE = 32768;             // bytes of line-start ownership per tile
+// Per-thread chunk of the tile for the newline scans and the emit walks.
+// 68 bytes = 17 words: an odd word stride puts the 32 lanes of a warp on 32
+// different shared-memory banks (a 64-byte stride would be a 16-way conflict).
+constexpr int CHUNK = 68;
+constexpr int TILE = CHUNK * NT;        // 34816 bytes of line-start ownership per tile
 constexpr int EXTRA = 4096;             // window overhang past the tile end
 constexpr int HEAD = 16;                // bytes staged before the tile start
 constexpr int WIN = HEAD + TILE + EXTRA;  // staged window (multiple of 16)
-constexpr int CHUNK = TILE / NT;        // per-thread newline-scan chunk (64 B)
-constexpr int QCAP = 4096;              // line queue capacity per round
-constexpr int OUTCAP = TILE + EXTRA;    // compress staging (no-expansion case)
+constexpr int QCAP = 2048;              // line queue capacity per round
+constexpr int OUTCAP = 20480;           // compress staging (~0.4 B/B typical; else direct)
 constexpr int DOUTCAP = 3 * TILE;       // decompress staging
 constexpr int NCOL = 97;                // DFA columns: bytes 0x20..0x7f, other
 constexpr int FAST_W = 8;               // max pattern length on the fast path
 constexpr int FAST_STATES = 256;        // max DFA states on the fast path
+constexpr int T2_MASKS = 16;            // cost-window transducer: mask indices per window
+constexpr int T2_WINDOWS = 1024;        // ... and windows (4 B entries: <= 64 KB)
 
 // decision-byte sentinels (never valid codes: codes are 0x21-0x7e, 0x80-0xff)
 constexpr uint8_t D_ESC = 0x20;   // escape: emit 0x20 + literal
@@ -67,6 +72,12 @@ struct Tables {
     const uint8_t *codes;   // [n_states][FAST_W] code of the match of length L+1
     int n_states;
     int fast;               // 1 if the DFA path serves this dictionary
+    // cost-window transducer (fast path, when built): dfa2 entries carry a
+    // mask index instead of the mask; t2[window][mask index] = next window |
+    // L << 12 | (cost delta + 16) << 16
+    const uint16_t *dfa2;
+    const uint32_t *t2;
+    int n_windows;
     // generic path (reference layout): dense trie in HBM
     const int32_t *children;  // [n_nodes][256]
     const int16_t *term_code;
@@ -90,6 +101,7 @@ struct Ctl {                    // zeroed before every launch
     unsigned long long arena_used;
     unsigned long long overflow;   // output or arena capacity exceeded
     unsigned long long in_lines;   // lines seen (records in)
+    unsigned long long phase[8];   // per-phase SM cycles (thread 0), when Job.timing
 };
 
 struct TileState {
@@ -117,14 +129,68 @@ struct Job {
     TileErr *terr;
     uint8_t *arena;
     long long arena_cap;
+    int timing;  // accumulate per-phase clock64 deltas into Ctl.phase
+};
+
+// thread-0 phase clock: PHASE(k) adds the cycles since the last mark to phase k
+struct PhaseClock {
+    long long t;
+    __device__ __forceinline__ void start() { t = clock64(); }
+    __device__ __forceinline__ void mark(const Job &job, int k) {
+        if (job.timing && threadIdx.x == 0) {
+            long long now = clock64();
+            atomicAdd(&job.ctl->phase[k], (unsigned long long)(now - t));
+            t = now;
+        }
+    }
 };
 
 // ----------------------------------------------------------------------------
-// small helpers
+// small helpers (host-callable too: tests/hostcheck runs the per-line
+// routines on the CPU against the oracle)
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ int dcol(unsigned b) { return (int)min(b - 0x20u, 96u); }
+#define ZS_HD __host__ __device__ __forceinline__
 
-__device__ __forceinline__ bool is_digit(unsigned b) { return b - '0' < 10u; }
+ZS_HD unsigned umin_(unsigned a, unsigned b) { return a < b ? a : b; }
+ZS_HD int imin_(int a, int b) { return a < b ? a : b; }
+ZS_HD int ffs64_(unsigned long long x) {
+#ifdef __CUDA_ARCH__
+    return __ffsll((long long)x);
+#else
+    return __builtin_ffsll((long long)x);
+#endif
+}
+
+ZS_HD int dcol(unsigned b) { return (int)umin_(b - 0x20u, 96u); }
+
+// Byte loads from a buffer that lives in shared memory on the device: the
+// 32-bit shared address is formed once (a generic pointer re-derives the
+// window base every access).  Host builds read through the pointer.
+struct SmemBytes {
+#ifdef __CUDA_ARCH__
+    unsigned base;
+    __device__ __forceinline__ explicit SmemBytes(const uint8_t *p)
+        : base((unsigned)__cvta_generic_to_shared(p)) {}
+    __device__ __forceinline__ unsigned ld(int i) const {
+        unsigned v;
+        asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(base + i));
+        return v;
+    }
+#else
+    const uint8_t *p;
+    explicit SmemBytes(const uint8_t *q) : p(q) {}
+    unsigned ld(int i) const { return p[i]; }
+#endif
+};
+
+// warp-uniform loop condition (device: all 32 lanes must take part)
+#ifdef __CUDA_ARCH__
+#define ZS_ANY(p) __any_sync(0xffffffffu, (p))
+#else
+#define ZS_ANY(p) (p)
+#endif
+
+ZS_HD bool is_digit(unsigned b) { return b - '0' < 10u; }
 
 // byte classes for the tokenizer (smiles.py:23-35, 83-137)
 enum : uint8_t {
@@ -132,7 +198,7 @@ enum : uint8_t {
     C_BOPEN = 7, C_BCLOSE = 8, C_DOT = 9, C_CR = 10
 };
 
-__device__ __forceinline__ uint8_t tok_class(unsigned b) {
+ZS_HD uint8_t tok_class(unsigned b) {
     if ((b | 0x20u) - 'a' < 26u || b == '*') return C_ATOM;
     if (b - '0' < 10u) return C_DIGIT;
     switch (b) {
@@ -188,28 +254,37 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
     return v;
 }
 
-__device__ __forceinline__ void lookback(TileState *ts, long long t, unsigned long long agg_out,
-                                         unsigned long long agg_lines,
-                                         unsigned long long &pre_out,
-                                         unsigned long long &pre_lines) {
+// Publish this tile's aggregate (tile 0 publishes its inclusive prefix).
+__device__ __forceinline__ void lookback_publish(TileState *ts, long long t,
+                                                 unsigned long long agg_out,
+                                                 unsigned long long agg_lines) {
     volatile TileState *vts = ts;
-    const int lane = threadIdx.x & 31;
     if (t == 0) {
-        if (lane == 0) {
-            vts[0].inc_out = agg_out;
-            vts[0].inc_lines = agg_lines;
-            __threadfence();
-            atomicExch(&ts[0].flag, F_INC);
-        }
-        pre_out = 0;
-        pre_lines = 0;
-        return;
-    }
-    if (lane == 0) {
+        vts[0].inc_out = agg_out;
+        vts[0].inc_lines = agg_lines;
+        __threadfence();
+        atomicExch(&ts[0].flag, F_INC);
+    } else {
         vts[t].agg_out = agg_out;
         vts[t].agg_lines = agg_lines;
         __threadfence();
         atomicExch(&ts[t].flag, F_AGG);
+    }
+}
+
+// Resolve the exclusive prefix of tile t (all 32 lanes of one warp) and
+// publish t's inclusive prefix.
+__device__ __forceinline__ void lookback_resolve(TileState *ts, long long t,
+                                                 unsigned long long agg_out,
+                                                 unsigned long long agg_lines,
+                                                 unsigned long long &pre_out,
+                                                 unsigned long long &pre_lines) {
+    volatile TileState *vts = ts;
+    const int lane = threadIdx.x & 31;
+    if (t == 0) {
+        pre_out = 0;
+        pre_lines = 0;
+        return;
     }
     unsigned long long po = 0, pl = 0;
     long long j = t - 1;
@@ -246,6 +321,15 @@ __device__ __forceinline__ void lookback(TileState *ts, long long t, unsigned lo
     pre_lines = pl;
 }
 
+__device__ __forceinline__ void lookback(TileState *ts, long long t, unsigned long long agg_out,
+                                         unsigned long long agg_lines,
+                                         unsigned long long &pre_out,
+                                         unsigned long long &pre_lines) {
+    if ((threadIdx.x & 31) == 0) lookback_publish(ts, t, agg_out, agg_lines);
+    __syncwarp();
+    lookback_resolve(ts, t, agg_out, agg_lines, pre_out, pre_lines);
+}
+
 // ----------------------------------------------------------------------------
 // ring renumbering of one line (smiles.py:83-213), strict semantics.
 //
@@ -261,7 +345,7 @@ __device__ __forceinline__ void lookback(TileState *ts, long long t, unsigned lo
 // E_* on a tokenize/pair/colour error (err_off / ids filled), or -1 when the
 // line grows (caller re-runs it out of place with out != buf).
 // ----------------------------------------------------------------------------
-__device__ int preprocess_line(const uint8_t *buf, int n, uint8_t *marks, uint8_t *out,
+__host__ __device__ int preprocess_line(const uint8_t *buf, int n, uint8_t *marks, uint8_t *out,
                                int *new_len, int *err_off, unsigned long long ids[2],
                                bool cr_is_error = true) {
     uint64_t open0 = 0, open1 = 0;  // currently open ring ids
@@ -327,8 +411,8 @@ __device__ int preprocess_line(const uint8_t *buf, int n, uint8_t *marks, uint8_
                         if (m < 64) used0 |= 1ull << m; else used1 |= 1ull << (m - 64);
                     }
                 }
-                int col = used0 != ~0ull ? __ffsll((long long)~used0) - 1
-                                         : 64 + (used1 != ~0ull ? __ffsll((long long)~used1) - 1 : 64);
+                int col = used0 != ~0ull ? ffs64_(~used0) - 1
+                                         : 64 + (used1 != ~0ull ? ffs64_(~used1) - 1 : 64);
                 if (col > 99) { err = E_OVERFLOW; break; }
                 marks[o] = (uint8_t)col;
                 marks[i] = (uint8_t)col;
@@ -385,63 +469,111 @@ __device__ int preprocess_line(const uint8_t *buf, int n, uint8_t *marks, uint8_
 }
 
 // ----------------------------------------------------------------------------
-// ring renumbering, fast path (the common case, one byte per loop trip).
+// ring renumbering, fast path (the common case), in three steps:
 //
-// Same semantics as preprocess_line, restricted to lines whose ring tokens
-// are single digits, with at most 4 rings open at once and colours < 8 (so
-// every token keeps its width and the rewrite is in place at close time).
-// Open rings live in 4 register slots (id, position); the smallest free
-// colour is found from lc[k] = position where colour k last closed: colour k
-// is taken by a ring closed inside (o, c) iff lc[k] > o.  Anything else
-// returns RN_FALLBACK and the caller re-runs the line through
-// preprocess_line on pristine bytes.  On any return other than E_NONE the
-// line bytes may be partially rewritten (callers restore them from HBM).
+//  1. tokenize: one tight pass over the bytes (class LUT in smem).  Ring
+//     tokens are threaded into a forward chain kept in `marks`: marks[pos]
+//     = distance to the next chain node (0 = last; 255 = a hop node that is
+//     not a token, inserted when the gap exceeds 254).
+//  2. pair + colour: walk the chain (~6 nodes per line).  Open rings live in
+//     4 register slots (id, position); the smallest free colour comes from
+//     lc[k] = position where colour k last closed (k is taken by a ring
+//     closed inside (o, c) iff lc[k] > o).  Single-digit tokens are
+//     rewritten in place; a '%nn' token gets its digit in s[pos+1] and the
+//     line is compacted in step 3.
+//  3. compaction (only with '%nn' ring tokens): walk the chain again,
+//     shifting the bytes between tokens left.
+//
+// Same semantics as preprocess_line for lines with at most 4 rings open at
+// once and colours < 8; otherwise RN_FALLBACK (the caller restores the line
+// from HBM and runs preprocess_line).  On any return other than E_NONE the
+// line bytes may be partially rewritten.
 // ----------------------------------------------------------------------------
 constexpr int RN_FALLBACK = -4;
-enum : uint8_t { K_OKP = 1, K_DIG = 2, K_PCT = 4, K_LBR = 8, K_CR = 16 };
+enum : uint8_t { K_OKP = 1, K_DIG = 2, K_PCT = 4, K_LBR = 8, K_CR = 16, K_SPECIAL = K_PCT | K_LBR | K_CR };
 
-__device__ __forceinline__ uint8_t tok_bits(unsigned b) {
+ZS_HD uint8_t tok_bits(unsigned b) {
     uint8_t c = tok_class(b);
     return c == C_ATOM || c == C_BOND ? K_OKP : c == C_DIGIT ? K_DIG : c == C_PCT ? K_PCT
          : c == C_LBR ? K_LBR : c == C_CR ? K_CR : 0;
 }
 
-__device__ __forceinline__ int renumber_fast(uint8_t *s, int n, const uint8_t *lut, int *err_off,
-                                             unsigned long long ids[2]) {
+// next ring token after chain node i (step = marks[i] != 0); 255 = hop of 254
+ZS_HD int chain_next(const uint8_t *marks, int i, unsigned step) {
+    while (step == 255) {
+        i += 254;
+        step = marks[i];
+    }
+    return i + step;
+}
+
+// All 32 lanes of a warp must call renumber_fast together (lanes with
+// nothing to do pass n = 0): its loops are warp-uniform (ZS_ANY) so the lanes
+// stay converged trip by trip under independent thread scheduling.
+ZS_HD int renumber_fast(uint8_t *s, int n, const uint8_t *lut, uint8_t *marks,
+                        int *new_len, int *err_off, unsigned long long ids[2]) {
+    int res = E_NONE;
+    // ---- 1. tokenize, chain the ring tokens ----
+    // Branch-free per byte (selects + one predicated store), so a warp pays
+    // one path per trip; only '%' tokens and chain hops branch (rare).
+    int first = -1, last = -1, n_pct = 0, br = -1;  // br: open '[' position, -1 outside
+    unsigned ring_ok = 0, crs = 0;
+    const SmemBytes sb(s), lb(lut);
+    for (int i = 0; ZS_ANY(i < n && res == E_NONE);) {
+        if (i >= n || res != E_NONE) continue;
+        const unsigned b = sb.ld(i);
+        const unsigned c = lb.ld(b);
+        crs |= c;
+        const bool inside = br >= 0;
+        unsigned ring = (inside ? 0u : ring_ok) & (c >> 1);  // K_DIG = 2
+        int adv = 1;
+        if (!inside && (c & K_PCT)) {
+            // '%': two digits must follow, in any context
+            if (i + 2 >= n || !is_digit(sb.ld(i + 1)) || !is_digit(sb.ld(i + 2))) {
+                res = E_PERCENT;
+                *err_off = i;
+                continue;
+            }
+            ring = ring_ok;
+            n_pct += ring;
+            adv = 3;
+        }
+        const bool rbr = inside && b == ']';
+        br = inside ? (rbr ? -1 : br) : ((c & K_LBR) ? i : -1);
+        ring_ok = inside ? (ring_ok | rbr) : (ring | (c & K_OKP));
+        if (ring && last >= 0 && i - last > 254) {  // hop nodes (not tokens)
+            while (i - last > 254) {
+                marks[last] = 255;
+                last += 254;
+            }
+        }
+        if (ring && last >= 0) marks[last] = (uint8_t)(i - last);
+        first = (ring && first < 0) ? i : first;
+        last = ring ? i : last;
+        i += adv;
+    }
+    if (res == E_PERCENT)  // the scan stopped early: look for a '\r' in the rest
+        for (int k = 0; k < n; ++k) crs |= s[k] == '\r' ? K_CR : 0u;
+    if (crs & K_CR) {
+        res = E_CR;  // '\r' anywhere in the line takes precedence (pipeline.py:102-107)
+    } else if (res == E_NONE && br >= 0) {
+        *err_off = br;  // '[' never closed
+        res = E_BRACKET;
+    }
+    if (res == E_NONE && first >= 0) marks[last] = 0;
+    // ---- 2. pair + colour along the chain ----
     unsigned oid = 0xffffffffu;  // 4 slots: open ring id per byte, 0xff = free
     int opos[4] = {0, 0, 0, 0};
     int lc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) lc[k] = -1;
-    bool ring_ok = false, in_br = false;
-    int br = 0;
-    for (int i = 0; i < n; ++i) {
-        const unsigned b = s[i];
-        const unsigned c = lut[b];
-        if (in_br) {
-            if (b == ']') { in_br = false; ring_ok = true; }
-            else if (c & K_CR) return E_CR;
-            continue;
-        }
-        if (!(c & (K_DIG | K_PCT | K_LBR | K_CR))) {
-            ring_ok = c & K_OKP;
-            continue;
-        }
-        if (c & K_LBR) { in_br = true; br = i; continue; }
-        if (c & K_CR) return E_CR;
-        if (c & K_PCT) {
-            if (i + 2 >= n || !is_digit(s[i + 1]) || !is_digit(s[i + 2])) {
-                for (int k = i; k < n; ++k)
-                    if (s[k] == '\r') return E_CR;
-                *err_off = i;
-                return E_PERCENT;
-            }
-            if (ring_ok) return RN_FALLBACK;  // %nn ring id: width may change
-            i += 2;                           // '%nn' as an Other token
-            continue;
-        }
-        if (!ring_ok) continue;  // digit after a non-atom: Other, ring_ok stays false
-        const unsigned rid = b - '0';
+    int node = res == E_NONE ? first : -1;
+    while (ZS_ANY(node >= 0)) {
+        if (node < 0) continue;
+        const int i = node;
+        const unsigned step = marks[i];
+        const bool pct = s[i] == '%';
+        const unsigned rid = pct ? (s[i + 1] - '0') * 10u + (s[i + 2] - '0') : s[i] - '0';
         int slot = -1, free_slot = -1;
 #pragma unroll
         for (int k = 3; k >= 0; --k) {
@@ -450,7 +582,11 @@ __device__ __forceinline__ int renumber_fast(uint8_t *s, int n, const uint8_t *l
             if (v == 0xffu) free_slot = k;
         }
         if (slot < 0) {
-            if (free_slot < 0) return RN_FALLBACK;
+            if (free_slot < 0) {
+                res = RN_FALLBACK;
+                node = -1;
+                continue;
+            }
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 if (k == free_slot) opos[k] = i;
@@ -465,29 +601,46 @@ __device__ __forceinline__ int renumber_fast(uint8_t *s, int n, const uint8_t *l
 #pragma unroll
             for (int k = 7; k >= 0; --k)
                 if (lc[k] <= o) col = k;
-            if (col == 8) return RN_FALLBACK;
+            if (col == 8) {
+                res = RN_FALLBACK;
+                node = -1;
+                continue;
+            }
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 if (k == col) lc[k] = i;
-            s[o] = (uint8_t)('0' + col);
-            s[i] = (uint8_t)('0' + col);
+            s[o + (s[o] == '%')] = (uint8_t)('0' + col);
+            s[i + pct] = (uint8_t)('0' + col);
         }
-        ring_ok = true;
+        node = step ? chain_next(marks, i, step) : -1;
     }
-    if (in_br) {
-        *err_off = br;
-        return E_BRACKET;
-    }
-    if (oid != 0xffffffffu) {
+    if (res == E_NONE && oid != 0xffffffffu) {
         ids[0] = ids[1] = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const unsigned v = (oid >> (8 * k)) & 0xffu;
-            if (v != 0xffu) ids[0] |= 1ull << v;
+            if (v != 0xffu) ids[v >> 6] |= 1ull << (v & 63);
         }
-        return E_UNPAIRED;
+        res = E_UNPAIRED;
     }
-    return E_NONE;
+    // ---- 3. compaction of '%nn' ring tokens (rare: no warp-uniform loop) ----
+    *new_len = n;
+    if (res == E_NONE && n_pct) {
+        int w = first, r = first;
+        for (int i = first;;) {
+            while (r < i) s[w++] = s[r++];
+            const unsigned step = marks[i];
+            if (s[i] == '%') {
+                s[w++] = s[i + 1];
+                r = i + 3;
+            }
+            if (!step) break;
+            i = chain_next(marks, i, step);
+        }
+        while (r < n) s[w++] = s[r++];
+        *new_len = w;
+    }
+    return res;
 }
 
 // ----------------------------------------------------------------------------
@@ -501,7 +654,7 @@ __device__ __forceinline__ int renumber_fast(uint8_t *s, int n, const uint8_t *l
 // s[0..n) line bytes, dec[0..n] decisions out.  Returns cost[0].
 // ----------------------------------------------------------------------------
 template <int W>
-__device__ __forceinline__ int dp_fast(const uint8_t *s, int n, uint8_t *dec,
+ZS_HD int dp_fast(const uint8_t *s, int n, uint8_t *dec,
                                        const uint16_t *dfa, const uint8_t *codes) {
     constexpr int INF = 0x3fffffff;
     int k[W + 1];
@@ -522,9 +675,9 @@ __device__ __forceinline__ int dp_fast(const uint8_t *s, int n, uint8_t *dec,
         int mm = INF;
 #pragma unroll
         for (int L = 1; L <= W; ++L)
-            if (e & (0x100u << (L - 1))) mm = min(mm, k[L]);
+            if (e & (0x100u << (L - 1))) mm = imin_(mm, k[L]);
         int esc = k[1] + (2 << 3);
-        int best = min(esc, mm + (1 << 3));
+        int best = imin_(esc, mm + (1 << 3));
         int t = best + i + W;
         int L = W - (t & 7);
         key = (t & ~7) - i;
@@ -532,6 +685,30 @@ __device__ __forceinline__ int dp_fast(const uint8_t *s, int n, uint8_t *dec,
         dec[i] = esc < mm + (1 << 3) ? D_ESC : code;
     }
     return key >> 3;  // position 0: key = cost[0] << 3
+}
+
+// ----------------------------------------------------------------------------
+// min-cost parse through the cost-window transducer: per byte one AC-DFA
+// lookup (next state, match-mask index) and one t2 lookup (next relative cost
+// window, chosen length, cost delta).  Same decisions as dp_fast by
+// construction (build_t2 enumerates exactly dp_fast's step).  Returns cost[0].
+// ----------------------------------------------------------------------------
+ZS_HD int dp_t2(const uint8_t *s, int n, uint8_t *dec, const uint16_t *dfa2, const uint32_t *t2,
+                const uint8_t *codes) {
+    unsigned st = 0, wi = 0;
+    int cost = 0;
+    dec[n] = D_END;
+    for (int i = n - 1; i >= 0; --i) {
+        const unsigned b = s[i];
+        const unsigned e = dfa2[st * NCOL + dcol(b)];
+        st = e & 0xffu;
+        const unsigned x = t2[wi * T2_MASKS + (e >> 8)];
+        wi = x & 0xfffu;
+        const unsigned L = (x >> 12) & 15u;
+        cost += (int)(x >> 16) - 16;
+        dec[i] = L ? codes[st * FAST_W + L - 1] : D_ESC;
+    }
+    return cost;
 }
 
 // ----------------------------------------------------------------------------

@@ -9,7 +9,8 @@ namespace zs {
 // shared-memory carve-up for the compress tile kernel
 // ----------------------------------------------------------------------------
 struct CSmem {
-    uint16_t *dfa;
+    uint16_t *dfa;    // AC DFA (mask-index entries in transducer mode)
+    uint32_t *t2;     // cost-window transducer (transducer mode only)
     uint8_t *codes;
     uint8_t *explen;
     uint8_t *win;
@@ -18,19 +19,22 @@ struct CSmem {
     uint16_t *queue;  // line starts (window offsets) of the current round
     uint16_t *qlen;   // their lengths (0xffff = runs past the window)
     uint16_t *qsort;  // queue indices sorted by length, longest first
+    unsigned *qoff;   // per line: payload size, then (scanned) tile output offset
     unsigned *chunk;  // per-thread-chunk output byte sums
 };
 
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
-__host__ __device__ inline int compress_smem_bytes(int n_states) {
-    return align16(n_states * NCOL * 2) + align16(n_states * FAST_W) + 256 + align16(WIN + 16) +
-           align16(WIN + 16) + align16(OUTCAP) + 3 * QCAP * 2 + NT * 4;
+__host__ __device__ inline int compress_smem_bytes(int n_states, int n_windows) {
+    return align16(n_states * NCOL * 2) + n_windows * T2_MASKS * 4 + align16(n_states * FAST_W) +
+           256 + align16(WIN + 16) +
+           align16(WIN + 16) + align16(OUTCAP) + 3 * QCAP * 2 + QCAP * 4 + NT * 4;
 }
 
-__device__ inline CSmem carve_csmem(uint8_t *p, int ns) {
+__device__ inline CSmem carve_csmem(uint8_t *p, int ns, int nw) {
     CSmem S;
     S.dfa = reinterpret_cast<uint16_t *>(p); p += align16(ns * NCOL * 2);
+    S.t2 = reinterpret_cast<uint32_t *>(p); p += nw * T2_MASKS * 4;
     S.codes = p; p += align16(ns * FAST_W);
     S.explen = p; p += 256;
     S.win = p; p += align16(WIN + 16);
@@ -39,6 +43,7 @@ __device__ inline CSmem carve_csmem(uint8_t *p, int ns) {
     S.queue = reinterpret_cast<uint16_t *>(p); p += QCAP * 2;
     S.qlen = reinterpret_cast<uint16_t *>(p); p += QCAP * 2;
     S.qsort = reinterpret_cast<uint16_t *>(p); p += QCAP * 2;
+    S.qoff = reinterpret_cast<unsigned *>(p); p += QCAP * 4;
     S.chunk = reinterpret_cast<unsigned *>(p);
     return S;
 }
@@ -117,12 +122,26 @@ __device__ __forceinline__ int scan_starts(const uint8_t *win, int tile_len, int
                                            uint16_t *queue, int q0, int q1) {
     const int c0 = threadIdx.x * CHUNK;
     const int c1 = min(c0 + CHUNK, tile_len);
+    if (c0 >= c1) return 0;
+    // the predecessor bytes of the chunk's positions: window [a, b)
+    const int a = HEAD + c0 - 1, b = HEAD + c1 - 1;
     int cnt = 0;
-    for (int p = c0; p < c1; ++p) {
-        if (win[HEAD + p - 1] == '\n') {
-            int ord = base_ord + cnt;
-            if (queue && ord >= q0 && ord < q1) queue[ord - q0] = (uint16_t)(HEAD + p);
-            ++cnt;
+    for (int wa = a & ~3; wa < b; wa += 4) {
+        const unsigned x = *reinterpret_cast<const unsigned *>(win + wa) ^ 0x0a0a0a0au;
+        // exact per-byte zero test: bit 7 of each byte set iff byte == '\n'
+        unsigned z = ~(((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x | 0x7f7f7f7fu);
+        if (wa < a) z &= 0xffffffffu << (8 * (a - wa));
+        if (wa + 4 > b) z &= 0xffffffffu >> (8 * (wa + 4 - b));
+        if (queue) {
+            while (z) {
+                const int pos = wa + ((__ffs(z) - 1) >> 3);
+                const int ord = base_ord + cnt;
+                if (ord >= q0 && ord < q1) queue[ord - q0] = (uint16_t)(pos + 1);
+                ++cnt;
+                z &= z - 1;
+            }
+        } else {
+            cnt += __popc(z);
         }
     }
     return cnt;
@@ -207,10 +226,12 @@ __device__ __forceinline__ unsigned emit_chunk(const Job &job, const CSmem &S, l
     const int c1 = min(c0 + CHUNK, tile_len);
     unsigned esc = 0;
     int nxt = -1;
-    for (int x = c0; x < c1 || nxt >= 0; ++x) {
+    // warp-uniform trip count (lanes finish their last line at different x)
+    for (int x = c0; __any_sync(0xffffffffu, x < c1 || nxt >= 0); ++x) {
         const int p = HEAD + x;
         if (x < c1 && S.win[p - 1] == '\n') {
             const uint8_t first = S.dec[p];
+            nxt = first == D_DROP || first == D_GLOBAL ? -1 : p;
             if (first == D_GLOBAL) {
                 // out-of-smem line: its decisions live in the HBM arena
                 const unsigned aoff = S.dec[p + 1] | (S.dec[p + 2] << 8) | (S.dec[p + 3] << 16) |
@@ -233,10 +254,7 @@ __device__ __forceinline__ unsigned emit_chunk(const Job &job, const CSmem &S, l
                     }
                 }
                 og[w++] = '\n';
-                nxt = -1;
-                continue;
             }
-            nxt = first == D_DROP ? -1 : p;
         }
         if (p == nxt) {
             const uint8_t c = S.dec[p];
@@ -258,10 +276,73 @@ __device__ __forceinline__ unsigned emit_chunk(const Job &job, const CSmem &S, l
 }
 
 // ----------------------------------------------------------------------------
+// compress emit, one line per lane (the tile's lines were parsed in one
+// round): warps take the same length-sorted groups of 32 lines as the parse,
+// so the lanes' decision walks have similar lengths.  w = the line's output
+// offset (tile-local when staged).
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ unsigned emit_lines(const Job &job, const CSmem &S, long long ws, int nq,
+                                               int *grp, uint8_t *o, unsigned long long base) {
+    unsigned esc = 0;
+    for (;;) {
+        int g = 0;
+        if ((threadIdx.x & 31) == 0) g = atomicAdd(grp, 1);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g * 32 >= nq) break;
+        const int r = g * 32 + (threadIdx.x & 31);
+        __syncwarp();
+        if (r < nq) {
+            const int q = S.qsort[r];
+            const int p = S.queue[q];
+            unsigned long long w = base + S.qoff[q];
+            const uint8_t first = S.dec[p];
+            if (first == D_GLOBAL) {
+                const unsigned aoff = S.dec[p + 1] | (S.dec[p + 2] << 8) | (S.dec[p + 3] << 16) |
+                                      ((unsigned)S.dec[p + 4] << 24);
+                const uint8_t *blk = job.arena + ((long long)aoff << 4);
+                const ArenaHdr *h = reinterpret_cast<const ArenaHdr *>(blk);
+                const uint8_t *bytes = h->bytes_off < 0 ? job.in + ws + p : job.arena + h->bytes_off;
+                const uint8_t *dec = job.arena + h->dec_off;
+                for (long long i = 0; i < h->n_pre;) {
+                    const uint8_t c = dec[i];
+                    if (c == D_ESC) {
+                        o[w++] = 0x20;
+                        o[w++] = bytes[i];
+                        ++esc;
+                        ++i;
+                    } else {
+                        o[w++] = c;
+                        i += S.explen[c];
+                    }
+                }
+                o[w++] = '\n';
+            } else if (first != D_DROP) {
+                for (int i = p;;) {
+                    const uint8_t c = S.dec[i];
+                    if (c == D_END) break;
+                    if (c == D_ESC) {
+                        o[w++] = 0x20;
+                        o[w++] = S.win[i];
+                        ++esc;
+                        ++i;
+                    } else {
+                        o[w++] = c;
+                        i += S.explen[c];
+                    }
+                }
+                o[w++] = '\n';
+            }
+        }
+        __syncwarp();
+    }
+    return esc;
+}
+
+// ----------------------------------------------------------------------------
 // compress: one persistent CTA per SM, tiles in ticket order.
 // W = fast-path window (max pattern length) or 0 for the generic trie walk.
 // ----------------------------------------------------------------------------
-template <int W>
+template <int W, bool T2>
 __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ unsigned long long s_tmp64[NWARP];
@@ -269,28 +350,34 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
     __shared__ unsigned s_hist[256];
     __shared__ uint8_t s_lut[256];
     __shared__ long long s_tile;
-    __shared__ int s_err_ord, s_global;
+    __shared__ int s_err_ord, s_global, s_grp;
+    __shared__ unsigned long long s_wmax, s_wsum, s_wmin, s_ngrp;
     __shared__ unsigned long long s_pre_out, s_pre_lines;
     __shared__ unsigned s_kept, s_esc, s_skip, s_flag;
 
-    const CSmem S = carve_csmem(smem, W ? tb.n_states : 0);
+    const CSmem S = carve_csmem(smem, W ? tb.n_states : 0, T2 ? tb.n_windows : 0);
     {
         const int ns = W ? tb.n_states : 0;
         if (W) {
-            const uint4 *src = reinterpret_cast<const uint4 *>(tb.dfa);
+            const uint4 *src = reinterpret_cast<const uint4 *>(T2 ? tb.dfa2 : tb.dfa);
             uint4 *dst = reinterpret_cast<uint4 *>(S.dfa);
             for (int k = threadIdx.x; k < align16(ns * NCOL * 2) / 16; k += NT) dst[k] = src[k];
             for (int k = threadIdx.x; k < ns * FAST_W; k += NT) S.codes[k] = tb.codes[k];
         }
+        if (T2)
+            for (int k = threadIdx.x; k < tb.n_windows * T2_MASKS; k += NT) S.t2[k] = tb.t2[k];
         for (int k = threadIdx.x; k < 256; k += NT) {
             S.explen[k] = tb.exp_len[k];
             s_lut[k] = tok_bits(k);
         }
     }
     const int tid = threadIdx.x;
+    PhaseClock pc;
+    pc.start();
 
     for (;;) {
         __syncthreads();
+        pc.mark(job, 5);  // end of previous tile / table load
         if (tid == 0) {
             s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
             s_err_ord = 0x7fffffff;
@@ -315,6 +402,7 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
         int tile_lines;
         const int my_off = block_exscan<int>(my_cnt, s_tmp32, tile_lines);
 
+        pc.mark(job, 7);  // ticket, window load, line-start scan
         // ---- parse phase, in rounds of QCAP lines ----
         for (int q0 = 0; q0 < tile_lines; q0 += QCAP) {
             const int nq = min(QCAP, tile_lines - q0);
@@ -343,41 +431,74 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                 const unsigned r = atomicAdd(&s_hist[255 - min(len, 255)], 1u);
                 S.qsort[r] = (uint16_t)q;
             }
+            if (tid == 0) {
+                s_grp = 0;
+                s_wmax = s_wsum = s_ngrp = 0;
+                s_wmin = ~0ull;
+            }
             __syncthreads();
-            for (int r = tid; r < nq; r += NT) {
-                const int q = S.qsort[r];
-                const int ord = q0 + q;
-                const int p = S.queue[q];
-                const int qlen = S.qlen[q];
+            pc.mark(job, 7);  // queue, lengths, sort
+            const long long wt0 = clock64();
+            int my_groups = 0;
+            // warps pull groups of 32 lines, longest first (LPT scheduling).
+            // Independent thread scheduling does not reconverge lanes on its
+            // own: every divergent step below ends in __syncwarp() so the 32
+            // lanes enter the parse together.
+            for (;;) {
+                int g = 0;
+                if ((tid & 31) == 0) g = atomicAdd(&s_grp, 1);
+                g = __shfl_sync(0xffffffffu, g, 0);
+                if (g * 32 >= nq) break;
+                ++my_groups;
+                const int r = g * 32 + (tid & 31);
+                const bool valid = r < nq;
+                int ord = 0, p = HEAD, qlen = 0, q = 0;
+                if (valid) {
+                    q = S.qsort[r];
+                    ord = q0 + q;
+                    p = S.queue[q];
+                    qlen = S.qlen[q];
+                }
                 const int chunk_owner = (p - HEAD) / CHUNK;
                 int kind = E_NONE;
                 long long size = 0;
-                bool global_line = qlen == 0xffff;
-                if (!global_line) {
-                    uint8_t *s = S.win + p;
-                    uint8_t *d = S.dec + p;
-                    int n_l = qlen;
+                bool global_line = valid && qlen == 0xffff;
+                bool do_dp = valid && !global_line;
+                uint8_t *s = S.win + p;
+                uint8_t *d = S.dec + p;
+                int n_l = qlen;
+                // ---- CR policy + ring renumbering ----
+                // renumber_fast is called by all 32 lanes (warp-uniform loops)
+                int rn_k = E_NONE, rn_len = 0, rn_off = -1;
+                unsigned long long rn_ids[2] = {0, 0};
+                const bool rn = do_dp && job.preprocess;
+                rn_k = renumber_fast(s, rn ? n_l : 0, s_lut, d, &rn_len, &rn_off, rn_ids);
+                if (do_dp) {
                     if (job.preprocess) {
-                        int eoff = -1;
-                        unsigned long long ids[2] = {0, 0};
-                        int k = renumber_fast(s, n_l, s_lut, &eoff, ids);
-                        if (k == RN_FALLBACK) {
+                        int eoff = rn_off;
+                        unsigned long long ids[2] = {rn_ids[0], rn_ids[1]};
+                        int nlf = rn_len;
+                        int k = rn_k;
+                        if (k == E_NONE) {
+                            n_l = nlf;
+                        } else if (k == RN_FALLBACK) {
                             // pristine bytes, then the general routine
-                            const uint8_t *g = job.in + ws + p;
-                            for (int j = 0; j < n_l; ++j) s[j] = g[j];
+                            const uint8_t *g8 = job.in + ws + p;
+                            for (int j = 0; j < n_l; ++j) s[j] = g8[j];
                             int nl2 = n_l;
                             k = preprocess_line(s, n_l, d, s, &nl2, &eoff, ids);
                             if (k == E_NONE) n_l = nl2;
                         }
                         if (k == -1) {
                             global_line = true;
+                            do_dp = false;
                         } else if (k != E_NONE) {
                             if (k == E_CR) {
                                 kind = E_CR;
                             } else if (job.lenient) {
                                 // keep the raw line (pipeline.py:108-115)
-                                const uint8_t *g = job.in + ws + p;
-                                for (int j = 0; j < n_l; ++j) s[j] = g[j];
+                                const uint8_t *g8 = job.in + ws + p;
+                                for (int j = 0; j < n_l; ++j) s[j] = g8[j];
                                 atomicAdd(&s_flag, 1u);
                             } else {
                                 kind = k;
@@ -387,21 +508,26 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                         for (int j = 0; j < n_l; ++j)
                             if (s[j] == '\r') { kind = E_CR; break; }
                     }
-                    if (!global_line) {
-                        if (kind != E_NONE) {
-                            d[0] = D_DROP;
-                            if (job.lenient) atomicAdd(&s_skip, 1u);
-                            else atomicMin(&s_err_ord, ord);
-                        } else {
-                            if constexpr (W > 0)
-                                size = dp_fast<W>(s, n_l, d, S.dfa, S.codes) + 1;
-                            else {
-                                long long ring[128];
-                                size = dp_generic(s, n_l, d, tb, ring) + 1;
-                            }
-                        }
+                    if (do_dp && kind != E_NONE) {
+                        d[0] = D_DROP;
+                        do_dp = false;
+                        if (job.lenient) atomicAdd(&s_skip, 1u);
+                        else atomicMin(&s_err_ord, ord);
                     }
                 }
+                __syncwarp();
+                // ---- min-cost parse (converged) ----
+                if (do_dp) {
+                    if constexpr (T2) {
+                        size = dp_t2(s, n_l, d, S.dfa, S.t2, S.codes) + 1;
+                    } else if constexpr (W > 0) {
+                        size = dp_fast<W>(s, n_l, d, S.dfa, S.codes) + 1;
+                    } else {
+                        long long ring[128];
+                        size = dp_generic(s, n_l, d, tb, ring) + 1;
+                    }
+                }
+                __syncwarp();
                 if (global_line) {
                     // line in HBM: find its end, process in the arena
                     const long long gs = ws + p;
@@ -412,7 +538,6 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                     unsigned long long ids[2] = {0, 0};
                     long long cost = compress_line_global(job, tb, gs, ge - gs, &aoff, &kind, &eoff, ids);
                     s_global = 1;
-                    uint8_t *d = S.dec + p;
                     if (kind == -2) {
                         d[0] = D_DROP;  // arena exhausted; host re-runs
                         kind = E_NONE;
@@ -429,39 +554,81 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                         size = cost + 1;
                     }
                 }
+                if (valid) S.qoff[q] = (unsigned)size;
                 if (size) {
                     atomicAdd(&S.chunk[chunk_owner], (unsigned)size);
                     atomicAdd(&s_kept, 1u);
                 }
+                __syncwarp();
             }
+            if (job.timing && (tid & 31) == 0) {
+                const unsigned long long dt = (unsigned long long)(clock64() - wt0);
+                atomicMax(&s_wmax, dt);
+                atomicMin(&s_wmin, dt);
+                atomicAdd(&s_wsum, dt);
+                atomicAdd(&s_ngrp, (unsigned long long)my_groups);
+            }
+            pc.mark(job, 6);  // thread 0's own parse work
             __syncthreads();
+            pc.mark(job, 2);  // waiting for the slowest warp
+            if (job.timing && tid == 0) {
+                atomicAdd(&job.ctl->phase[3], s_wmax);  // slot 3: max warp parse time
+                atomicAdd(&job.ctl->phase[4], s_wmin);  // slot 4: min warp parse time
+                atomicAdd(&job.ctl->phase[0], s_wsum / NWARP);  // slot 0: avg warp parse
+                atomicAdd(&job.ctl->phase[1], s_ngrp);  // slot 1: groups per tile
+            }
         }
 
-        // ---- tile output size, look-back ----
+        // ---- tile output size; publish the aggregate, emit to smem while
+        // predecessors resolve, then the look-back ----
         unsigned long long tile_out;
         const unsigned long long my_out = S.chunk[tid];
         const unsigned long long my_out_off = block_exscan<unsigned long long>(my_out, s_tmp64, tile_out);
+        const bool one_round = tile_lines <= QCAP;
+        if (one_round) {
+            // per-line output offsets: exclusive scan of S.qoff[0, tile_lines)
+            const int per = (tile_lines + NT - 1) / NT;
+            const int l0 = min(tid * per, tile_lines), l1 = min(l0 + per, tile_lines);
+            unsigned sum = 0;
+            for (int l = l0; l < l1; ++l) sum += S.qoff[l];
+            unsigned tot;
+            unsigned run = block_exscan<unsigned>(sum, reinterpret_cast<unsigned *>(s_tmp32), tot);
+            for (int l = l0; l < l1; ++l) {
+                const unsigned v = S.qoff[l];
+                S.qoff[l] = run;
+                run += v;
+            }
+            if (tid == 0) s_grp = 0;
+            __syncthreads();
+        }
+        if (tid == 0) lookback_publish(job.ts, t, tile_out, (unsigned long long)tile_lines);
+        const bool staged = !s_global && tile_out <= (unsigned long long)OUTCAP;
+        if (staged) {
+            const unsigned esc = one_round ? emit_lines(job, S, ws, tile_lines, &s_grp, S.out, 0)
+                                           : emit_chunk<true>(job, S, ws, tile_len, my_out_off, S.out);
+            if (esc) atomicAdd(&s_esc, esc);
+        }
+        pc.mark(job, 5);  // thread 0: publish + its own emit
         if (tid < 32) {
             unsigned long long po, pl;
-            lookback(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
+            lookback_resolve(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
             if (tid == 0) {
                 s_pre_out = po;
                 s_pre_lines = pl;
             }
         }
+        __syncthreads();
+        pc.mark(job, 7);  // look-back resolve + wait for the slowest emitter
+        const unsigned long long pre_out = s_pre_out;
+        const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
         if (tid == 0) {
             atomicAdd(&job.ctl->total_out, tile_out);
             atomicAdd(&job.ctl->lines, (unsigned long long)s_kept);
             atomicAdd(&job.ctl->in_lines, (unsigned long long)tile_lines);
             if (s_skip) atomicAdd(&job.ctl->skipped, (unsigned long long)s_skip);
             if (s_flag) atomicAdd(&job.ctl->flagged, (unsigned long long)s_flag);
-            if (s_pre_out + tile_out > (unsigned long long)job.out_cap)
-                atomicOr(&job.ctl->overflow, 1ull);
+            if (!fits) atomicOr(&job.ctl->overflow, 1ull);
         }
-        __syncthreads();
-        const unsigned long long pre_out = s_pre_out;
-        const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
-        const bool staged = fits && !s_global && tile_out <= (unsigned long long)OUTCAP;
 
         // ---- strict error: re-derive details of the first bad line ----
         if (tid == 0 && s_err_ord != 0x7fffffff) {
@@ -477,18 +644,15 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
             bool cr = false;
             for (long long k = gs; k < ge; ++k) cr |= job.in[k] == '\r';
             if (!cr && job.preprocess) {
-                // recompute from the pristine input (marks + output in the
-                // staging area, unused until the emit)
+                // recompute from the pristine input (marks + output in HBM
+                // scratch from the arena)
                 int nl2, eoff = -1;
                 unsigned long long ids[2] = {0, 0};
                 const long long n_l = ge - gs;
-                uint8_t *tmp = S.out;  // n_l+1 marks + 3n_l+3 out
-                if (4 * n_l + 4 > OUTCAP) {
-                    const unsigned long long need = 4 * n_l + 4;
-                    unsigned long long a = atomicAdd(&job.ctl->arena_used, need);
-                    tmp = a + need <= (unsigned long long)job.arena_cap ? job.arena + a : nullptr;
-                    if (!tmp) atomicOr(&job.ctl->overflow, 2ull);
-                }
+                const unsigned long long need = 4 * n_l + 4;
+                unsigned long long a = atomicAdd(&job.ctl->arena_used, need);
+                uint8_t *tmp = a + need <= (unsigned long long)job.arena_cap ? job.arena + a : nullptr;
+                if (!tmp) atomicOr(&job.ctl->overflow, 2ull);
                 int k = tmp ? preprocess_line(job.in + gs, (int)n_l, tmp, tmp + n_l + 1, &nl2, &eoff, ids)
                             : E_NONE;
                 e.kind = k;
@@ -503,16 +667,18 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
         }
         if (!fits) continue;
 
-        // ---- emit ----
-        __syncthreads();
-        {
-            unsigned esc;
-            if (staged) esc = emit_chunk<true>(job, S, ws, tile_len, my_out_off, S.out);
-            else esc = emit_chunk<false>(job, S, ws, tile_len, pre_out + my_out_off, job.out);
+        // ---- store (staged) or emit straight to HBM (direct) ----
+        if (staged) {
+            store_out(job.out + pre_out, S.out, (int)tile_out);
+            pc.mark(job, 5);
+        } else {
+            if (tid == 0) s_grp = 0;
+            __syncthreads();
+            const unsigned esc = one_round ? emit_lines(job, S, ws, tile_lines, &s_grp, job.out, pre_out)
+                                           : emit_chunk<false>(job, S, ws, tile_len, pre_out + my_out_off, job.out);
             if (esc) atomicAdd(&s_esc, esc);
         }
         __syncthreads();
-        if (staged) store_out(job.out + pre_out, S.out, (int)tile_out);
         if (tid == 0 && s_esc) atomicAdd(&job.ctl->escapes, (unsigned long long)s_esc);
     }
 }
@@ -575,7 +741,7 @@ __device__ __forceinline__ void dec_emit_chunk(const Job &job, const DSmem &S, l
     const int c0 = threadIdx.x * CHUNK;
     const int c1 = min(c0 + CHUNK, tile_len);
     bool in = false, esc_next = false;
-    for (int x = c0; x < c1 || in; ++x) {
+    for (int x = c0; __any_sync(0xffffffffu, x < c1 || in); ++x) {
         const int p = HEAD + x;
         if (x < c1 && S.win[p - 1] == '\n') {
             const uint8_t st = S.stat[ord++];
@@ -587,7 +753,6 @@ __device__ __forceinline__ void dec_emit_chunk(const Job &job, const DSmem &S, l
                 while (ge < job.n && job.in[ge] != '\n') ++ge;
                 w += decode_fill(job.in + gs, ge - gs, S.explen, S.expoff, S.expflat, job.out + w);
                 job.out[w++] = '\n';
-                continue;
             }
         }
         if (!in) continue;
@@ -664,9 +829,18 @@ __global__ void __launch_bounds__(NT, 1) decompress_tiles(Job job, Tables tb) {
             if (my_cnt) scan_starts(win, tile_len, my_off, queue, q0, q1);
             if (tid == 0) s_qhead = 0;
             __syncthreads();
+            // warps take 32 consecutive records at a time; lanes reconverge
+            // (__syncwarp) before the per-record size/validate walk
             for (;;) {
-                const int q = atomicAdd(&s_qhead, 1);
-                if (q >= q1 - q0) break;
+                int g = 0;
+                if ((tid & 31) == 0) g = atomicAdd(&s_qhead, 1);
+                g = __shfl_sync(0xffffffffu, g, 0);
+                if (g * 32 >= q1 - q0) break;
+                const int q = g * 32 + (tid & 31);
+                if (q >= q1 - q0) {
+                    __syncwarp();
+                    continue;
+                }
                 const int ord = q0 + q;
                 const int p = queue[q];
                 int end = (q + 1 < q1 - q0) ? queue[q + 1] - 1 : find_end(win, p, win_len, hits_eof);
@@ -682,6 +856,7 @@ __global__ void __launch_bounds__(NT, 1) decompress_tiles(Job job, Tables tb) {
                     n_r = ge - gs;
                     s_global = 1;
                 }
+                __syncwarp();
                 long long m = 0, ep = -1;
                 int code = 0;
                 unsigned esc = 0;
