@@ -77,6 +77,7 @@ struct zs_ctx {
     int fast_w = 0;
     DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2;
     int no_t2 = 0;  // debug: force the key-window DP
+    int no_ip = 0;  // debug: force the decision-array kernel
     // per-slot (double-buffered) work buffers
     DevBuf ctl[2], ts[2], terr[2], in[2], out[2], arena[2];  // arena: per slot
     // shim scratch
@@ -308,7 +309,9 @@ BatchKernel batch_kernel(int w) {
 // one whole-buffer launch (device pointers) on `slot`'s buffers and stream
 int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, long long n,
                   uint8_t *d_out, long long out_cap, int flags, bool timed) {
-    const long long nt = (n + TILE - 1) / TILE;
+    const bool ip = compress && ctx->fast_w && ctx->ht.t2_ok && !ctx->no_t2 && !ctx->no_ip;
+    const long long tile = ip ? CTILE : TILE;
+    const long long nt = (n + tile - 1) / tile;
     cudaStream_t st = ctx->stream[slot];
     if (ctx->ctl[slot].reserve(sizeof(Ctl)) || ctx->ts[slot].reserve(sizeof(TileState) * (nt + 1)) ||
         ctx->terr[slot].reserve(sizeof(TileErr) * (nt + 1)))
@@ -336,7 +339,11 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
     if (nt > 0) {
         const int grid = (int)std::min<long long>(nt, ctx->n_sm);
         if (timed) CK(cudaEventRecord(ctx->ev0, st));
-        if (compress) {
+        if (ip) {
+            const int smem = ip_smem_bytes(ctx->tb.n_states, ctx->ht.n_windows);
+            CK(set_smem(compress_tiles_ip, smem));
+            compress_tiles_ip<<<grid, NT, smem, st>>>(job, ctx->tb);
+        } else if (compress) {
             const bool t2 = ctx->fast_w && ctx->ht.t2_ok && !ctx->no_t2;
             TileKernel k = compress_kernel(ctx->fast_w, t2);
             const int smem = compress_smem_bytes(ctx->fast_w ? ctx->tb.n_states : 0,
@@ -734,7 +741,8 @@ int zs_build_t2_host(const int32_t *children, const int16_t *term_code, int32_t 
 
 int zs_set_transducer(zs_ctx *ctx, int on) {
     if (!ctx) return ZS_E_ARG;
-    ctx->no_t2 = on ? 0 : 1;
+    ctx->no_t2 = (on & 1) ? 0 : 1;  // bit 0: transducer parse
+    ctx->no_ip = (on & 2) ? 0 : 1;  // bit 1: in-place kernel (needs the transducer)
     return ZS_OK;
 }
 

@@ -490,6 +490,44 @@ __host__ __device__ int preprocess_line(const uint8_t *buf, int n, uint8_t *mark
 // line bytes may be partially rewritten.
 // ----------------------------------------------------------------------------
 constexpr int RN_FALLBACK = -4;
+
+// Tokenizer transducer (smiles.py:83-137 as an 8-state machine).  Entry =
+// tk[state << 8 | byte]: bits 0-2 next state, TK_RING = a ring-closure token
+// starts here, TK_CR = '\r', TK_ENTER_BR / TK_ENTER_PCT = this byte is a '['
+// opening a bracket atom / a '%' starting a %nn token (outside brackets).
+enum : unsigned {
+    TK_OUT0 = 0, TK_OUT1 = 1,  // outside brackets; ring_ok = 0 / 1
+    TK_IN = 2,                 // inside a bracket atom
+    TK_ERR = 3,                // '%' not followed by two digits (sticky)
+    TK_P1R = 4, TK_P2R = 5,    // after '%' / '%d' of a ring-closure %nn token
+    TK_P1O = 6, TK_P2O = 7,    // ... of an Other %nn token
+    TK_RING = 8, TK_CR = 16, TK_ENTER_BR = 32, TK_ENTER_PCT = 64
+};
+
+ZS_HD uint8_t tk_entry(unsigned st, unsigned b) {
+    const uint8_t c = tok_class(b);
+    const unsigned cr = c == C_CR ? TK_CR : 0u;
+    switch (st) {
+    case TK_OUT0:
+    case TK_OUT1: {
+        const bool ok = st == TK_OUT1;
+        switch (c) {
+        case C_LBR: return TK_IN | TK_ENTER_BR;
+        case C_PCT: return (ok ? TK_P1R | TK_RING : TK_P1O) | TK_ENTER_PCT;
+        case C_DIGIT: return ok ? TK_OUT1 | TK_RING : TK_OUT0;
+        case C_ATOM:
+        case C_BOND: return TK_OUT1;
+        default: return TK_OUT0 | cr;  // ( ) . stray ] and any other byte
+        }
+    }
+    case TK_IN: return b == ']' ? TK_OUT1 : TK_IN | cr;
+    case TK_P1R: return c == C_DIGIT ? TK_P2R : TK_ERR | cr;
+    case TK_P2R: return c == C_DIGIT ? TK_OUT1 : TK_ERR | cr;
+    case TK_P1O: return c == C_DIGIT ? TK_P2O : TK_ERR | cr;
+    case TK_P2O: return c == C_DIGIT ? TK_OUT0 : TK_ERR | cr;
+    default: return TK_ERR | cr;
+    }
+}
 enum : uint8_t { K_OKP = 1, K_DIG = 2, K_PCT = 4, K_LBR = 8, K_CR = 16, K_SPECIAL = K_PCT | K_LBR | K_CR };
 
 ZS_HD uint8_t tok_bits(unsigned b) {
@@ -513,67 +551,50 @@ ZS_HD int chain_next(const uint8_t *marks, int i, unsigned step) {
 ZS_HD int renumber_fast(uint8_t *s, int n, const uint8_t *lut, uint8_t *marks,
                         int *new_len, int *err_off, unsigned long long ids[2]) {
     int res = E_NONE;
-    // ---- 1. tokenize, chain the ring tokens ----
-    // Branch-free per byte (selects + one predicated store), so a warp pays
-    // one path per trip; only '%' tokens and chain hops branch (rare).
-    int first = -1, last = -1, n_pct = 0, br = -1;  // br: open '[' position, -1 outside
-    unsigned ring_ok = 0, crs = 0;
-    const SmemBytes sb(s), lb(lut);
-    for (int i = 0; ZS_ANY(i < n && res == E_NONE);) {
-        if (i >= n || res != E_NONE) continue;
-        const unsigned b = sb.ld(i);
-        const unsigned c = lb.ld(b);
-        crs |= c;
-        const bool inside = br >= 0;
-        unsigned ring = (inside ? 0u : ring_ok) & (c >> 1);  // K_DIG = 2
-        int adv = 1;
-        if (!inside && (c & K_PCT)) {
-            // '%': two digits must follow, in any context
-            if (i + 2 >= n || !is_digit(sb.ld(i + 1)) || !is_digit(sb.ld(i + 2))) {
-                res = E_PERCENT;
-                *err_off = i;
-                continue;
-            }
-            ring = ring_ok;
-            n_pct += ring;
-            adv = 3;
-        }
-        const bool rbr = inside && b == ']';
-        br = inside ? (rbr ? -1 : br) : ((c & K_LBR) ? i : -1);
-        ring_ok = inside ? (ring_ok | rbr) : (ring | (c & K_OKP));
-        if (ring && last >= 0 && i - last > 254) {  // hop nodes (not tokens)
-            while (i - last > 254) {
-                marks[last] = 255;
-                last += 254;
-            }
-        }
-        if (ring && last >= 0) marks[last] = (uint8_t)(i - last);
-        first = (ring && first < 0) ? i : first;
-        last = ring ? i : last;
-        i += adv;
+    // ---- 1. tokenize (one table lookup per byte) ----
+    // Ring-token positions go to a u16 list in the line's scratch (marks,
+    // 2-byte aligned): a predicated store per byte, no branch.  A line with
+    // more ring tokens than the list holds (> ~n/2) takes the fallback.
+    uint16_t *list = reinterpret_cast<uint16_t *>(reinterpret_cast<uintptr_t>(marks + 1) & ~(uintptr_t)1);
+    const int cap = (n - 1) / 2;
+    int cnt = 0, br = -1, pct = -1, n_pct = 0;
+    unsigned st = TK_OUT0, crs = 0;
+    const SmemBytes sb(s), tk(lut);
+    for (int i = 0; ZS_ANY(i < n); ++i) {
+        if (i >= n) continue;
+        const unsigned e = tk.ld((st << 8) | sb.ld(i));
+        st = e & 7u;
+        crs |= e;
+        br = (e & TK_ENTER_BR) ? i : br;
+        pct = (e & TK_ENTER_PCT) ? i : pct;
+        const bool ring = e & TK_RING;
+        n_pct += ring & ((e & TK_ENTER_PCT) != 0);
+        if (ring && cnt < cap) list[cnt] = (uint16_t)i;
+        cnt += ring;
     }
-    if (res == E_PERCENT)  // the scan stopped early: look for a '\r' in the rest
-        for (int k = 0; k < n; ++k) crs |= s[k] == '\r' ? K_CR : 0u;
-    if (crs & K_CR) {
+    if (crs & TK_CR) {
         res = E_CR;  // '\r' anywhere in the line takes precedence (pipeline.py:102-107)
-    } else if (res == E_NONE && br >= 0) {
+    } else if (st == TK_ERR || st >= TK_P1R) {
+        *err_off = pct;  // '%' without two digits (the first such '%' wins: ERR is sticky)
+        res = E_PERCENT;
+    } else if (st == TK_IN) {
         *err_off = br;  // '[' never closed
         res = E_BRACKET;
+    } else if (cnt > cap) {
+        res = RN_FALLBACK;
     }
-    if (res == E_NONE && first >= 0) marks[last] = 0;
-    // ---- 2. pair + colour along the chain ----
+    // ---- 2. pair + colour along the list ----
     unsigned oid = 0xffffffffu;  // 4 slots: open ring id per byte, 0xff = free
     int opos[4] = {0, 0, 0, 0};
     int lc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) lc[k] = -1;
-    int node = res == E_NONE ? first : -1;
-    while (ZS_ANY(node >= 0)) {
-        if (node < 0) continue;
-        const int i = node;
-        const unsigned step = marks[i];
-        const bool pct = s[i] == '%';
-        const unsigned rid = pct ? (s[i + 1] - '0') * 10u + (s[i + 2] - '0') : s[i] - '0';
+    const int ntok = res == E_NONE ? cnt : 0;
+    for (int t = 0; ZS_ANY(t < ntok && res == E_NONE); ++t) {
+        if (t >= ntok || res != E_NONE) continue;
+        const int i = list[t];
+        const bool pct_tok = sb.ld(i) == '%';
+        const unsigned rid = pct_tok ? (sb.ld(i + 1) - '0') * 10u + (sb.ld(i + 2) - '0') : sb.ld(i) - '0';
         int slot = -1, free_slot = -1;
 #pragma unroll
         for (int k = 3; k >= 0; --k) {
@@ -584,7 +605,6 @@ ZS_HD int renumber_fast(uint8_t *s, int n, const uint8_t *lut, uint8_t *marks,
         if (slot < 0) {
             if (free_slot < 0) {
                 res = RN_FALLBACK;
-                node = -1;
                 continue;
             }
 #pragma unroll
@@ -603,16 +623,16 @@ ZS_HD int renumber_fast(uint8_t *s, int n, const uint8_t *lut, uint8_t *marks,
                 if (lc[k] <= o) col = k;
             if (col == 8) {
                 res = RN_FALLBACK;
-                node = -1;
                 continue;
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 if (k == col) lc[k] = i;
+            // colour digits: 1-byte tokens in place, '%nn' tokens in their
+            // first digit slot (compacted below)
             s[o + (s[o] == '%')] = (uint8_t)('0' + col);
-            s[i + pct] = (uint8_t)('0' + col);
+            s[i + pct_tok] = (uint8_t)('0' + col);
         }
-        node = step ? chain_next(marks, i, step) : -1;
     }
     if (res == E_NONE && oid != 0xffffffffu) {
         ids[0] = ids[1] = 0;
@@ -626,21 +646,175 @@ ZS_HD int renumber_fast(uint8_t *s, int n, const uint8_t *lut, uint8_t *marks,
     // ---- 3. compaction of '%nn' ring tokens (rare: no warp-uniform loop) ----
     *new_len = n;
     if (res == E_NONE && n_pct) {
-        int w = first, r = first;
-        for (int i = first;;) {
+        int w = list[0], r = list[0];
+        for (int t = 0; t < cnt; ++t) {
+            const int i = list[t];
             while (r < i) s[w++] = s[r++];
-            const unsigned step = marks[i];
             if (s[i] == '%') {
                 s[w++] = s[i + 1];
                 r = i + 3;
             }
-            if (!step) break;
-            i = chain_next(marks, i, step);
         }
         while (r < n) s[w++] = s[r++];
         *new_len = w;
     }
     return res;
+}
+
+// ----------------------------------------------------------------------------
+// Bitmap variant of renumber_fast for the in-place compress kernel: the
+// ring-token starts are set in a shared bitmap (bit = window position,
+// atomicOr since neighbouring lines share words) instead of a per-line list,
+// so the line needs no scratch bytes.  bit0 = window position of s[0].
+// Same contract as renumber_fast (all 32 lanes call together).
+// ----------------------------------------------------------------------------
+ZS_HD void bm_set(unsigned *bm, int pos) {
+#ifdef __CUDA_ARCH__
+    atomicOr(&bm[pos >> 5], 1u << (pos & 31));
+#else
+    bm[pos >> 5] |= 1u << (pos & 31);
+#endif
+}
+
+// next set bit at or after pos within [pos, end); -1 if none
+ZS_HD int bm_next(const unsigned *bm, int pos, int end) {
+    while (pos < end) {
+        unsigned w = bm[pos >> 5] >> (pos & 31);
+        if (w) {
+            const int q = pos + ffs64_(w) - 1;
+            return q < end ? q : -1;
+        }
+        pos = (pos | 31) + 1;
+    }
+    return -1;
+}
+
+ZS_HD int renumber_bm(uint8_t *s, int n, const uint8_t *lut, unsigned *rbits, int bit0,
+                      int *new_len, int *err_off, unsigned long long ids[2]) {
+    int res = E_NONE;
+    // ---- 1. tokenize (one table lookup per byte); mark ring-token starts ----
+    int cnt = 0, br = -1, pct = -1, n_pct = 0;
+    unsigned st = TK_OUT0, crs = 0;
+    const SmemBytes sb(s), tk(lut);
+    for (int i = 0; ZS_ANY(i < n); ++i) {
+        if (i >= n) continue;
+        const unsigned e = tk.ld((st << 8) | sb.ld(i));
+        st = e & 7u;
+        crs |= e;
+        br = (e & TK_ENTER_BR) ? i : br;
+        pct = (e & TK_ENTER_PCT) ? i : pct;
+        const bool ring = e & TK_RING;
+        n_pct += ring & ((e & TK_ENTER_PCT) != 0);
+        if (ring) bm_set(rbits, bit0 + i);
+        cnt += ring;
+    }
+    if (crs & TK_CR) {
+        res = E_CR;  // '\r' anywhere in the line takes precedence (pipeline.py:102-107)
+    } else if (st == TK_ERR || st >= TK_P1R) {
+        *err_off = pct;  // '%' without two digits (the first such '%' wins: ERR is sticky)
+        res = E_PERCENT;
+    } else if (st == TK_IN) {
+        *err_off = br;  // '[' never closed
+        res = E_BRACKET;
+    }
+    // ---- 2. pair + colour, tokens in order ----
+    unsigned oid = 0xffffffffu;  // 4 slots: open ring id per byte, 0xff = free
+    int opos[4] = {0, 0, 0, 0};
+    int lc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) lc[k] = -1;
+    const int ntok = res == E_NONE ? cnt : 0;
+    int cur = bit0 - 1;
+    for (int t = 0; ZS_ANY(t < ntok && res == E_NONE); ++t) {
+        if (t >= ntok || res != E_NONE) continue;
+        cur = bm_next(rbits, cur + 1, bit0 + n);
+        const int i = cur - bit0;
+        const bool pct_tok = sb.ld(i) == '%';
+        const unsigned rid = pct_tok ? (sb.ld(i + 1) - '0') * 10u + (sb.ld(i + 2) - '0') : sb.ld(i) - '0';
+        int slot = -1, free_slot = -1;
+#pragma unroll
+        for (int k = 3; k >= 0; --k) {
+            const unsigned v = (oid >> (8 * k)) & 0xffu;
+            if (v == rid) slot = k;
+            if (v == 0xffu) free_slot = k;
+        }
+        if (slot < 0) {
+            if (free_slot < 0) {
+                res = RN_FALLBACK;
+                continue;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k == free_slot) opos[k] = i;
+            oid = (oid & ~(0xffu << (8 * free_slot))) | (rid << (8 * free_slot));
+        } else {
+            int o = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k == slot) o = opos[k];
+            oid |= 0xffu << (8 * slot);
+            int col = 8;
+#pragma unroll
+            for (int k = 7; k >= 0; --k)
+                if (lc[k] <= o) col = k;
+            if (col == 8) {
+                res = RN_FALLBACK;
+                continue;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k == col) lc[k] = i;
+            s[o + (s[o] == '%')] = (uint8_t)('0' + col);
+            s[i + pct_tok] = (uint8_t)('0' + col);
+        }
+    }
+    if (res == E_NONE && oid != 0xffffffffu) {
+        ids[0] = ids[1] = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned v = (oid >> (8 * k)) & 0xffu;
+            if (v != 0xffu) ids[v >> 6] |= 1ull << (v & 63);
+        }
+        res = E_UNPAIRED;
+    }
+    // ---- 3. compaction of '%nn' ring tokens (rare) ----
+    *new_len = n;
+    if (res == E_NONE && n_pct) {
+        int w = -1, r = 0;
+        for (int q = bm_next(rbits, bit0, bit0 + n); q >= 0; q = bm_next(rbits, q + 1, bit0 + n)) {
+            const int i = q - bit0;
+            if (w < 0) w = r = i;
+            while (r < i) s[w++] = s[r++];
+            if (s[i] == '%') {
+                s[w++] = s[i + 1];
+                r = i + 3;
+            }
+        }
+        while (r < n) s[w++] = s[r++];
+        *new_len = w;
+    }
+    return res;
+}
+
+// dp_t2 writing its decisions over the line bytes (each byte is read once,
+// right to left, before its decision replaces it).  Escapes keep the literal
+// byte and set its bit in `ebits` (bit0 = window position of s[0]).
+ZS_HD int dp_t2_inplace(uint8_t *s, int n, const uint16_t *dfa2, const uint32_t *t2,
+                        const uint8_t *codes, unsigned *ebits, int bit0) {
+    unsigned st = 0, wi = 0;
+    int cost = 0;
+    for (int i = n - 1; i >= 0; --i) {
+        const unsigned b = s[i];
+        const unsigned e = dfa2[st * NCOL + dcol(b)];
+        st = e & 0xffu;
+        const unsigned x = t2[wi * T2_MASKS + (e >> 8)];
+        wi = x & 0xfffu;
+        const unsigned L = (x >> 12) & 15u;
+        cost += (int)(x >> 16) - 16;
+        if (L) s[i] = codes[st * FAST_W + L - 1];
+        else bm_set(ebits, bit0 + i);
+    }
+    return cost;
 }
 
 // ----------------------------------------------------------------------------

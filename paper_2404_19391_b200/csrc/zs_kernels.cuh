@@ -118,10 +118,11 @@ __device__ __forceinline__ void load_window(const uint8_t *in, long long n, long
 // position p in [T0, T1) whose previous byte is '\n').  Returns the count and,
 // when `queue` is given, writes the window offsets of the starts whose
 // ordinal falls in [q0, q1) at queue[ord - q0].
+template <int CH = CHUNK>
 __device__ __forceinline__ int scan_starts(const uint8_t *win, int tile_len, int base_ord,
                                            uint16_t *queue, int q0, int q1) {
-    const int c0 = threadIdx.x * CHUNK;
-    const int c1 = min(c0 + CHUNK, tile_len);
+    const int c0 = threadIdx.x * CH;
+    const int c1 = min(c0 + CH, tile_len);
     if (c0 >= c1) return 0;
     // the predecessor bytes of the chunk's positions: window [a, b)
     const int a = HEAD + c0 - 1, b = HEAD + c1 - 1;
@@ -348,10 +349,10 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
     __shared__ unsigned long long s_tmp64[NWARP];
     __shared__ int s_tmp32[NWARP];
     __shared__ unsigned s_hist[256];
-    __shared__ uint8_t s_lut[256];
+    __shared__ __align__(16) uint8_t s_lut[8 * 256];  // tokenizer transducer
     __shared__ long long s_tile;
     __shared__ int s_err_ord, s_global, s_grp;
-    __shared__ unsigned long long s_wmax, s_wsum, s_wmin, s_ngrp;
+    __shared__ unsigned long long s_wmax, s_wsum, s_wmin, s_ngrp, s_trn, s_tdp;
     __shared__ unsigned long long s_pre_out, s_pre_lines;
     __shared__ unsigned s_kept, s_esc, s_skip, s_flag;
 
@@ -366,10 +367,8 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
         }
         if (T2)
             for (int k = threadIdx.x; k < tb.n_windows * T2_MASKS; k += NT) S.t2[k] = tb.t2[k];
-        for (int k = threadIdx.x; k < 256; k += NT) {
-            S.explen[k] = tb.exp_len[k];
-            s_lut[k] = tok_bits(k);
-        }
+        for (int k = threadIdx.x; k < 256; k += NT) S.explen[k] = tb.exp_len[k];
+        for (int k = threadIdx.x; k < 8 * 256; k += NT) s_lut[k] = tk_entry(k >> 8, k & 255);
     }
     const int tid = threadIdx.x;
     PhaseClock pc;
@@ -377,7 +376,7 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
 
     for (;;) {
         __syncthreads();
-        pc.mark(job, 5);  // end of previous tile / table load
+        pc.mark(job, 2);  // end of previous tile / table load
         if (tid == 0) {
             s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
             s_err_ord = 0x7fffffff;
@@ -402,7 +401,7 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
         int tile_lines;
         const int my_off = block_exscan<int>(my_cnt, s_tmp32, tile_lines);
 
-        pc.mark(job, 7);  // ticket, window load, line-start scan
+        pc.mark(job, 2);  // ticket, window load, line-start scan
         // ---- parse phase, in rounds of QCAP lines ----
         for (int q0 = 0; q0 < tile_lines; q0 += QCAP) {
             const int nq = min(QCAP, tile_lines - q0);
@@ -433,11 +432,11 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
             }
             if (tid == 0) {
                 s_grp = 0;
-                s_wmax = s_wsum = s_ngrp = 0;
+                s_wmax = s_wsum = s_ngrp = s_trn = s_tdp = 0;
                 s_wmin = ~0ull;
             }
             __syncthreads();
-            pc.mark(job, 7);  // queue, lengths, sort
+            pc.mark(job, 2);  // queue, lengths, sort
             const long long wt0 = clock64();
             int my_groups = 0;
             // warps pull groups of 32 lines, longest first (LPT scheduling).
@@ -472,7 +471,10 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                 int rn_k = E_NONE, rn_len = 0, rn_off = -1;
                 unsigned long long rn_ids[2] = {0, 0};
                 const bool rn = do_dp && job.preprocess;
+                const long long tr0 = clock64();
                 rn_k = renumber_fast(s, rn ? n_l : 0, s_lut, d, &rn_len, &rn_off, rn_ids);
+                __syncwarp();
+                if (job.timing && (tid & 31) == 0) atomicAdd(&s_trn, (unsigned long long)(clock64() - tr0));
                 if (do_dp) {
                     if (job.preprocess) {
                         int eoff = rn_off;
@@ -516,6 +518,7 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                     }
                 }
                 __syncwarp();
+                const long long td0 = clock64();
                 // ---- min-cost parse (converged) ----
                 if (do_dp) {
                     if constexpr (T2) {
@@ -528,6 +531,7 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                     }
                 }
                 __syncwarp();
+                if (job.timing && (tid & 31) == 0) atomicAdd(&s_tdp, (unsigned long long)(clock64() - td0));
                 if (global_line) {
                     // line in HBM: find its end, process in the arena
                     const long long gs = ws + p;
@@ -576,6 +580,8 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                 atomicAdd(&job.ctl->phase[4], s_wmin);  // slot 4: min warp parse time
                 atomicAdd(&job.ctl->phase[0], s_wsum / NWARP);  // slot 0: avg warp parse
                 atomicAdd(&job.ctl->phase[1], s_ngrp);  // slot 1: groups per tile
+                atomicAdd(&job.ctl->phase[5], s_trn / NWARP);  // slot 5: renumber per warp
+                atomicAdd(&job.ctl->phase[7], s_tdp / NWARP);  // slot 7: parse per warp
             }
         }
 
@@ -608,7 +614,7 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                                            : emit_chunk<true>(job, S, ws, tile_len, my_out_off, S.out);
             if (esc) atomicAdd(&s_esc, esc);
         }
-        pc.mark(job, 5);  // thread 0: publish + its own emit
+        pc.mark(job, 2);  // thread 0: publish + its own emit
         if (tid < 32) {
             unsigned long long po, pl;
             lookback_resolve(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
@@ -618,7 +624,7 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
             }
         }
         __syncthreads();
-        pc.mark(job, 7);  // look-back resolve + wait for the slowest emitter
+        pc.mark(job, 2);  // look-back resolve + wait for the slowest emitter
         const unsigned long long pre_out = s_pre_out;
         const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
         if (tid == 0) {
@@ -649,7 +655,7 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                 int nl2, eoff = -1;
                 unsigned long long ids[2] = {0, 0};
                 const long long n_l = ge - gs;
-                const unsigned long long need = 4 * n_l + 4;
+                const unsigned long long need = (4 * (unsigned long long)n_l + 19) & ~15ull;
                 unsigned long long a = atomicAdd(&job.ctl->arena_used, need);
                 uint8_t *tmp = a + need <= (unsigned long long)job.arena_cap ? job.arena + a : nullptr;
                 if (!tmp) atomicOr(&job.ctl->overflow, 2ull);
@@ -670,12 +676,438 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
         // ---- store (staged) or emit straight to HBM (direct) ----
         if (staged) {
             store_out(job.out + pre_out, S.out, (int)tile_out);
-            pc.mark(job, 5);
+            pc.mark(job, 2);
         } else {
             if (tid == 0) s_grp = 0;
             __syncthreads();
             const unsigned esc = one_round ? emit_lines(job, S, ws, tile_lines, &s_grp, job.out, pre_out)
                                            : emit_chunk<false>(job, S, ws, tile_len, pre_out + my_out_off, job.out);
+            if (esc) atomicAdd(&s_esc, esc);
+        }
+        __syncthreads();
+        if (tid == 0 && s_esc) atomicAdd(&job.ctl->escapes, (unsigned long long)s_esc);
+    }
+}
+
+// ============================================================================
+// In-place compress kernel (transducer dictionaries): decisions overwrite the
+// line bytes in the staged window, so a CTA stages ~67 KB tiles (~1500 lines,
+// ~46 warp groups) instead of ~34 KB; escape literals stay in place with
+// their bit set in `ebits`; ring-token starts are marked in `rbits`.
+// In-band line encoding after the parse (position p = line start):
+//   ebits[p] && win[p] == '\n'  -> line dropped (lenient CR / strict error)
+//   ebits[p] && win[p] == 0x0d  -> line parsed in the HBM arena (offset/16 in
+//                                   win[p+1..p+4])
+//   otherwise decisions from p: code (advance by its length) or, with the
+//   ebits bit, an escaped literal; '\n' ends the line.
+// ============================================================================
+constexpr int CCHUNK = 116;                 // 29 words: odd stride across lanes
+constexpr int CTILE = CCHUNK * NT;          // 59392 bytes of line starts per tile
+constexpr int CWIN = HEAD + CTILE + EXTRA;  // 63504 (multiple of 16; window offsets fit u16)
+static_assert(CWIN + 16 < 65536, "line queue stores u16 window offsets");
+constexpr int CWORDS = CWIN / 32 + 2;       // bitmap words
+constexpr int COUTCAP = 30720;
+constexpr int CQCAP = 2048;
+
+struct IpSmem {
+    uint16_t *dfa;
+    uint32_t *t2;
+    uint8_t *codes;
+    uint8_t *explen;
+    uint8_t *win;
+    unsigned *rbits;
+    unsigned *ebits;
+    uint8_t *out;
+    uint16_t *queue, *qlen, *qsort;
+    unsigned *qoff;
+    unsigned *chunk;
+};
+
+__host__ __device__ inline int ip_smem_bytes(int n_states, int n_windows) {
+    return align16(n_states * NCOL * 2) + n_windows * T2_MASKS * 4 + align16(n_states * FAST_W) +
+           256 + align16(CWIN + 16) + 2 * CWORDS * 4 + align16(COUTCAP) + 3 * CQCAP * 2 +
+           CQCAP * 4 + NT * 4;
+}
+
+__device__ inline IpSmem carve_ip(uint8_t *p, int ns, int nw) {
+    IpSmem S;
+    S.dfa = reinterpret_cast<uint16_t *>(p); p += align16(ns * NCOL * 2);
+    S.t2 = reinterpret_cast<uint32_t *>(p); p += nw * T2_MASKS * 4;
+    S.codes = p; p += align16(ns * FAST_W);
+    S.explen = p; p += 256;
+    S.win = p; p += align16(CWIN + 16);
+    S.rbits = reinterpret_cast<unsigned *>(p); p += CWORDS * 4;
+    S.ebits = reinterpret_cast<unsigned *>(p); p += CWORDS * 4;
+    S.out = p; p += align16(COUTCAP);
+    S.queue = reinterpret_cast<uint16_t *>(p); p += CQCAP * 2;
+    S.qlen = reinterpret_cast<uint16_t *>(p); p += CQCAP * 2;
+    S.qsort = reinterpret_cast<uint16_t *>(p); p += CQCAP * 2;
+    S.qoff = reinterpret_cast<unsigned *>(p); p += CQCAP * 4;
+    S.chunk = reinterpret_cast<unsigned *>(p);
+    return S;
+}
+
+__device__ __forceinline__ bool bm_get(const unsigned *bm, int pos) {
+    return (bm[pos >> 5] >> (pos & 31)) & 1u;
+}
+
+// Emit one line from the in-place encoding at o[w...] (w advanced); returns
+// the escapes emitted.
+__device__ __forceinline__ unsigned ip_emit_line(const Job &job, const IpSmem &S, long long ws, int p,
+                                                 uint8_t *o, unsigned long long &w) {
+    unsigned esc = 0;
+    const uint8_t *win = S.win;
+    if (bm_get(S.ebits, p) && win[p] == '\n') return 0;  // dropped
+    if (bm_get(S.ebits, p) && win[p] == 0x0d) {           // parsed in the arena
+        const unsigned aoff = win[p + 1] | (win[p + 2] << 8) | (win[p + 3] << 16) |
+                              ((unsigned)win[p + 4] << 24);
+        const uint8_t *blk = job.arena + ((long long)aoff << 4);
+        const ArenaHdr *h = reinterpret_cast<const ArenaHdr *>(blk);
+        const uint8_t *bytes = h->bytes_off < 0 ? job.in + ws + p : job.arena + h->bytes_off;
+        const uint8_t *dec = job.arena + h->dec_off;
+        for (long long i = 0; i < h->n_pre;) {
+            const uint8_t c = dec[i];
+            if (c == D_ESC) {
+                o[w++] = 0x20;
+                o[w++] = bytes[i];
+                ++esc;
+                ++i;
+            } else {
+                o[w++] = c;
+                i += S.explen[c];
+            }
+        }
+        o[w++] = '\n';
+        return esc;
+    }
+    for (int i = p;;) {
+        const uint8_t c = win[i];
+        if (c == '\n') break;
+        if (bm_get(S.ebits, i)) {
+            o[w++] = 0x20;
+            o[w++] = c;
+            ++esc;
+            ++i;
+        } else {
+            o[w++] = c;
+            i += S.explen[c];
+        }
+    }
+    o[w++] = '\n';
+    return esc;
+}
+
+__global__ void __launch_bounds__(NT, 1) compress_tiles_ip(Job job, Tables tb) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ unsigned long long s_tmp64[NWARP];
+    __shared__ int s_tmp32[NWARP];
+    __shared__ unsigned s_hist[256];
+    __shared__ __align__(16) uint8_t s_lut[8 * 256];  // tokenizer transducer
+    __shared__ long long s_tile;
+    __shared__ int s_err_ord, s_global, s_grp;
+    __shared__ unsigned long long s_pre_out, s_pre_lines;
+    __shared__ unsigned s_kept, s_esc, s_skip, s_flag;
+
+    const IpSmem S = carve_ip(smem, tb.n_states, tb.n_windows);
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(tb.dfa2);
+        uint4 *dst = reinterpret_cast<uint4 *>(S.dfa);
+        for (int k = threadIdx.x; k < align16(tb.n_states * NCOL * 2) / 16; k += NT) dst[k] = src[k];
+        for (int k = threadIdx.x; k < tb.n_windows * T2_MASKS; k += NT) S.t2[k] = tb.t2[k];
+        for (int k = threadIdx.x; k < tb.n_states * FAST_W; k += NT) S.codes[k] = tb.codes[k];
+        for (int k = threadIdx.x; k < 256; k += NT) S.explen[k] = tb.exp_len[k];
+        for (int k = threadIdx.x; k < 8 * 256; k += NT) s_lut[k] = tk_entry(k >> 8, k & 255);
+    }
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) {
+            s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
+            s_err_ord = 0x7fffffff;
+            s_global = 0;
+            s_kept = s_esc = s_skip = s_flag = 0;
+        }
+        __syncthreads();
+        const long long t = s_tile;
+        if (t >= job.n_tiles) break;
+        const long long T0 = t * (long long)CTILE;
+        const int tile_len = (int)min((long long)CTILE, job.n - T0);
+        const long long ws = T0 - HEAD;
+        const long long we = min(job.n, T0 + CTILE + EXTRA);
+        const int win_len = (int)(we - ws);
+        const bool hits_eof = we == job.n;
+        load_window(job.in, job.n, ws, align16(win_len), S.win);
+        for (int k = tid; k < CWORDS; k += NT) S.rbits[k] = S.ebits[k] = 0u;
+        S.chunk[tid] = 0;
+        __syncthreads();
+        if (tid == 0 && hits_eof) S.win[win_len] = '\n';  // end of a final partial line
+
+        const int my_cnt = scan_starts<CCHUNK>(S.win, tile_len, 0, nullptr, 0, 0);
+        int tile_lines;
+        const int my_off = block_exscan<int>(my_cnt, s_tmp32, tile_lines);
+
+        for (int q0 = 0; q0 < tile_lines; q0 += CQCAP) {
+            const int nq = min(CQCAP, tile_lines - q0);
+            if (my_cnt) scan_starts<CCHUNK>(S.win, tile_len, my_off, S.queue, q0, q0 + nq);
+            for (int k = tid; k < 256; k += NT) s_hist[k] = 0;
+            __syncthreads();
+            for (int q = tid; q < nq; q += NT) {
+                const int p = S.queue[q];
+                const int end = (q + 1 < nq) ? S.queue[q + 1] - 1 : find_end(S.win, p, win_len, hits_eof);
+                const int len = end < 0 ? 0xffff : end - p;
+                S.qlen[q] = (uint16_t)len;
+                atomicAdd(&s_hist[255 - min(len, 255)], 1u);
+            }
+            __syncthreads();
+            {
+                unsigned h = tid < 256 ? s_hist[tid] : 0u;
+                unsigned tot;
+                const unsigned ex = block_exscan<unsigned>(h, reinterpret_cast<unsigned *>(s_tmp32), tot);
+                if (tid < 256) s_hist[tid] = ex;
+            }
+            __syncthreads();
+            for (int q = tid; q < nq; q += NT) {
+                const unsigned r = atomicAdd(&s_hist[255 - min((int)S.qlen[q], 255)], 1u);
+                S.qsort[r] = (uint16_t)q;
+            }
+            if (tid == 0) s_grp = 0;
+            __syncthreads();
+            // warps pull groups of 32 lines, longest first (LPT)
+            for (;;) {
+                int g = 0;
+                if (lane == 0) g = atomicAdd(&s_grp, 1);
+                g = __shfl_sync(0xffffffffu, g, 0);
+                if (g * 32 >= nq) break;
+                const int r = g * 32 + lane;
+                const bool valid = r < nq;
+                int q = 0, p = HEAD, qlen = 0;
+                if (valid) {
+                    q = S.qsort[r];
+                    p = S.queue[q];
+                    qlen = S.qlen[q];
+                }
+                const int ord = q0 + q;
+                int kind = E_NONE;
+                long long size = 0;
+                bool global_line = valid && qlen == 0xffff;
+                bool do_dp = valid && !global_line;
+                uint8_t *s = S.win + p;
+                int n_l = qlen;
+                // ---- CR policy + ring renumbering (all lanes call) ----
+                int rn_len = 0, rn_off = -1;
+                unsigned long long rn_ids[2] = {0, 0};
+                const bool rn = do_dp && job.preprocess;
+                int k = renumber_bm(s, rn ? n_l : 0, s_lut, S.rbits, p, &rn_len, &rn_off, rn_ids);
+                if (do_dp) {
+                    if (job.preprocess) {
+                        if (k == E_NONE) {
+                            if (rn_len < n_l) s[rn_len] = '\n';  // end of the shrunk line
+                            n_l = rn_len;
+                        } else if (k == RN_FALLBACK) {
+                            // pristine bytes, then the general routine (marks in the arena)
+                            const uint8_t *g8 = job.in + ws + p;
+                            for (int j = 0; j < n_l; ++j) s[j] = g8[j];
+                            const unsigned long long need = ((unsigned long long)n_l + 31) & ~15ull;
+                            const unsigned long long a = atomicAdd(&job.ctl->arena_used, need);
+                            if (a + need <= (unsigned long long)job.arena_cap) {
+                                int nl2 = n_l;
+                                k = preprocess_line(s, n_l, job.arena + a, s, &nl2, &rn_off, rn_ids);
+                                if (k == E_NONE) {
+                                    if (nl2 < n_l) s[nl2] = '\n';
+                                    n_l = nl2;
+                                }
+                            } else {
+                                atomicOr(&job.ctl->overflow, 2ull);
+                                k = E_NONE;
+                            }
+                        }
+                        if (k == -1) {
+                            global_line = true;
+                            do_dp = false;
+                        } else if (k != E_NONE) {
+                            if (k == E_CR) {
+                                kind = E_CR;
+                            } else if (job.lenient) {
+                                // keep the raw line (pipeline.py:108-115)
+                                const uint8_t *g8 = job.in + ws + p;
+                                for (int j = 0; j < n_l; ++j) s[j] = g8[j];
+                                atomicAdd(&s_flag, 1u);
+                            } else {
+                                kind = k;
+                            }
+                        }
+                    } else {
+                        for (int j = 0; j < n_l; ++j)
+                            if (s[j] == '\r') { kind = E_CR; break; }
+                    }
+                    if (do_dp && kind != E_NONE) {
+                        do_dp = false;
+                        s[0] = '\n';
+                        bm_set(S.ebits, p);
+                        if (job.lenient) atomicAdd(&s_skip, 1u);
+                        else atomicMin(&s_err_ord, ord);
+                    }
+                }
+                __syncwarp();
+                // ---- min-cost parse, decisions in place (converged) ----
+                if (do_dp) size = dp_t2_inplace(s, n_l, S.dfa, S.t2, S.codes, S.ebits, p) + 1;
+                __syncwarp();
+                if (global_line) {
+                    const long long gs = ws + p;
+                    long long ge = gs;
+                    while (ge < job.n && job.in[ge] != '\n') ++ge;
+                    unsigned aoff = 0;
+                    int eoff = -1;
+                    unsigned long long ids[2] = {0, 0};
+                    long long cost = compress_line_global(job, tb, gs, ge - gs, &aoff, &kind, &eoff, ids);
+                    s_global = 1;
+                    if (kind == -2) {
+                        kind = E_NONE;  // arena exhausted; host re-runs
+                        s[0] = '\n';
+                        bm_set(S.ebits, p);
+                    } else if (kind == E_CR || (kind > 0 && !job.lenient)) {
+                        s[0] = '\n';
+                        bm_set(S.ebits, p);
+                        if (job.lenient) atomicAdd(&s_skip, 1u);
+                        else atomicMin(&s_err_ord, ord);
+                    } else {
+                        if (kind == -3) atomicAdd(&s_flag, 1u);
+                        kind = E_NONE;
+                        s[0] = 0x0d;
+                        s[1] = aoff & 0xff; s[2] = (aoff >> 8) & 0xff;
+                        s[3] = (aoff >> 16) & 0xff; s[4] = (aoff >> 24) & 0xff;
+                        bm_set(S.ebits, p);
+                        size = cost + 1;
+                    }
+                }
+                if (valid) S.qoff[q] = (unsigned)size;
+                if (size) {
+                    atomicAdd(&S.chunk[(p - HEAD) / CCHUNK], (unsigned)size);
+                    atomicAdd(&s_kept, 1u);
+                }
+                __syncwarp();
+            }
+            __syncthreads();
+        }
+
+        // ---- tile output size; publish; emit to smem; look-back ----
+        unsigned long long tile_out;
+        const unsigned long long my_out = S.chunk[tid];
+        const unsigned long long my_out_off = block_exscan<unsigned long long>(my_out, s_tmp64, tile_out);
+        const bool one_round = tile_lines <= CQCAP;
+        if (one_round) {
+            const int per = (tile_lines + NT - 1) / NT;
+            const int l0 = min(tid * per, tile_lines), l1 = min(l0 + per, tile_lines);
+            unsigned sum = 0;
+            for (int l = l0; l < l1; ++l) sum += S.qoff[l];
+            unsigned tot;
+            unsigned run = block_exscan<unsigned>(sum, reinterpret_cast<unsigned *>(s_tmp32), tot);
+            for (int l = l0; l < l1; ++l) {
+                const unsigned v = S.qoff[l];
+                S.qoff[l] = run;
+                run += v;
+            }
+            if (tid == 0) s_grp = 0;
+            __syncthreads();
+        }
+        if (tid == 0) lookback_publish(job.ts, t, tile_out, (unsigned long long)tile_lines);
+        const bool staged = !s_global && one_round && tile_out <= (unsigned long long)COUTCAP;
+        if (staged) {
+            unsigned esc = 0;
+            for (;;) {
+                int g = 0;
+                if (lane == 0) g = atomicAdd(&s_grp, 1);
+                g = __shfl_sync(0xffffffffu, g, 0);
+                if (g * 32 >= tile_lines) break;
+                const int r = g * 32 + lane;
+                __syncwarp();
+                if (r < tile_lines) {
+                    const int q = S.qsort[r];
+                    unsigned long long w = S.qoff[q];
+                    esc += ip_emit_line(job, S, ws, S.queue[q], S.out, w);
+                }
+                __syncwarp();
+            }
+            if (esc) atomicAdd(&s_esc, esc);
+        }
+        if (tid < 32) {
+            unsigned long long po, pl;
+            lookback_resolve(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
+            if (tid == 0) {
+                s_pre_out = po;
+                s_pre_lines = pl;
+            }
+        }
+        __syncthreads();
+        const unsigned long long pre_out = s_pre_out;
+        const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
+        if (tid == 0) {
+            atomicAdd(&job.ctl->total_out, tile_out);
+            atomicAdd(&job.ctl->lines, (unsigned long long)s_kept);
+            atomicAdd(&job.ctl->in_lines, (unsigned long long)tile_lines);
+            if (s_skip) atomicAdd(&job.ctl->skipped, (unsigned long long)s_skip);
+            if (s_flag) atomicAdd(&job.ctl->flagged, (unsigned long long)s_flag);
+            if (!fits) atomicOr(&job.ctl->overflow, 1ull);
+        }
+        // ---- strict error: re-derive details of the first bad line ----
+        if (tid == 0 && s_err_ord != 0x7fffffff) {
+            int ord = s_err_ord, seen = 0;
+            long long gp = -1;
+            for (long long x = T0; x < T0 + tile_len && gp < 0; ++x)
+                if (x == 0 || job.in[x - 1] == '\n') {
+                    if (seen == ord) gp = x;
+                    ++seen;
+                }
+            long long gs = gp, ge = gs;
+            while (ge < job.n && job.in[ge] != '\n') ++ge;
+            TileErr e = {E_CR, 0, -1, {0, 0}};
+            bool cr = false;
+            for (long long k = gs; k < ge; ++k) cr |= job.in[k] == '\r';
+            if (!cr && job.preprocess) {
+                int nl2, eoff = -1;
+                unsigned long long ids[2] = {0, 0};
+                const long long n_l = ge - gs;
+                const unsigned long long need = (4 * (unsigned long long)n_l + 19) & ~15ull;
+                unsigned long long a = atomicAdd(&job.ctl->arena_used, need);
+                uint8_t *tmp = a + need <= (unsigned long long)job.arena_cap ? job.arena + a : nullptr;
+                if (!tmp) atomicOr(&job.ctl->overflow, 2ull);
+                int k = tmp ? preprocess_line(job.in + gs, (int)n_l, tmp, tmp + n_l + 1, &nl2, &eoff, ids)
+                            : E_NONE;
+                e.kind = k;
+                e.offset = eoff;
+                e.ids[0] = ids[0];
+                e.ids[1] = ids[1];
+            }
+            job.terr[t] = e;
+            __threadfence();
+            atomicMin(&job.ctl->err_key, ((s_pre_lines + (unsigned long long)ord) << 24) |
+                                             (unsigned long long)(t & 0xffffff));
+        }
+        if (!fits) continue;
+
+        if (staged) {
+            store_out(job.out + pre_out, S.out, (int)tile_out);
+        } else {
+            // direct emit: per line in queue order (single round) or, for
+            // tiles with more than CQCAP lines, by chunk with the line starts
+            // re-derived from the pristine input in HBM (rare paths)
+            unsigned esc = 0;
+            if (one_round) {
+                for (int q = tid; q < tile_lines; q += NT) {
+                    unsigned long long w = pre_out + S.qoff[q];
+                    esc += ip_emit_line(job, S, ws, S.queue[q], job.out, w);
+                }
+            } else {
+                unsigned long long w = pre_out + my_out_off;
+                const int c0 = tid * CCHUNK, c1 = min(c0 + CCHUNK, tile_len);
+                for (int x = c0; x < c1; ++x) {
+                    const long long gx = T0 + x;
+                    if (gx == 0 || job.in[gx - 1] == '\n')
+                        esc += ip_emit_line(job, S, ws, HEAD + x, job.out, w);
+                }
+            }
             if (esc) atomicAdd(&s_esc, esc);
         }
         __syncthreads();

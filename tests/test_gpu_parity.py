@@ -333,3 +333,26 @@ def test_device_and_host_api_agree():
         assert ctx.last_kernel_ms() > 0
     assert dout[:r.out_bytes].cpu().numpy().tobytes() == comp.tobytes()
     assert (r.lines, r.out_bytes) == (res.lines, res.out_bytes)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 3])
+def test_kernel_variants_bit_exact(corpus_hashes, mode):
+    """Every compress kernel variant (0: key-window DP with a decision array,
+    1: + cost-window transducer, 3: + in-place decisions, the default) gives
+    the reference bytes."""
+    ctx = _lib.context()
+    try:
+        ctx.lib.zs_set_transducer(ctx.h, mode)
+        for name in ("c1_100k", "c3_skewed_20k", "mixed_50k"):
+            e = corpus_hashes[name]
+            buf = synth.generate(e["kind"], e["lines"], e["seed"])
+            d = z.deserialize(golden_dict_bytes(e["dict"]))
+            for key, pre in (("pre_off", False), ("pre_on", True)):
+                comp, res = z.run_buffer(buf, d, "compress", preprocess=pre, lenient=True)
+                assert hashlib.sha256(comp.tobytes()).hexdigest() == e[key]["comp_sha256"], (name, key)
+        test_long_lines_global_path()
+        test_growing_renumbering_line()
+        test_many_tiny_lines_multiple_rounds()
+        test_errors_across_tiles()
+    finally:
+        ctx.lib.zs_set_transducer(ctx.h, 3)

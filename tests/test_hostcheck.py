@@ -32,6 +32,9 @@ def build():
     lib.hc_compress_fast.restype = ctypes.c_longlong
     lib.hc_compress_t2.argtypes = [P, P, P, P, P, ctypes.c_int, P]
     lib.hc_compress_t2.restype = ctypes.c_longlong
+    lib.hc_renumber_bm.argtypes = [P, ctypes.c_int, P, P, P, P, P, ctypes.c_int]
+    lib.hc_inplace_stream.argtypes = [P, P, P, P, P, ctypes.c_int, ctypes.c_int, P]
+    lib.hc_inplace_stream.restype = ctypes.c_longlong
     return lib
 
 
@@ -46,14 +49,17 @@ def _buf(b):
     return ctypes.create_string_buffer(bytes(b), max(1, len(b)))
 
 
-def renumber(hc, line, fast=True):
+def renumber(hc, line, fast=True, bm=None):
     src = _buf(line)
     out = ctypes.create_string_buffer(3 * len(line) + 4)
     n = ctypes.c_int(0)
     off = ctypes.c_int(-1)
     ids = (ctypes.c_uint64 * 2)()
     fb = ctypes.c_int(0)
-    if fast:
+    if bm is not None:
+        k = hc.hc_renumber_bm(src, len(line), out, ctypes.byref(n), ctypes.byref(off), ids,
+                              ctypes.byref(fb), bm)
+    elif fast:
         k = hc.hc_renumber(src, len(line), out, ctypes.byref(n), ctypes.byref(off), ids,
                            ctypes.byref(fb))
     else:
@@ -76,13 +82,14 @@ def test_renumber_matches_reference(hc, preprocess_cases):
             assert want.get("err") == NAMES[k], c
         if b"\r" in line:
             continue  # the kernel path treats CR as a line error (pipeline policy)
-        k2, out2, off2, ids2, _ = renumber(hc, line)
-        if k2 == -1:  # a token grows: the kernel re-runs the line out of smem
-            assert k == 0  # some 1-byte id takes a colour >= 10
-            continue
-        assert (k2, out2) == (k, out), (line, k2, k)
-        if k:
-            assert (off2, ids2) == (off, ids)
+        for bm in (None, 0, 13):
+            k2, out2, off2, ids2, _ = renumber(hc, line, bm=bm)
+            if k2 == -1:  # a token grows: the kernel re-runs the line out of smem
+                assert k == 0  # some 1-byte id takes a colour >= 10
+                continue
+            assert (k2, out2) == (k, out), (line, k2, k, bm)
+            if k:
+                assert (off2, ids2) == (off, ids)
 
 
 @pytest.mark.parametrize("kind,n,seed", [("aromatic", 100000, 2024), ("mixed", 50000, 2024),
@@ -94,7 +101,9 @@ def test_renumber_corpus_fast_path(hc, kind, n, seed):
         k, out, _, _, fb = renumber(hc, line)
         ok, want = oracle.preprocess(line)
         assert k == ok == 0 and out == want, line
-        fallbacks += fb
+        k, out, _, _, fb2 = renumber(hc, line, bm=7)
+        assert k == 0 and out == want, line
+        fallbacks += fb + fb2
     assert fallbacks <= len(lines) // 1000
 
 
@@ -176,3 +185,29 @@ def test_transducer_corpus(hc, name, corpus_hashes):
         w = hc.hc_compress_t2(dfa2.ctypes.data, t2.ctypes.data, codes.ctypes.data,
                               t.exp_len.ctypes.data, _buf(line), len(line), out)
         assert out.raw[:w] == rec
+
+
+@pytest.mark.parametrize("kind,n,seed", [("aromatic", 20000, 2024), ("mixed", 20000, 2024),
+                                         ("skewed", 1000, 2025)])
+def test_inplace_pipeline(hc, kind, n, seed):
+    """The in-place kernel's line pipeline (bitmap renumbering, in-place
+    transducer decisions, in-band emit) on whole buffers == oracle stream."""
+    lib = __import__("paper_2404_19391_b200._lib", fromlist=["load"]).load()
+    t = oracle.Tables.from_zsd(golden_dict_bytes())
+    dfa = np.zeros(256 * 97, np.uint16)
+    codes = np.zeros(256 * 8, np.uint8)
+    ns, ml = ctypes.c_int32(0), ctypes.c_int32(0)
+    lib.zs_build_tables_host(t.children.ctypes.data, t.term_code.ctypes.data, t.children.shape[0],
+                             dfa.ctypes.data, codes.ctypes.data, ctypes.byref(ns), ctypes.byref(ml))
+    dfa2 = np.zeros(256 * 97, np.uint16)
+    t2 = np.zeros(1024 * 16, np.uint32)
+    nw, nm = ctypes.c_int32(0), ctypes.c_int32(0)
+    assert lib.zs_build_t2_host(t.children.ctypes.data, t.term_code.ctypes.data, t.children.shape[0],
+                                dfa2.ctypes.data, t2.ctypes.data, ctypes.byref(nw), ctypes.byref(nm))
+    buf = synth.generate(kind, n, seed).tobytes()
+    for pre in (0, 1):
+        out = ctypes.create_string_buffer(2 * len(buf) + 2)
+        w = hc.hc_inplace_stream(dfa2.ctypes.data, t2.ctypes.data, codes.ctypes.data,
+                                 t.exp_len.ctypes.data, _buf(buf), len(buf), pre, out)
+        want, _ = oracle.run_stream(t, buf, "compress", bool(pre), False, 4)
+        assert w == len(want) and out.raw[:w] == want

@@ -14,7 +14,7 @@ import synth  # noqa: E402
 import paper_2404_19391_b200 as z  # noqa: E402
 from paper_2404_19391_b200 import _lib  # noqa: E402
 
-NAMES = ["warp-parse-avg", "groups/tile", "parse-wait-t0", "warp-parse-max", "warp-parse-min", "other", "parse-t0", "load/sort/lookback"]
+NAMES = ["warp-groups-avg", "groups/tile", "everything-else-t0", "warp-groups-max", "warp-groups-min", "renumber/warp", "parse-t0", "dp/warp"]
 
 
 def main():
