@@ -351,9 +351,9 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
             CK(set_smem(k, smem));
             k<<<grid, NT, smem, st>>>(job, ctx->tb);
         } else {
-            const int smem = decompress_smem_bytes(ctx->tb.n_flat);
-            CK(set_smem(decompress_tiles, smem));
-            decompress_tiles<<<grid, NT, smem, st>>>(job, ctx->tb);
+            const int smem = bp_smem_bytes(ctx->tb.n_flat);
+            CK(set_smem(decompress_tiles_bp, smem));
+            decompress_tiles_bp<<<grid, NT, smem, st>>>(job, ctx->tb);
         }
         CK(cudaGetLastError());
         if (timed) CK(cudaEventRecord(ctx->ev1, st));
@@ -711,6 +711,8 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
     tb.exp_off = ctx->d_expoff.as<uint16_t>();
     tb.exp_flat = ctx->d_expflat.as<uint8_t>();
     tb.n_flat = (int)exp_off[256];
+    tb.max_exp = 0;
+    for (int b = 0; b < 256; ++b) tb.max_exp = std::max<int>(tb.max_exp, ht.exp_len[b]);
     ctx->fast_w = 0;
     if (ht.fast) {
         const int L = std::max(1, ht.max_len);

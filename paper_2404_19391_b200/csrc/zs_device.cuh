@@ -88,6 +88,7 @@ struct Tables {
     const uint16_t *exp_off;  // [257]
     const uint8_t *exp_flat;
     int n_flat;
+    int max_exp;  // longest expansion (<= 8 enables the unrolled copy)
 };
 
 struct Ctl {                    // zeroed before every launch
@@ -182,6 +183,30 @@ struct SmemBytes {
     unsigned ld(int i) const { return p[i]; }
 #endif
 };
+
+// Explicit shared-memory accesses through 32-bit addresses formed once (a
+// generic pointer makes the compiler re-derive the shared window base,
+// S2R SR_CgaCtaId + LEA, at many accesses under register pressure).  All are
+// volatile so they keep program order with each other and with barriers.
+__device__ __forceinline__ unsigned sa(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned ldsb(unsigned a) {
+    unsigned v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ unsigned ldsh(unsigned a) {
+    unsigned v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ unsigned ldsw(unsigned a) {
+    unsigned v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void stsb(unsigned a, unsigned v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 
 // warp-uniform loop condition (device: all 32 lanes must take part)
 #ifdef __CUDA_ARCH__

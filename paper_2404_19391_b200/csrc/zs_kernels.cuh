@@ -1364,6 +1364,314 @@ __global__ void __launch_bounds__(NT, 1) decompress_tiles(Job job, Tables tb) {
     }
 }
 
+// ============================================================================
+// Byte-parallel decompress.  Each thread owns a fixed slice of the tile's
+// compressed bytes (its CHUNK; the thread holding the tile end also takes
+// the overhang of the last record) and walks it three times with a uniform
+// trip count: (1) validate -- unknown codes and dangling escapes flag their
+// record in a per-tile bitmap (rare atomics); (2) sum the output bytes of
+// good records -> block scan -> the slice's output offset; (3) expand.
+// The escape state at a slice start is the parity of the 0x20 run just
+// before it (a 0x20 at an odd index of a run is a literal).  Records are
+// framed by '\n' exactly as run_stream splits them (pipeline.py:49-74).
+// ============================================================================
+struct BpSmem {
+    uint8_t *expflat;
+    uint16_t *expoff;
+    uint8_t *explen;
+    uint8_t *win;
+    uint8_t *out;
+    unsigned *bad;   // bit per record ordinal of the tile
+};
+
+constexpr int BP_BADW = TILE / 32 + 2;
+
+__host__ __device__ inline int bp_smem_bytes(int n_flat) {
+    return align16(n_flat + 16) + align16(257 * 2) + 256 + align16(WIN + 16) + align16(DOUTCAP) +
+           BP_BADW * 4;
+}
+
+__device__ inline BpSmem carve_bp(uint8_t *p, int n_flat) {
+    BpSmem S;
+    S.expflat = p; p += align16(n_flat + 16);
+    S.expoff = reinterpret_cast<uint16_t *>(p); p += align16(257 * 2);
+    S.explen = p; p += 256;
+    S.win = p; p += align16(WIN + 16);
+    S.out = p; p += align16(DOUTCAP);
+    S.bad = reinterpret_cast<unsigned *>(p);
+    return S;
+}
+
+// one compressed byte: window when resident, else HBM (long last record)
+struct BpBytes {
+    const uint8_t *win;
+    const uint8_t *in;
+    long long ws;
+    int lim;  // window bytes [0, lim) are resident (incl. the EOF sentinel)
+    __device__ __forceinline__ unsigned operator()(int p) const {
+        return p < lim ? win[p] : in[ws + p];
+    }
+};
+
+// One walk over a decompress slice.  MODE 0: validate (flag bad records);
+// 1: count output bytes and escapes of good records; 2: expand to smem
+// (staged) or HBM.  RES: every byte of the slice is in the smem window
+// (bytes come 4 at a time from aligned words; p0 is word-aligned).
+struct BpWalk {
+    unsigned a_win, a_len, a_bad, a_off, a_flat, a_out;
+    int p0, p1, tile_end, ord0;
+    bool esc0, short_exp;
+};
+
+template <int MODE, bool RES>
+__device__ __forceinline__ void bp_walk(const BpWalk &W, const BpSmem &S, const BpBytes &B,
+                                        unsigned *bad, unsigned &sum, unsigned &nesc,
+                                        uint8_t *o_glob, unsigned long long w) {
+    int ord = W.ord0;
+    unsigned esc = W.esc0;
+    unsigned good = 0;
+    if (MODE > 0 && ord >= 0) good = !((ldsw(W.a_bad + 4 * (ord >> 5)) >> (ord & 31)) & 1u);
+    unsigned prev = W.p0 < W.p1 ? ldsb(W.a_win + W.p0 - 1) : 0u;
+    unsigned word = 0;
+    for (int p = W.p0; p < W.p1; ++p) {
+        unsigned b;
+        if (RES) {
+            if (((p - W.p0) & 3) == 0) word = ldsw(W.a_win + p);  // p0 is 4-aligned
+            b = word & 0xffu;
+            word >>= 8;
+        } else {
+            b = B(p);
+        }
+        const unsigned start = (p < W.tile_end) & (prev == '\n');
+        prev = b;
+        ord += (int)start;
+        esc &= start ^ 1u;
+        if (MODE > 0 && start) good = !((ldsw(W.a_bad + 4 * (ord >> 5)) >> (ord & 31)) & 1u);
+        const unsigned nl = b == '\n';
+        const unsigned mark = (esc ^ 1u) & (nl ^ 1u) & (b == 0x20);
+        const unsigned code = (esc ^ 1u) & (nl ^ 1u) & (mark ^ 1u);
+        const unsigned L = ldsb(W.a_len + b);
+        if (MODE == 0) {
+            const unsigned err = (ord >= 0) & ((nl & esc) | (code & (L == 0)));
+            if (err) atomicOr(&bad[ord >> 5], 1u << (ord & 31));
+        } else {
+            const unsigned add = code ? L : (mark ^ 1u);
+            if (MODE == 1) {
+                sum += good ? add : 0u;
+                nesc += good & mark;
+            } else if (good) {
+                if (o_glob == nullptr) {
+                    const unsigned ow = W.a_out + (unsigned)w;
+                    if (!code) {
+                        if (!mark) stsb(ow, b);  // literal or '\n'
+                    } else {
+                        const unsigned e = W.a_flat + ldsh(W.a_off + 2 * b);
+                        if (W.short_exp) {
+#pragma unroll
+                            for (unsigned k = 0; k < 8; ++k)
+                                if (k < L) stsb(ow + k, ldsb(e + k));
+                        } else {
+                            for (unsigned k = 0; k < L; ++k) stsb(ow + k, ldsb(e + k));
+                        }
+                    }
+                } else {
+                    if (!code) {
+                        if (!mark) o_glob[w] = (uint8_t)b;
+                    } else {
+                        const uint8_t *e = S.expflat + S.expoff[b];
+                        for (unsigned k = 0; k < L; ++k) o_glob[w + k] = e[k];
+                    }
+                }
+                w += add;
+            }
+        }
+        esc = mark;
+    }
+}
+
+__global__ void __launch_bounds__(NT, 1) decompress_tiles_bp(Job job, Tables tb) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ unsigned long long s_tmp64[NWARP];
+    __shared__ int s_tmp32[NWARP];
+    __shared__ long long s_tile;
+    __shared__ int s_last_end, s_first_start, s_nbad;
+    __shared__ unsigned long long s_pre_out, s_pre_lines;
+    __shared__ unsigned s_esc;
+
+    const BpSmem S = carve_bp(smem, tb.n_flat);
+    for (int k = threadIdx.x; k < tb.n_flat; k += NT) S.expflat[k] = tb.exp_flat[k];
+    for (int k = threadIdx.x; k < 257; k += NT) S.expoff[k] = tb.exp_off[k];
+    for (int k = threadIdx.x; k < 256; k += NT) S.explen[k] = tb.exp_len[k];
+    const int tid = threadIdx.x;
+    PhaseClock pc;
+    pc.start();
+
+    for (;;) {
+        __syncthreads();
+        pc.mark(job, 7);  // end of previous tile
+        if (tid == 0) {
+            s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
+            s_nbad = 0;
+            s_esc = 0;
+            s_last_end = -1;
+            s_first_start = 0x7fffffff;
+        }
+        __syncthreads();
+        const long long t = s_tile;
+        if (t >= job.n_tiles) break;
+        const long long T0 = t * (long long)TILE;
+        const int tile_len = (int)min((long long)TILE, job.n - T0);
+        const long long ws = T0 - HEAD;
+        const long long we = min(job.n, T0 + TILE + EXTRA);
+        const int win_len = (int)(we - ws);
+        const bool hits_eof = we == job.n;
+        load_window(job.in, job.n, ws, align16(win_len), S.win);
+        for (int k = tid; k < BP_BADW; k += NT) S.bad[k] = 0u;
+        __syncthreads();
+        if (tid == 0) S.win[win_len] = hits_eof ? '\n' : S.win[win_len];
+        const int my_cnt = scan_starts(S.win, tile_len, 0, nullptr, 0, 0);
+        int tile_lines;
+        const int my_off = block_exscan<int>(my_cnt, s_tmp32, tile_lines);
+        const int c0 = tid * CHUNK, c1 = min(c0 + CHUNK, tile_len);
+        // the thread holding the tile end finishes the last record (overhang)
+        const bool tail = c0 < tile_len && c1 == tile_len;
+        if (tail && tile_lines > 0) {
+            int e = HEAD + tile_len;
+            // the last owned record ends at the first '\n' at or after the
+            // tile end -- unless the tile's last byte is itself a '\n'
+            if (S.win[HEAD + tile_len - 1] == '\n') {
+                e = HEAD + tile_len - 1;
+            } else {
+                while (e < win_len && S.win[e] != '\n') ++e;
+                if (e >= win_len && !hits_eof) {
+                    long long g = ws + e;
+                    while (g < job.n && job.in[g] != '\n') ++g;
+                    e = (int)(g - ws);
+                }
+            }
+            s_last_end = e;
+        }
+        __syncthreads();
+        pc.mark(job, 0);  // ticket, load, start scan, last record end
+        const int last_end = s_last_end;
+        const BpBytes B{S.win, job.in, ws, hits_eof ? win_len + 1 : win_len};
+        // my slice: [HEAD + c0, HEAD + c1), plus (tail) up to last_end inclusive
+        const int p0 = HEAD + c0;
+        const int p1 = tail ? last_end + 1 : HEAD + c1;
+        const bool resident = last_end < (hits_eof ? win_len + 1 : win_len);
+        // escape parity at the slice start
+        bool esc0 = false;
+        if (p0 < p1 && S.win[p0 - 1] != '\n') {
+            int r = 0;
+            while (p0 - 1 - r > 0 && S.win[p0 - 1 - r] == 0x20) ++r;
+            esc0 = r & 1;
+        }
+        // Per-byte role, branch-free (selects + predicated stores):
+        //   start : a record starts here (ord++, escape state reset)
+        //   nl    : '\n' record end (outputs '\n' for a good record)
+        //   lit   : escaped literal (outputs the byte)
+        //   mark  : 0x20 escape marker (outputs nothing)
+        //   code  : dictionary code (outputs explen bytes; explen 0 = error)
+        // Non-resident tiles (last record longer than the window) read HBM
+        // through B on the same path.
+        const int tile_end = HEAD + tile_len;
+        BpWalk W;
+        W.a_win = sa(S.win);
+        W.a_len = sa(S.explen);
+        W.a_bad = sa(S.bad);
+        W.a_off = sa(S.expoff);
+        W.a_flat = sa(S.expflat);
+        W.a_out = sa(S.out);
+        W.p0 = p0;
+        W.p1 = p1;
+        W.tile_end = tile_end;
+        W.ord0 = my_off - 1;
+        W.esc0 = esc0;
+        W.short_exp = tb.max_exp <= 8;
+        unsigned dummy = 0, my_sum = 0, my_esc = 0;
+        // ---- (1) validate ----
+        if (resident) bp_walk<0, true>(W, S, B, S.bad, dummy, dummy, nullptr, 0);
+        else bp_walk<0, false>(W, S, B, S.bad, dummy, dummy, nullptr, 0);
+        __syncthreads();
+        // ---- (2) output bytes of good records in my slice ----
+        if (resident) bp_walk<1, true>(W, S, B, S.bad, my_sum, my_esc, nullptr, 0);
+        else bp_walk<1, false>(W, S, B, S.bad, my_sum, my_esc, nullptr, 0);
+        unsigned long long tile_out;
+        const unsigned long long my_base = block_exscan<unsigned long long>(my_sum, s_tmp64, tile_out);
+        if (my_esc) atomicAdd(&s_esc, my_esc);
+        if (tid == 0) lookback_publish(job.ts, t, tile_out, (unsigned long long)tile_lines);
+        const bool staged = resident && tile_out <= (unsigned long long)DOUTCAP;
+        // ---- (3) expand: to smem now when staged, else to HBM after the look-back ----
+        if (staged) bp_walk<2, true>(W, S, B, S.bad, dummy, dummy, nullptr, my_base);
+        pc.mark(job, 3);  // thread 0's expand
+        if (tid < 32) {
+            unsigned long long po, pl;
+            lookback_resolve(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
+            if (tid == 0) {
+                s_pre_out = po;
+                s_pre_lines = pl;
+            }
+        }
+        // bad records: count, and the stats/error details (rare, serial)
+        {
+            unsigned nb = 0;
+            for (int k = tid; k < (tile_lines + 31) / 32; k += NT) nb += __popc(S.bad[k]);
+            if (nb) atomicAdd(&s_nbad, (int)nb);
+        }
+        __syncthreads();
+        pc.mark(job, 4);  // look-back + wait for the slowest expander
+        const unsigned long long pre_out = s_pre_out;
+        const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
+        if (tid == 0) {
+            const int nbad = s_nbad;
+            atomicAdd(&job.ctl->total_out, tile_out);
+            atomicAdd(&job.ctl->lines, (unsigned long long)(tile_lines - nbad));
+            atomicAdd(&job.ctl->in_lines, (unsigned long long)tile_lines);
+            if (!fits) atomicOr(&job.ctl->overflow, 1ull);
+            unsigned long long esc_bad = 0;
+            if (nbad) {
+                if (job.lenient) atomicAdd(&job.ctl->skipped, (unsigned long long)nbad);
+                // walk the bad records from the pristine input: escapes
+                // before the error count too (numba_impl.py:99-101)
+                int ord = -1, first_bad = -1;
+                for (long long x = T0; x < T0 + tile_len; ++x) {
+                    if (!(x == 0 || job.in[x - 1] == '\n')) continue;
+                    ++ord;
+                    if (!((S.bad[ord >> 5] >> (ord & 31)) & 1u)) continue;
+                    long long ge = x;
+                    while (ge < job.n && job.in[ge] != '\n') ++ge;
+                    long long m = 0, ep = -1;
+                    int code = 0;
+                    unsigned e2 = 0;
+                    const int kind = decode_size(job.in + x, ge - x, S.explen, &m, &ep, &code, &e2);
+                    esc_bad += e2;
+                    if (first_bad < 0) {
+                        first_bad = ord;
+                        if (!job.lenient) {
+                            TileErr e;
+                            e.kind = kind;
+                            e.code = code;
+                            e.offset = ep;
+                            e.ids[0] = e.ids[1] = 0;
+                            job.terr[t] = e;
+                            __threadfence();
+                            atomicMin(&job.ctl->err_key, ((s_pre_lines + (unsigned long long)ord) << 24) |
+                                                             (unsigned long long)(t & 0xffffff));
+                        }
+                    }
+                }
+            }
+            if (s_esc + esc_bad) atomicAdd(&job.ctl->escapes, (unsigned long long)s_esc + esc_bad);
+        }
+        pc.mark(job, 5);  // stats
+        if (!fits) continue;
+        if (staged) store_out(job.out + pre_out, S.out, (int)tile_out);
+        else if (resident) bp_walk<2, true>(W, S, B, S.bad, dummy, dummy, job.out, pre_out + my_base);
+        else bp_walk<2, false>(W, S, B, S.bad, dummy, dummy, job.out, pre_out + my_base);
+        pc.mark(job, 6);  // store
+    }
+}
+
 // ----------------------------------------------------------------------------
 // parity-shim kernels: reference kernel layouts, one thread per line, HBM
 // ----------------------------------------------------------------------------
