@@ -78,6 +78,7 @@ struct zs_ctx {
     DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2;
     int no_t2 = 0;  // debug: force the key-window DP
     int no_ip = 0;  // debug: force the decision-array kernel
+    int dec_variant = 1;  // 1: per-thread slices (default), 0: warp-cooperative
     // per-slot (double-buffered) work buffers
     DevBuf ctl[2], ts[2], terr[2], in[2], out[2], arena[2];  // arena: per slot
     // shim scratch
@@ -352,8 +353,13 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
             k<<<grid, NT, smem, st>>>(job, ctx->tb);
         } else {
             const int smem = bp_smem_bytes(ctx->tb.n_flat);
-            CK(set_smem(decompress_tiles_bp, smem));
-            decompress_tiles_bp<<<grid, NT, smem, st>>>(job, ctx->tb);
+            if (ctx->dec_variant == 1) {
+                CK(set_smem(decompress_tiles_bp, smem));
+                decompress_tiles_bp<<<grid, NT, smem, st>>>(job, ctx->tb);
+            } else {
+                CK(set_smem(decompress_tiles_wc, smem));
+                decompress_tiles_wc<<<grid, NT, smem, st>>>(job, ctx->tb);
+            }
         }
         CK(cudaGetLastError());
         if (timed) CK(cudaEventRecord(ctx->ev1, st));
@@ -743,6 +749,7 @@ int zs_build_t2_host(const int32_t *children, const int16_t *term_code, int32_t 
 
 int zs_set_transducer(zs_ctx *ctx, int on) {
     if (!ctx) return ZS_E_ARG;
+    ctx->dec_variant = (on & 4) ? 0 : 1;  // bit 2: warp-cooperative decompress
     ctx->no_t2 = (on & 1) ? 0 : 1;  // bit 0: transducer parse
     ctx->no_ip = (on & 2) ? 0 : 1;  // bit 1: in-place kernel (needs the transducer)
     return ZS_OK;

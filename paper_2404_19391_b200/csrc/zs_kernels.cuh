@@ -1672,6 +1672,320 @@ __global__ void __launch_bounds__(NT, 1) decompress_tiles_bp(Job job, Tables tb)
     }
 }
 
+// ============================================================================
+// Warp-cooperative decompress.  A warp owns a contiguous range of the tile's
+// compressed bytes and processes it in 32-byte blocks, one byte per lane
+// (conflict-free smem reads).  Byte roles come from ballot masks:
+//   SP = 0x20 bytes, NL = '\n' bytes.  Inside a maximal 0x20 run the bytes at
+//   even offsets from the run start are escape markers, odd offsets are
+//   literals; the byte after a run that ends on a marker is a literal
+//   (numba_impl.py:93-101 read sequentially).  Per block, with A = even bit
+//   positions, Rodd = runs whose start offset is odd (a run continuing from
+//   the previous block takes the carried parity):
+//     D_odd = SP & ~(SP + Rodd)        (carry fills each odd-start run)
+//     M     = SP & (A ^ D_odd)         markers
+//     LIT   = (SP & ~M) | (((M & runend) << 1) & ~SP) | carry-in literal
+//   A marker right before '\n' is a dangling escape (record error).
+// Record ordinals are popcounts of NL; output offsets are warp scans.
+// ============================================================================
+struct WcRoles {
+    unsigned nl, mark, lit, code, e_out;
+};
+
+__device__ __forceinline__ WcRoles wc_roles(unsigned b, bool valid, unsigned e_in) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned NL = __ballot_sync(0xffffffffu, valid && b == '\n');
+    const unsigned SP = __ballot_sync(0xffffffffu, valid && b == 0x20);
+    const unsigned VA = __ballot_sync(0xffffffffu, valid);
+    constexpr unsigned A = 0x55555555u;
+    const unsigned rstart = SP & ~(SP << 1);
+    const unsigned rodd = (rstart & ~A & ~1u) | (SP & e_in & 1u);
+    const unsigned d_odd = SP & ~(SP + rodd);
+    const unsigned M = SP & (A ^ d_odd);
+    const unsigned runend = SP & ~(SP >> 1);
+    const unsigned litc = (SP & ~M) | (((M & runend) << 1) & ~SP) | ((e_in & ~SP) & 1u);
+    WcRoles r;
+    r.nl = NL;
+    r.mark = M;
+    r.lit = litc & ~NL & VA;
+    r.code = VA & ~SP & ~NL & ~r.lit;
+    // error: a marker directly before '\n' (litc candidate on a NL byte)
+    r.e_out = (M >> 31) & 1u;
+    (void)lane;
+    return r;
+}
+
+__global__ void __launch_bounds__(NT, 1) decompress_tiles_wc(Job job, Tables tb) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ unsigned long long s_tmp64[NWARP];
+    __shared__ int s_tmp32[NWARP];
+    __shared__ long long s_tile;
+    __shared__ int s_last_end, s_first_start, s_nbad;
+    __shared__ unsigned long long s_pre_out, s_pre_lines;
+    __shared__ unsigned s_esc;
+
+    const BpSmem S = carve_bp(smem, tb.n_flat);
+    for (int k = threadIdx.x; k < tb.n_flat; k += NT) S.expflat[k] = tb.exp_flat[k];
+    for (int k = threadIdx.x; k < 257; k += NT) S.expoff[k] = tb.exp_off[k];
+    for (int k = threadIdx.x; k < 256; k += NT) S.explen[k] = tb.exp_len[k];
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, wid = tid >> 5;
+    const unsigned a_win = sa(S.win), a_len = sa(S.explen), a_bad = sa(S.bad);
+    const unsigned a_off = sa(S.expoff), a_flat = sa(S.expflat), a_out = sa(S.out);
+    const bool short_exp = tb.max_exp <= 8;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) {
+            s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
+            s_nbad = 0;
+            s_esc = 0;
+            s_last_end = -1;
+            s_first_start = 0x7fffffff;
+        }
+        __syncthreads();
+        const long long t = s_tile;
+        if (t >= job.n_tiles) break;
+        const long long T0 = t * (long long)TILE;
+        const int tile_len = (int)min((long long)TILE, job.n - T0);
+        const long long ws = T0 - HEAD;
+        const long long we = min(job.n, T0 + TILE + EXTRA);
+        const int win_len = (int)(we - ws);
+        const bool hits_eof = we == job.n;
+        load_window(job.in, job.n, ws, align16(win_len), S.win);
+        for (int k = tid; k < BP_BADW; k += NT) S.bad[k] = 0u;
+        __syncthreads();
+        if (tid == 0 && hits_eof) S.win[win_len] = '\n';
+        // owned range: [first owned start, end of the last owned record]
+        const int my_cnt = scan_starts(S.win, tile_len, 0, nullptr, 0, 0);
+        int tile_lines;
+        (void)block_exscan<int>(my_cnt, s_tmp32, tile_lines);
+        {
+            const int c0 = tid * CHUNK, c1 = min(c0 + CHUNK, tile_len);
+            for (int x = c0; x < c1; ++x)
+                if (S.win[HEAD + x - 1] == '\n') {
+                    atomicMin(&s_first_start, HEAD + x);
+                    break;
+                }
+            if (tid == 0 && tile_lines > 0) {
+                int e;
+                if (S.win[HEAD + tile_len - 1] == '\n') {
+                    e = HEAD + tile_len - 1;
+                } else {
+                    e = HEAD + tile_len;
+                    while (e < win_len && S.win[e] != '\n') ++e;
+                    if (e >= win_len && !hits_eof) {
+                        long long g = ws + e;
+                        while (g < job.n && job.in[g] != '\n') ++g;
+                        e = (int)(g - ws);
+                    }
+                }
+                s_last_end = e;
+            }
+        }
+        __syncthreads();
+        const int first = s_first_start, last_end = s_last_end;
+        const int lim = hits_eof ? win_len + 1 : win_len;  // resident bytes [0, lim)
+        const BpBytes B{S.win, job.in, ws, lim};
+        const bool resident = last_end < lim;
+        // warp ranges over [first, last_end], whole 32-byte blocks
+        int r0 = 0, r1 = 0;
+        if (tile_lines > 0) {
+            const int nblk = (last_end + 1 - first + 31) / 32;
+            r0 = first + 32 * (int)((long long)nblk * wid / NWARP);
+            r1 = first + 32 * (int)((long long)nblk * (wid + 1) / NWARP);
+            r1 = min(r1, last_end + 1);
+            r0 = min(r0, r1);
+        }
+        // pass 0: newlines per warp range -> ordinal base; escape carry-in
+        int nl_cnt = 0;
+        for (int q0 = r0; q0 < r1; q0 += 32) {
+            const int q = q0 + lane;
+            const bool valid = q < r1;
+            const unsigned b = valid ? (resident ? ldsb(a_win + q) : B(q)) : 0u;
+            nl_cnt += __popc(__ballot_sync(0xffffffffu, valid && b == '\n'));
+        }
+        int n_before;
+        {
+            int tot;
+            const int v = lane == 0 ? nl_cnt : 0;
+            n_before = block_exscan<int>(v, s_tmp32, tot);
+            n_before = __shfl_sync(0xffffffffu, n_before, 0);
+        }
+        unsigned e_in0 = 0;
+        if (lane == 0 && r0 < r1 && r0 > first) {
+            int rr = 0;
+            while (r0 - 1 - rr >= first && B(r0 - 1 - rr) == 0x20) ++rr;
+            // the run before r0 (within the record) ends in a marker iff its length is odd
+            e_in0 = rr & 1;
+        }
+        e_in0 = __shfl_sync(0xffffffffu, e_in0, 0);
+        // pass 1: validate
+        {
+            int ord = n_before;
+            unsigned e_in = e_in0;
+            for (int q0 = r0; q0 < r1; q0 += 32) {
+                const int q = q0 + lane;
+                const bool valid = q < r1;
+                const unsigned b = valid ? (resident ? ldsb(a_win + q) : B(q)) : 0u;
+                const WcRoles R = wc_roles(b, valid, e_in);
+                const unsigned me = 1u << lane;
+                const int my_ord = ord + __popc(R.nl & (me - 1));
+                const unsigned L = ldsb(a_len + b);
+                // dangling escape: the byte before this '\n' is a marker
+                const unsigned prev_mark = lane ? (R.mark >> (lane - 1)) & 1u : e_in;
+                const bool err = ((R.code & me) && L == 0) || ((R.nl & me) && prev_mark);
+                if (err) atomicOr(&S.bad[my_ord >> 5], 1u << (my_ord & 31));
+                ord += __popc(R.nl);
+                e_in = R.e_out;
+            }
+        }
+        __syncthreads();
+        // pass 2: output bytes of good records
+        unsigned long long wsum = 0;
+        unsigned wesc = 0;
+        {
+            int ord = n_before;
+            unsigned e_in = e_in0;
+            for (int q0 = r0; q0 < r1; q0 += 32) {
+                const int q = q0 + lane;
+                const bool valid = q < r1;
+                const unsigned b = valid ? (resident ? ldsb(a_win + q) : B(q)) : 0u;
+                const WcRoles R = wc_roles(b, valid, e_in);
+                const unsigned me = 1u << lane;
+                const int my_ord = ord + __popc(R.nl & (me - 1));
+                const bool good = valid && !((ldsw(a_bad + 4 * (my_ord >> 5)) >> (my_ord & 31)) & 1u);
+                const unsigned L = ldsb(a_len + b);
+                const unsigned add = (R.code & me) ? L : ((R.lit | R.nl) & me ? 1u : 0u);
+                unsigned v = good ? add : 0u;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                wsum += v;
+                wesc += __popc(__ballot_sync(0xffffffffu, good && (R.mark & me)));
+                ord += __popc(R.nl);
+                e_in = R.e_out;
+            }
+        }
+        unsigned long long tile_out;
+        const unsigned long long wbase = block_exscan<unsigned long long>(lane == 0 ? wsum : 0ull, s_tmp64, tile_out);
+        const unsigned long long my_wbase = __shfl_sync(0xffffffffu, wbase, 0);
+        if (lane == 0 && wesc) atomicAdd(&s_esc, wesc);
+        if (tid == 0) lookback_publish(job.ts, t, tile_out, (unsigned long long)tile_lines);
+        const bool staged = resident && tile_out <= (unsigned long long)DOUTCAP;
+        // pass 3: expand (smem when staged, else HBM after the look-back)
+        auto expand = [&](uint8_t *o_glob, unsigned long long base) {
+            int ord = n_before;
+            unsigned e_in = e_in0;
+            unsigned long long run = base;
+            for (int q0 = r0; q0 < r1; q0 += 32) {
+                const int q = q0 + lane;
+                const bool valid = q < r1;
+                const unsigned b = valid ? (resident ? ldsb(a_win + q) : B(q)) : 0u;
+                const WcRoles R = wc_roles(b, valid, e_in);
+                const unsigned me = 1u << lane;
+                const int my_ord = ord + __popc(R.nl & (me - 1));
+                const bool good = valid && !((ldsw(a_bad + 4 * (my_ord >> 5)) >> (my_ord & 31)) & 1u);
+                const bool is_code = R.code & me;
+                const unsigned L = ldsb(a_len + b);
+                const unsigned add = good ? (is_code ? L : ((R.lit | R.nl) & me ? 1u : 0u)) : 0u;
+                unsigned inc = add;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                const unsigned long long w = run + inc - add;
+                if (add) {
+                    if (o_glob == nullptr) {
+                        const unsigned ow = a_out + (unsigned)w;
+                        if (!is_code) {
+                            stsb(ow, b);
+                        } else {
+                            const unsigned e = a_flat + ldsh(a_off + 2 * b);
+                            if (short_exp) {
+#pragma unroll
+                                for (unsigned k = 0; k < 8; ++k)
+                                    if (k < L) stsb(ow + k, ldsb(e + k));
+                            } else {
+                                for (unsigned k = 0; k < L; ++k) stsb(ow + k, ldsb(e + k));
+                            }
+                        }
+                    } else {
+                        if (!is_code) {
+                            o_glob[w] = (uint8_t)b;
+                        } else {
+                            const uint8_t *e = S.expflat + S.expoff[b];
+                            for (unsigned k = 0; k < L; ++k) o_glob[w + k] = e[k];
+                        }
+                    }
+                }
+                run += __shfl_sync(0xffffffffu, inc, 31);
+                ord += __popc(R.nl);
+                e_in = R.e_out;
+            }
+        };
+        if (staged) expand(nullptr, my_wbase);
+        if (tid < 32) {
+            unsigned long long po, pl;
+            lookback_resolve(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
+            if (tid == 0) {
+                s_pre_out = po;
+                s_pre_lines = pl;
+            }
+        }
+        {
+            unsigned nb = 0;
+            for (int k = tid; k < (tile_lines + 31) / 32; k += NT) nb += __popc(S.bad[k]);
+            if (nb) atomicAdd(&s_nbad, (int)nb);
+        }
+        __syncthreads();
+        const unsigned long long pre_out = s_pre_out;
+        const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
+        if (tid == 0) {
+            const int nbad = s_nbad;
+            atomicAdd(&job.ctl->total_out, tile_out);
+            atomicAdd(&job.ctl->lines, (unsigned long long)(tile_lines - nbad));
+            atomicAdd(&job.ctl->in_lines, (unsigned long long)tile_lines);
+            if (!fits) atomicOr(&job.ctl->overflow, 1ull);
+            unsigned long long esc_bad = 0;
+            if (nbad) {
+                if (job.lenient) atomicAdd(&job.ctl->skipped, (unsigned long long)nbad);
+                int ord = -1, first_bad = -1;
+                for (long long x = T0; x < T0 + tile_len; ++x) {
+                    if (!(x == 0 || job.in[x - 1] == '\n')) continue;
+                    ++ord;
+                    if (!((S.bad[ord >> 5] >> (ord & 31)) & 1u)) continue;
+                    long long ge = x;
+                    while (ge < job.n && job.in[ge] != '\n') ++ge;
+                    long long m = 0, ep = -1;
+                    int code = 0;
+                    unsigned e2 = 0;
+                    const int kind = decode_size(job.in + x, ge - x, S.explen, &m, &ep, &code, &e2);
+                    esc_bad += e2;
+                    if (first_bad < 0) {
+                        first_bad = ord;
+                        if (!job.lenient) {
+                            TileErr e;
+                            e.kind = kind;
+                            e.code = code;
+                            e.offset = ep;
+                            e.ids[0] = e.ids[1] = 0;
+                            job.terr[t] = e;
+                            __threadfence();
+                            atomicMin(&job.ctl->err_key, ((s_pre_lines + (unsigned long long)ord) << 24) |
+                                                             (unsigned long long)(t & 0xffffff));
+                        }
+                    }
+                }
+            }
+            if (s_esc + esc_bad) atomicAdd(&job.ctl->escapes, (unsigned long long)s_esc + esc_bad);
+        }
+        if (!fits) continue;
+        if (staged) store_out(job.out + pre_out, S.out, (int)tile_out);
+        else expand(job.out, pre_out + my_wbase);
+    }
+}
+
 // ----------------------------------------------------------------------------
 // parity-shim kernels: reference kernel layouts, one thread per line, HBM
 // ----------------------------------------------------------------------------

@@ -335,11 +335,12 @@ def test_device_and_host_api_agree():
     assert (r.lines, r.out_bytes) == (res.lines, res.out_bytes)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 3])
+@pytest.mark.parametrize("mode", [0, 1, 3, 7])
 def test_kernel_variants_bit_exact(corpus_hashes, mode):
     """Every compress kernel variant (0: key-window DP with a decision array,
-    1: + cost-window transducer, 3: + in-place decisions, the default) gives
-    the reference bytes."""
+    1: + cost-window transducer, 3: + in-place decisions, the default; bit 2
+    selects the warp-cooperative decompress instead of the per-thread-slice
+    one) gives the reference bytes, both directions."""
     ctx = _lib.context()
     try:
         ctx.lib.zs_set_transducer(ctx.h, mode)
@@ -350,9 +351,33 @@ def test_kernel_variants_bit_exact(corpus_hashes, mode):
             for key, pre in (("pre_off", False), ("pre_on", True)):
                 comp, res = z.run_buffer(buf, d, "compress", preprocess=pre, lenient=True)
                 assert hashlib.sha256(comp.tobytes()).hexdigest() == e[key]["comp_sha256"], (name, key)
+                back, _ = z.run_buffer(comp, d, "decompress")
+                assert hashlib.sha256(back.tobytes()).hexdigest() == e[key]["roundtrip_sha256"]
         test_long_lines_global_path()
         test_growing_renumbering_line()
         test_many_tiny_lines_multiple_rounds()
         test_errors_across_tiles()
     finally:
         ctx.lib.zs_set_transducer(ctx.h, 3)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_gpu_codec(world):
+    """The multi-GPU shard protocol with the GPU codec per shard (all ranks
+    simulated on cuda:0) == the whole-buffer oracle stream."""
+    from paper_2404_19391_b200 import shard
+    t = oracle.Tables.from_zsd(golden_dict_bytes())
+    d = z.default_dictionary()
+    buf = synth.generate("skewed", 20000, 2025).tobytes()[:-1]
+    want, st = oracle.run_stream(t, buf, "compress", True, True, 8)
+    arr = np.frombuffer(buf, np.uint8)
+    cuts = shard.shard_bounds(arr, world)
+    fn = shard.gpu_codec(d, "compress", preprocess=True, lenient=True)
+    outs = [fn(arr[cuts[r]:cuts[r + 1]]) for r in range(world)]
+    res = [o[1] for o in outs]
+    blob = b""
+    for r in range(world):
+        v = shard.combine(res, r, False)
+        assert v.out_offset == len(blob)
+        blob += outs[r][0][:v.out_bytes]
+    assert blob == want and v.total_lines == st["lines"]
