@@ -8,10 +8,12 @@ dictionary, ring renumbering ON.  One *step* = compress the whole library
 stream back, through the fused sm_100a tile kernels.
 
   value : round-trip input MB/s on HBM-resident buffers =
-          N * input_bytes / (compress + decompress device time), max over ranks
+          N * input_bytes / (time of one compress + decompress step), the
+          step timed with CUDA events on the library stream around whole
+          device-API calls (memsets, kernels, result read-back), max over ranks
   e2e   : the same through the public host-buffer API (pinned host memory,
           H2D + kernels + D2H in the timed region)
-  roofline : dominant kernel (compress_tiles), algorithmic bytes =
+  roofline : dominant kernel (compress_tiles_ip), algorithmic bytes =
           input bytes + compressed bytes (both incl. newlines) per launch
           over the CUDA-event kernel time, vs MEASURED_PEAKS.json hbm_gbs.
 
@@ -27,7 +29,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -40,7 +41,7 @@ import numpy as np  # noqa: E402
 N_LINES = 10_000_000
 SEED = 2024
 KIND = "aromatic"
-METRIC = "round-trip (compress+decompress) input MB/s, 10M SMILES C2, ring renumbering on"
+METRIC = "input MB/s (device + end-to-end) for compress and decompress at 1/2/4/8 B200"
 
 
 def peaks():
@@ -53,58 +54,76 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled (NVML, every 5 ms) during the
+    timed region."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.sm, self.mx, self.reasons = [], 0.0, set()
+        self.stop = threading.Event()
+        self.t = None
+
+    def _handle(self, nv):
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _run(self):
+        import pynvml as nv
+        nv.nvmlInit()
+        h = self._handle(nv)
+        self.mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        while not self.stop.is_set():
+            self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for name, bit in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(name)
+            self.stop.wait(0.005)
+        nv.nvmlShutdown()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml  # noqa: F401
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.t:
+            self.t.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], 0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 6:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx = max(mx, float(f[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[2:6]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": self.mx or None, "reasons": sorted(self.reasons),
+                "samples": len(self.sm)}
+
+
+def traffic(kernel, lines):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed `ncu --set full` capture of this workload
+    (profiles/ncu_traffic.json, written by tools/ncu_hot.py traffic), or
+    None when no capture of this kernel at this size is committed."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            e = json.load(fh).get(kernel)
+    except (OSError, ValueError):
+        return None
+    if not e or e.get("lines") != lines:
+        return None
+    return int(e["dram_bytes"])
 
 
 def dist_env():
@@ -112,6 +131,17 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+WORKLOAD = ("C2: 10M synthetic SMILES (reference generator, seed 2024, aromatic 0.92), default "
+            "fixed dictionary, ring renumbering on, lenient")
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
 def run_reference(args, ws, rank):
@@ -122,7 +152,7 @@ def run_reference(args, ws, rank):
     import synth
     oracle.build()
     synth.build()
-    threads = os.cpu_count() or 1
+    threads = host_threads()
     sample_lines = args.ref_lines
     buf = synth.generate(KIND, sample_lines, SEED)
     with open(os.path.join(ROOT, "paper_2404_19391_b200", "data", "default.zsd"), "rb") as fh:
@@ -142,8 +172,9 @@ def run_reference(args, ws, rank):
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(1000 * tot / args.steps, 3), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-           "config": {"workload": "C2 10M SMILES (bounded sample per step)", "sample_lines": sample_lines,
-                      "preprocess": True, "dictionary": "default.zsd"},
+           "config": {"workload": WORKLOAD, "lines_per_gpu": args.lines,
+                      "parallelism": f"line-range shards x{ws}",
+                      "sample_lines_per_step": sample_lines},
            "cpu_baseline": {"value": round(v, 3), "unit": "MB/s", "cores": threads, "kind": "port",
                             "sample": f"first {sample_lines} lines of C2 ({buf.size} B), "
                                       "compress(preprocess on)+decompress per step"},
@@ -157,7 +188,7 @@ def cpu_baseline_sample(n_lines):
     import oracle
     import synth
     oracle.build()
-    threads = os.cpu_count() or 1
+    threads = host_threads()
     buf = synth.generate(KIND, n_lines, SEED)
     with open(os.path.join(ROOT, "paper_2404_19391_b200", "data", "default.zsd"), "rb") as fh:
         t = oracle.Tables.from_zsd(fh.read())
@@ -179,7 +210,7 @@ def cpu_baseline_sample(n_lines):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--lines", type=int, default=N_LINES)
@@ -221,42 +252,54 @@ def main():
     d_back = torch.empty(n_in + 64, dtype=torch.uint8, device=f"cuda:{local}")
     res_c, res_d = _lib.Result(), _lib.Result()
 
+    names = ["", ""]
+
     def step_device():
         rc = ctx.lib.zs_compress_device(ctx.h, d_in.data_ptr(), n_in, d_comp.data_ptr(),
                                         d_comp.numel(), flags, res_c)
         ctx.check(rc, "zs_compress_device")
         kc = ctx.last_kernel_ms()
+        names[0] = ctx.lib.zs_last_kernel(ctx.h).decode()
         rc = ctx.lib.zs_decompress_device(ctx.h, d_comp.data_ptr(), res_c.out_bytes,
                                           d_back.data_ptr(), d_back.numel(), 0, res_d)
         ctx.check(rc, "zs_decompress_device")
         kd = ctx.last_kernel_ms()
+        names[1] = ctx.lib.zs_last_kernel(ctx.h).decode()
         return kc, kd
 
     for _ in range(args.warmup):
         step_device()
     comp_bytes = res_c.out_bytes
-    # timed region: CUDA events on the library stream (kernel launches)
+    # timed region: barrier + synchronize on both sides; CUDA events on the
+    # library's stream bracket all K steps (whole calls: memsets, kernels,
+    # result read-back), per-kernel events inside each call explain it.
+    lib_stream = torch.cuda.ExternalStream(ctx.lib.zs_stream(ctx.h), device=f"cuda:{local}")
+    ev_a = torch.cuda.Event(enable_timing=True)
+    ev_b = torch.cuda.Event(enable_timing=True)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     kc_ms, kd_ms = [], []
+    launches = 0
     with ClockSampler(local) as clk:
+        ev_a.record(lib_stream)
         for _ in range(args.steps):
             kc, kd = step_device()
             kc_ms.append(kc)
             kd_ms.append(kd)
+            launches += res_c.gpu_launches + res_d.gpu_launches
+        ev_b.record(lib_stream)
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    t_c = sum(kc_ms) / 1000.0
-    t_d = sum(kd_ms) / 1000.0
-    t_step = (t_c + t_d) / args.steps
+    t_step = ev_a.elapsed_time(ev_b) / 1000.0 / args.steps
+    tcs = sum(kc_ms) / 1000.0 / args.steps
+    tds = sum(kd_ms) / 1000.0 / args.steps
     if dist:
-        tt = torch.tensor([t_step, t_c / args.steps, t_d / args.steps], device=f"cuda:{local}")
+        tt = torch.tensor([t_step, tcs, tds], device=f"cuda:{local}")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_step, tcs, tds = tt.tolist()
-    else:
-        tcs, tds = t_c / args.steps, t_d / args.steps
+    k_comp, k_dec = names
     value = ws * n_in / t_step / 1e6
 
     # end-to-end through the public host API (pinned host buffers)
@@ -281,10 +324,8 @@ def main():
             dist.barrier()
         t0 = time.perf_counter()
         e2e_steps = max(2, args.steps // 2)
-        launches = 0
         for _ in range(e2e_steps):
             step_host()
-            launches += rc_.gpu_launches + rd_.gpu_launches
         te = (time.perf_counter() - t0) / e2e_steps
         if dist:
             tt = torch.tensor([te], device=f"cuda:{local}")
@@ -308,9 +349,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1000, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic",
-            "config": {"workload": "C2: 10M synthetic SMILES (reference generator, seed 2024, "
-                                   "aromatic 0.92), default fixed dictionary, ring renumbering on, "
-                                   "lenient", "lines_per_gpu": args.lines, "input_bytes_per_gpu": n_in,
+            "config": {"workload": WORKLOAD, "lines_per_gpu": args.lines, "input_bytes_per_gpu": n_in,
                        "compressed_bytes": comp_bytes, "ratio": round(comp_bytes / n_in, 6),
                        "l2": "inputs (460 MB) larger than L2 (126 MB); no flush needed",
                        "parallelism": f"line-range shards x{ws}"},
@@ -319,13 +358,16 @@ def main():
                            "device_MBps_out": round(res_d.out_bytes / tds / 1e6, 3),
                            "kernel_ms": round(tds * 1000, 4),
                            "roofline": {"bound": "hbm", "achieved": round(ach_d, 2), "peak": peak,
-                                        "unit": "GB/s", "frac": round(ach_d / peak, 4)}},
+                                        "unit": "GB/s", "frac": round(ach_d / peak, 4),
+                                        "traffic": traffic(k_dec, args.lines), "kernel": k_dec}},
             "roofline": {"bound": "hbm", "achieved": round(ach_c, 2), "peak": peak, "unit": "GB/s",
-                         "frac": round(ach_c / peak, 4), "traffic": None,
-                         "kernel": "compress_tiles<6>", "peak_kind": peak_kind,
-                         "algorithmic_bytes_per_launch": int(alg_c)},
+                         "frac": round(ach_c / peak, 4), "traffic": traffic(k_comp, args.lines),
+                         "kernel": k_comp, "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": int(alg_c),
+                         "kernel_ms": round(tcs * 1000, 4),
+                         "share_of_step": round(tcs / t_step, 4)},
             "clocks": clk.summary(),
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": int(launches),
             "e2e": e2e,
         }
         if ws == 1 and not args.no_cpu_baseline:

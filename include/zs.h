@@ -143,6 +143,10 @@ int64_t zs_decompress_bound(zs_ctx *ctx, int64_t n);
 /* timing of the last whole-buffer call's main kernel (CUDA events on the
  * launching stream), milliseconds */
 float zs_last_kernel_ms(zs_ctx *ctx);
+/* name of that kernel (static string) */
+const char *zs_last_kernel(zs_ctx *ctx);
+/* the cudaStream_t the device API launches on (for events around whole calls) */
+void *zs_stream(zs_ctx *ctx);
 
 /* profiling aid: per-phase SM cycles of the tile kernels (summed over CTAs,
  * thread 0's view) for the last device-API call; off by default */

@@ -69,6 +69,7 @@ struct zs_ctx {
     int n_sm = 0;
     cudaStream_t stream[2] = {nullptr, nullptr};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    const char *last_kernel = "";
     cudaEvent_t ev_ctl[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
     std::string err;
     bool have_dict = false;
@@ -344,6 +345,7 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
             const int smem = ip_smem_bytes(ctx->tb.n_states, ctx->ht.n_windows);
             CK(set_smem(compress_tiles_ip, smem));
             compress_tiles_ip<<<grid, NT, smem, st>>>(job, ctx->tb);
+            ctx->last_kernel = "compress_tiles_ip";
         } else if (compress) {
             const bool t2 = ctx->fast_w && ctx->ht.t2_ok && !ctx->no_t2;
             TileKernel k = compress_kernel(ctx->fast_w, t2);
@@ -351,14 +353,18 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
                                                  t2 ? ctx->ht.n_windows : 0);
             CK(set_smem(k, smem));
             k<<<grid, NT, smem, st>>>(job, ctx->tb);
+            ctx->last_kernel = ctx->fast_w ? (t2 ? "compress_tiles<W,t2>" : "compress_tiles<W>")
+                                           : "compress_tiles<0>";
         } else {
             const int smem = bp_smem_bytes(ctx->tb.n_flat);
             if (ctx->dec_variant == 1) {
                 CK(set_smem(decompress_tiles_bp, smem));
                 decompress_tiles_bp<<<grid, NT, smem, st>>>(job, ctx->tb);
+                ctx->last_kernel = "decompress_tiles_bp";
             } else {
                 CK(set_smem(decompress_tiles_wc, smem));
                 decompress_tiles_wc<<<grid, NT, smem, st>>>(job, ctx->tb);
+                ctx->last_kernel = "decompress_tiles_wc";
             }
         }
         CK(cudaGetLastError());
@@ -637,6 +643,8 @@ int zs_ctx_destroy(zs_ctx *ctx) {
 const char *zs_last_error(zs_ctx *ctx) { return ctx ? ctx->err.c_str() : "no context"; }
 
 float zs_last_kernel_ms(zs_ctx *ctx) { return ctx ? ctx->last_ms : 0.f; }
+const char *zs_last_kernel(zs_ctx *ctx) { return ctx ? ctx->last_kernel : ""; }
+void *zs_stream(zs_ctx *ctx) { return ctx ? (void *)ctx->stream[0] : nullptr; }
 
 int zs_set_phase_timing(zs_ctx *ctx, int on) {
     if (!ctx) return ZS_E_ARG;

@@ -24,7 +24,7 @@ NCOL, FAST_W = 97, 8
 def test_header_symbols_exported():
     lib = _lib.load()
     with open(f"{ROOT}/include/zs.h") as fh:
-        declared = set(re.findall(r"^(?:int|int64_t|float|const char \*)\s*\*?\s*(zs_\w+)\(",
+        declared = set(re.findall(r"^(?:int|int64_t|float|void|const char)\s*\*?\s*(zs_\w+)\(",
                                   fh.read(), re.M))
     assert declared == set(_lib.EXPORTS)
     for name in declared:
