@@ -18,6 +18,7 @@
 
 #include "../../include/zs.h"
 #include "zs_kernels.cuh"
+#include "zs_fx.cuh"
 
 using namespace zs;
 
@@ -76,7 +77,9 @@ struct zs_ctx {
     HostTables ht;
     Tables tb{};
     int fast_w = 0;
-    DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2;
+    DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2, d_fx;
+    bool fx_ok = false;  // streaming decode kernel serves this dictionary (max expansion <= 7)
+    int fx_blocks = 0;   // resident decompress_fx CTAs per SM
     int no_t2 = 0;  // debug: force the key-window DP
     int no_ip = 0;  // debug: force the decision-array kernel
     int dec_variant = 1;  // 1: per-thread slices (default), 0: warp-cooperative
@@ -310,9 +313,10 @@ BatchKernel batch_kernel(int w) {
 
 // one whole-buffer launch (device pointers) on `slot`'s buffers and stream
 int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, long long n,
-                  uint8_t *d_out, long long out_cap, int flags, bool timed) {
+                  uint8_t *d_out, long long out_cap, int flags, bool timed, bool general = false) {
     const bool ip = compress && ctx->fast_w && ctx->ht.t2_ok && !ctx->no_t2 && !ctx->no_ip;
-    const long long tile = ip ? CTILE : TILE;
+    const bool fx = !compress && ctx->fx_ok && !general && ctx->dec_variant == 1;
+    const long long tile = ip ? CTILE : fx ? FX_TILE : TILE;
     const long long nt = (n + tile - 1) / tile;
     cudaStream_t st = ctx->stream[slot];
     if (ctx->ctl[slot].reserve(sizeof(Ctl)) || ctx->ts[slot].reserve(sizeof(TileState) * (nt + 1)) ||
@@ -355,6 +359,15 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
             k<<<grid, NT, smem, st>>>(job, ctx->tb);
             ctx->last_kernel = ctx->fast_w ? (t2 ? "compress_tiles<W,t2>" : "compress_tiles<W>")
                                            : "compress_tiles<0>";
+        } else if (fx) {
+            const bool al = (reinterpret_cast<uintptr_t>(d_in) & 15) == 0;
+            auto k = al ? decompress_fx<true> : decompress_fx<false>;
+            CK(set_smem(k, FX_SMEM));
+            if (!ctx->fx_blocks)
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->fx_blocks, k, FX_NT, FX_SMEM));
+            const int g = (int)std::min<long long>(nt, (long long)ctx->n_sm * std::max(1, ctx->fx_blocks));
+            k<<<g, FX_NT, FX_SMEM, st>>>(job, ctx->d_fx.as<unsigned long long>());
+            ctx->last_kernel = "decompress_fx";
         } else {
             const int smem = bp_smem_bytes(ctx->tb.n_flat);
             if (ctx->dec_variant == 1) {
@@ -387,6 +400,7 @@ int collect(zs_ctx *ctx, int slot, long long n, const uint8_t *h_last_byte_src, 
         return 1;
     }
     (void)h_last_byte_src;
+    if (c.overflow & 4ull) return 3;  // streaming decode met a bad record: re-run record-aware
     zs_result r{};
     r.lines = (long long)c.lines;
     r.in_bytes = n;
@@ -445,13 +459,18 @@ int run_device(zs_ctx *ctx, bool compress, const uint8_t *d_in, int64_t n, uint8
         CK(cudaStreamSynchronize(ctx->stream[0]));
         trailing = last == '\n';
     }
-    for (int attempt = 0; attempt < 4; ++attempt) {
-        int rc = launch_stream(ctx, 0, compress, d_in, n, d_out, out_cap, flags, true);
+    bool general = false;
+    for (int attempt = 0; attempt < 5; ++attempt) {
+        int rc = launch_stream(ctx, 0, compress, d_in, n, d_out, out_cap, flags, true, general);
         if (rc) return rc;
         CK(cudaEventSynchronize(ctx->ev_ctl[0]));
         if (n > 0) CK(cudaEventElapsedTime(&ctx->last_ms, ctx->ev0, ctx->ev1));
         rc = collect(ctx, 0, n, nullptr, trailing, 0, res, false);
         if (rc == 1) continue;  // arena grown, re-run
+        if (rc == 3) {          // bad record: the record-aware kernel decides
+            general = true;
+            continue;
+        }
         if (rc == 2) {
             res->out_bytes = (long long)ctx->h_ctl[0].total_out;
             return ZS_E_CAPACITY;
@@ -484,6 +503,7 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
     }
     const int nch = (int)cuts.size() - 1;
     long long written = 0, line_base = 0;
+    bool general = false;  // a chunk hit a bad record: the record-aware kernel from then on
     bool capacity_hit = false;
     int pending = -1;  // slot whose output is waiting for D2H
     long long pend_len = 0, pend_n = 0;
@@ -497,7 +517,7 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
         int rc = collect(ctx, slot, cn, nullptr, true, line_base, &r, false);
         if (rc < 0) return rc;
         (void)clen;
-        if (rc == 1 || rc == 2) return 10 + rc;  // caller re-runs this chunk synchronously
+        if (rc == 1 || rc == 2 || rc == 3) return 10 + rc;  // caller re-runs this chunk synchronously
         long long ob = (long long)ctx->h_ctl[slot].total_out;
         if (!capacity_hit && written + ob <= out_cap && ob > 0 && !r.err_line)
             CK(cudaMemcpyAsync(h_out + written, ctx->out[slot].p, ob, cudaMemcpyDeviceToHost,
@@ -542,8 +562,10 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
                     return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(out)");
                 CK(cudaMemcpyAsync(ctx->in[ps].p, h_in + cuts[k - 1], pend_n, cudaMemcpyHostToDevice,
                                    ctx->stream[ps]));
+                general |= rc == 13;
                 rc = launch_stream(ctx, ps, compress, ctx->in[ps].as<uint8_t>(), pend_n,
-                                   ctx->out[ps].as<uint8_t>(), (long long)ctx->out[ps].cap, flags, false);
+                                   ctx->out[ps].as<uint8_t>(), (long long)ctx->out[ps].cap, flags, false,
+                                   general);
                 if (rc) return rc;
                 rc = finish(ps, pend_n, pend_len);
             }
@@ -561,8 +583,10 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
                 return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(out)");
             CK(cudaMemcpyAsync(ctx->in[ps].p, h_in + cuts[nch - 1], pend_n, cudaMemcpyHostToDevice,
                                ctx->stream[ps]));
+            general |= rc == 13;
             rc = launch_stream(ctx, ps, compress, ctx->in[ps].as<uint8_t>(), pend_n,
-                               ctx->out[ps].as<uint8_t>(), (long long)ctx->out[ps].cap, flags, false);
+                               ctx->out[ps].as<uint8_t>(), (long long)ctx->out[ps].cap, flags, false,
+                               general);
             if (rc) return rc;
             rc = finish(ps, pend_n, pend_len);
         }
@@ -622,7 +646,7 @@ int zs_ctx_destroy(zs_ctx *ctx) {
     if (!ctx) return ZS_OK;
     cudaSetDevice(ctx->dev);
     for (DevBuf *b : {&ctx->d_dfa2, &ctx->d_t2, &ctx->d_dfa, &ctx->d_codes, &ctx->d_children, &ctx->d_term, &ctx->d_explen,
-                      &ctx->d_expoff, &ctx->d_expflat, &ctx->ctl[0], &ctx->ctl[1], &ctx->ts[0],
+                      &ctx->d_expoff, &ctx->d_expflat, &ctx->d_fx, &ctx->ctl[0], &ctx->ctl[1], &ctx->ts[0],
                       &ctx->ts[1], &ctx->terr[0], &ctx->terr[1], &ctx->in[0], &ctx->in[1],
                       &ctx->out[0], &ctx->out[1], &ctx->arena[0], &ctx->arena[1], &ctx->s_flat, &ctx->s_starts,
                       &ctx->s_out, &ctx->s_lens, &ctx->s_dec, &ctx->s_stat, &ctx->s_errpos,
@@ -709,6 +733,11 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
         CK(up(ctx->d_dfa2, ht.dfa2.data(), ht.dfa2.size() * 2));
         CK(up(ctx->d_t2, ht.t2.data(), ht.t2.size() * 4));
     }
+    {
+        unsigned long long fxt[256];
+        for (int b = 0; b < 256; ++b) fxt[b] = fx_entry(b, ht.exp_len, ht.exp_off, ht.exp_flat.data());
+        CK(up(ctx->d_fx, fxt, sizeof fxt));
+    }
     Tables &tb = ctx->tb;
     tb.dfa = ht.fast ? ctx->d_dfa.as<uint16_t>() : nullptr;
     tb.codes = ht.fast ? ctx->d_codes.as<uint8_t>() : nullptr;
@@ -727,6 +756,7 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
     tb.n_flat = (int)exp_off[256];
     tb.max_exp = 0;
     for (int b = 0; b < 256; ++b) tb.max_exp = std::max<int>(tb.max_exp, ht.exp_len[b]);
+    ctx->fx_ok = tb.max_exp <= 7;
     ctx->fast_w = 0;
     if (ht.fast) {
         const int L = std::max(1, ht.max_len);

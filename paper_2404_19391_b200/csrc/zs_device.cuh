@@ -267,6 +267,31 @@ __device__ __forceinline__ T block_exscan(T v, T *warp_tmp, T &total) {
     return base + x - v;
 }
 
+// block-wide exclusive scan for a CTA of NTH threads (NTH / 32 <= 32)
+template <typename T, int NTH>
+__device__ __forceinline__ T block_exscan_n(T v, T *warp_tmp, T &total) {
+    constexpr int NW = NTH / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tmp[wid] = x;
+    __syncthreads();
+    T base = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+        const T wv = warp_tmp[k];
+        base += k < wid ? wv : T(0);
+        tot += wv;
+    }
+    total = tot;
+    __syncthreads();
+    return base + x - v;
+}
+
 // ----------------------------------------------------------------------------
 // decoupled look-back over tiles, one warp (ordered tickets guarantee
 // progress).  Lanes inspect 32 predecessors per round trip: the nearest one

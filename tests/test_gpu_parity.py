@@ -381,3 +381,47 @@ def test_sharded_gpu_codec(world):
         assert v.out_offset == len(blob)
         blob += outs[r][0][:v.out_bytes]
     assert blob == want and v.total_lines == st["lines"]
+
+
+def test_streaming_decode_edges():
+    """decompress_fx (byte-local streaming decode): 0x20 runs across thread
+    chunks and tiles, a final record without '\\n', unaligned device input,
+    and bad records that hand the buffer to the record-aware kernel."""
+    import torch
+    d = z.Dictionary([b"CC", b"c1"], "smiles")
+    t = oracle.Tables(d.learned, bytes(sorted(d.identity)))
+    rng = random.Random(21)
+    lines = []
+    for i in range(6000):
+        k = rng.randrange(6)
+        if k == 0:
+            lines.append(b" " * rng.randrange(1, 90))
+        elif k == 1:
+            lines.append(b"C " * rng.randrange(1, 20) + b"\t\xff")
+        else:
+            lines.append(bytes(rng.choice(b"Cc1()= \x7f") for _ in range(rng.randrange(0, 60))))
+    for tail in (b"\n", b"", b"  x"):
+        payload = b"\n".join(lines) + tail
+        comp = _oracle_check(payload, d, False, True)
+        assert comp is not None and comp.count(b"  ") > 1000
+        _oracle_check(comp, d, False, False, "decompress")
+        _oracle_check(comp, d, False, True, "decompress")
+        # device API at every input alignment
+        ctx = _lib.context()
+        want, _ = oracle.run_stream(t, comp, "decompress", False, False, 1)
+        for off in (0, 1, 7, 13):
+            din = torch.zeros(len(comp) + 16, dtype=torch.uint8, device="cuda")
+            din[off:off + len(comp)] = torch.frombuffer(bytearray(comp), dtype=torch.uint8).cuda()
+            dout = torch.empty(8 * len(comp) + 64, dtype=torch.uint8, device="cuda")
+            r = _lib.Result()
+            with ctx.lock:
+                ctx.set_dictionary(d)
+                rc = ctx.lib.zs_decompress_device(ctx.h, din.data_ptr() + off, len(comp),
+                                                  dout.data_ptr(), dout.numel(), 0, r)
+                ctx.check(rc, "zs_decompress_device")
+            assert dout[:r.out_bytes].cpu().numpy().tobytes() == want, off
+    # a dangling escape at EOF, an escaped '\n', unknown codes: record-aware path
+    comp = _oracle_check(b"\n".join(lines) + b"\n", d, False, True)
+    for bad in (comp + b"C ", comp[:5000] + b" \n" + comp[5000:], comp[:9000] + b"\x99" + comp[9000:]):
+        _oracle_check(bad, d, False, True, "decompress")
+        _oracle_check(bad, d, False, False, "decompress")
