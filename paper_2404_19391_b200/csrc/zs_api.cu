@@ -77,14 +77,15 @@ struct zs_ctx {
     HostTables ht;
     Tables tb{};
     int fast_w = 0;
-    DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2, d_fx;
+    DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2, d_fxc, d_fxe;
     bool fx_ok = false;  // streaming decode kernel serves this dictionary (max expansion <= 7)
-    int fx_blocks = 0;   // resident decompress_fx CTAs per SM
+    int fx_blocks[2] = {0, 0};  // resident fx_count / fx_emit CTAs per SM
     int no_t2 = 0;  // debug: force the key-window DP
     int no_ip = 0;  // debug: force the decision-array kernel
     int dec_variant = 1;  // 1: per-thread slices (default), 0: warp-cooperative
     // per-slot (double-buffered) work buffers
     DevBuf ctl[2], ts[2], terr[2], in[2], out[2], arena[2];  // arena: per slot
+    DevBuf fxs[2];  // streaming-decode scratch per slot
     // shim scratch
     DevBuf s_flat, s_starts, s_out, s_lens, s_dec, s_stat, s_errpos, s_tot, s_ids, s_outst;
     Ctl *h_ctl = nullptr;  // pinned, 2 slots
@@ -361,13 +362,22 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
                                            : "compress_tiles<0>";
         } else if (fx) {
             const bool al = (reinterpret_cast<uintptr_t>(d_in) & 15) == 0;
-            auto k = al ? decompress_fx<true> : decompress_fx<false>;
-            CK(set_smem(k, FX_SMEM));
-            if (!ctx->fx_blocks)
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->fx_blocks, k, FX_NT, FX_SMEM));
-            const int g = (int)std::min<long long>(nt, (long long)ctx->n_sm * std::max(1, ctx->fx_blocks));
-            k<<<g, FX_NT, FX_SMEM, st>>>(job, ctx->d_fx.as<unsigned long long>());
-            ctx->last_kernel = "decompress_fx";
+            if (ctx->fxs[slot].reserve(fx_scratch_bytes(nt)))
+                return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(fx scratch)");
+            const FxScratch sc = fx_carve(ctx->fxs[slot].p, nt);
+            auto kc = al ? fx_count<true> : fx_count<false>;
+            auto ke = al ? fx_emit<true> : fx_emit<false>;
+            CK(set_smem(kc, FX_CNT_SMEM));
+            CK(set_smem(ke, FX_EMIT_SMEM));
+            if (!ctx->fx_blocks[0]) {
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->fx_blocks[0], kc, FX_NT, FX_CNT_SMEM));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->fx_blocks[1], ke, FX_NT, FX_EMIT_SMEM));
+            }
+            auto grid_of = [&](int b) { return (int)std::min<long long>(nt, (long long)ctx->n_sm * std::max(1, b)); };
+            kc<<<grid_of(ctx->fx_blocks[0]), FX_NT, FX_CNT_SMEM, st>>>(job, ctx->d_fxc.as<unsigned>(), sc);
+            fx_scan<<<1, 1024, 0, st>>>(job, sc);
+            ke<<<grid_of(ctx->fx_blocks[1]), FX_NT, FX_EMIT_SMEM, st>>>(job, ctx->d_fxe.as<unsigned long long>(), sc);
+            ctx->last_kernel = "fx_count+fx_scan+fx_emit";
         } else {
             const int smem = bp_smem_bytes(ctx->tb.n_flat);
             if (ctx->dec_variant == 1) {
@@ -646,7 +656,7 @@ int zs_ctx_destroy(zs_ctx *ctx) {
     if (!ctx) return ZS_OK;
     cudaSetDevice(ctx->dev);
     for (DevBuf *b : {&ctx->d_dfa2, &ctx->d_t2, &ctx->d_dfa, &ctx->d_codes, &ctx->d_children, &ctx->d_term, &ctx->d_explen,
-                      &ctx->d_expoff, &ctx->d_expflat, &ctx->d_fx, &ctx->ctl[0], &ctx->ctl[1], &ctx->ts[0],
+                      &ctx->d_expoff, &ctx->d_expflat, &ctx->d_fxc, &ctx->d_fxe, &ctx->fxs[0], &ctx->fxs[1], &ctx->ctl[0], &ctx->ctl[1], &ctx->ts[0],
                       &ctx->ts[1], &ctx->terr[0], &ctx->terr[1], &ctx->in[0], &ctx->in[1],
                       &ctx->out[0], &ctx->out[1], &ctx->arena[0], &ctx->arena[1], &ctx->s_flat, &ctx->s_starts,
                       &ctx->s_out, &ctx->s_lens, &ctx->s_dec, &ctx->s_stat, &ctx->s_errpos,
@@ -734,9 +744,14 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
         CK(up(ctx->d_t2, ht.t2.data(), ht.t2.size() * 4));
     }
     {
-        unsigned long long fxt[256];
-        for (int b = 0; b < 256; ++b) fxt[b] = fx_entry(b, ht.exp_len, ht.exp_off, ht.exp_flat.data());
-        CK(up(ctx->d_fx, fxt, sizeof fxt));
+        unsigned fxc[256];
+        unsigned long long fxe[256];
+        for (int b = 0; b < 256; ++b) {
+            fxc[b] = fx_count_entry(b, ht.exp_len);
+            fxe[b] = fx_emit_entry(b, ht.exp_len, ht.exp_off, ht.exp_flat.data());
+        }
+        CK(up(ctx->d_fxc, fxc, sizeof fxc));
+        CK(up(ctx->d_fxe, fxe, sizeof fxe));
     }
     Tables &tb = ctx->tb;
     tb.dfa = ht.fast ? ctx->d_dfa.as<uint16_t>() : nullptr;

@@ -1,22 +1,29 @@
-// zs_fx.cuh -- streaming decompress kernel (the decode hot path).
+// zs_fx.cuh -- streaming decompress (the decode hot path).
 //
 // Decode is byte-local: every compressed byte maps to its expansion
 // (numba_impl.py:115-139), '\n' to itself, a 0x20 mark to nothing and the
-// byte after a mark to itself.  Records only matter for errors, so this
-// kernel ignores them: each thread owns 32 consecutive compressed bytes,
-//   pass 1  sums the output bytes of its bytes (one table lookup each),
-//   scan    block exclusive scan + decoupled look-back over tiles,
-//   pass 2  appends the expansions to a 64-bit accumulator and writes
-//           aligned 8-byte words straight to HBM (head/tail bytes singly).
-// Any unknown code or dangling escape (numba_impl.py:94-109) sets
-// Ctl.overflow bit 2 and the host re-runs the buffer through the
-// record-aware kernel (decompress_tiles_bp), which owns error semantics.
+// byte after a mark to itself.  Records only matter for errors, so the
+// streaming path ignores them.  A buffer is cut into 8 KB tiles; each thread
+// of a 256-thread CTA owns 32 consecutive compressed bytes.  Three launches:
 //
-// Expansion table: u64 per code, bytes 0-6 = expansion, bits 56-59 = length,
-// bit 60 = invalid code, bit 61 = escape mark, bit 62 = record end.  It is
-// replicated 16x ([code][lane & 15]) so a warp's 64-bit lookups (two
-// half-warp wavefronts) never conflict on a bank.  Serves dictionaries whose
-// longest expansion is <= 7 bytes (the default one: 6).
+//   fx_count  one table lookup per byte sums the output bytes of each
+//             thread's slice; a block scan gives every thread its u16 offset
+//             inside the tile; tile totals, record and escape counts, and a
+//             per-tile "has escapes" flag go to HBM.  Unknown codes and
+//             dangling escapes (numba_impl.py:94-109) set Ctl.overflow bit 2:
+//             the host then re-runs the buffer through the record-aware
+//             kernel (decompress_tiles_bp), which owns the error semantics.
+//   fx_scan   one CTA: exclusive scan of the tile totals -> tile offsets.
+//   fx_emit   each thread appends its expansions to a 64-bit accumulator and
+//             stores whole 8-byte words into a zeroed smem staging tile (the
+//             two words it shares with its neighbours via atomic OR); the
+//             tile then leaves with aligned 16-byte stores.
+//
+// Tables (built on the host from the reference decode tables,
+// dictionary.py:112-129), replicated per bank so lookups never conflict:
+//   count: u32 [code][32 lanes] = len | invalid << 8 | mark << 16 | nl << 24
+//   emit : u64 [code][16 lanes] = expansion bytes 0-6 | len << 56
+// Serves dictionaries whose longest expansion is <= 7 bytes (default: 6).
 #pragma once
 #include "zs_device.cuh"
 
@@ -25,30 +32,53 @@ namespace zs {
 constexpr int FX_NT = 256;               // threads per CTA
 constexpr int FX_B = 32;                 // compressed bytes per thread per tile
 constexpr int FX_TILE = FX_NT * FX_B;    // 8 KB of compressed input per tile
-constexpr int FX_REP = 16;               // table replicas
-constexpr unsigned long long FX_LEN_SHIFT = 56;
-constexpr unsigned long long FX_INVALID = 1ull << 60;
-constexpr unsigned long long FX_MARK = 1ull << 61;
-constexpr unsigned long long FX_NL = 1ull << 62;
+constexpr int FX_STAGE = 24576;          // emit staging bytes (tile output + 16 alignment)
+constexpr int FX_CNT_SMEM = 256 * 32 * 4;
+constexpr int FX_EMIT_SMEM = 256 * 16 * 8 + FX_STAGE;
 constexpr unsigned long long FX_BYTES = (1ull << 56) - 1;
-constexpr int FX_SMEM = 256 * FX_REP * 8;
 
-// host: one table entry per code from the decode tables (dictionary.py:112-129)
-inline unsigned long long fx_entry(int b, const uint8_t *exp_len, const uint16_t *exp_off,
-                                   const uint8_t *exp_flat) {
-    if (b == '\n') return (unsigned long long)'\n' | (1ull << FX_LEN_SHIFT) | FX_NL;
-    if (b == 0x20) return FX_MARK;
+// per-slot scratch layout (device): tile totals, tile offsets, tile flags,
+// per-thread offsets inside the tile
+struct FxScratch {
+    unsigned *tsum;            // [n_tiles] output bytes of the tile
+    unsigned long long *toff;  // [n_tiles] exclusive prefix
+    uint8_t *tflag;            // [n_tiles] bit 0: escapes in the tile
+    uint16_t *off16;           // [n_tiles * FX_NT]
+};
+
+inline size_t fx_scratch_bytes(long long nt) {
+    return (size_t)nt * (4 + 8 + 1 + 2 * FX_NT) + 64;
+}
+
+inline FxScratch fx_carve(void *p, long long nt) {
+    FxScratch s;
+    uint8_t *q = reinterpret_cast<uint8_t *>(p);
+    s.toff = reinterpret_cast<unsigned long long *>(q); q += 8 * nt;
+    s.tsum = reinterpret_cast<unsigned *>(q); q += 4 * nt;
+    s.off16 = reinterpret_cast<uint16_t *>(q); q += 2 * nt * FX_NT;
+    s.tflag = q;
+    return s;
+}
+
+// host: table entries per code (a '\n' is a 1-byte code of itself)
+inline unsigned fx_count_entry(int b, const uint8_t *exp_len) {
+    if (b == '\n') return 1u | (1u << 24);
+    if (b == 0x20) return 1u << 16;
+    return exp_len[b] ? (unsigned)exp_len[b] : (1u << 8);
+}
+inline unsigned long long fx_emit_entry(int b, const uint8_t *exp_len, const uint16_t *exp_off,
+                                        const uint8_t *exp_flat) {
+    if (b == '\n') return (unsigned long long)'\n' | (1ull << 56);
     const int L = exp_len[b];
-    if (L == 0) return FX_INVALID;
-    unsigned long long e = (unsigned long long)L << FX_LEN_SHIFT;
+    if (b == 0x20 || L == 0) return 0;
+    unsigned long long e = (unsigned long long)L << 56;
     for (int k = 0; k < L && k < 7; ++k) e |= (unsigned long long)exp_flat[exp_off[b] + k] << (8 * k);
     return e;
 }
 
-__device__ __forceinline__ unsigned fx_byte(const uint4 &a, const uint4 &b, int k) {
-    const unsigned w = k < 4 ? a.x : k < 8 ? a.y : k < 12 ? a.z : k < 16 ? a.w
-                     : k < 20 ? b.x : k < 24 ? b.y : k < 28 ? b.z : b.w;
-    return (w >> (8 * (k & 3))) & 0xffu;
+__device__ __forceinline__ unsigned fx_word(const uint4 &a, const uint4 &b, int k) {
+    return k == 0 ? a.x : k == 1 ? a.y : k == 2 ? a.z : k == 3 ? a.w
+         : k == 4 ? b.x : k == 5 ? b.y : k == 6 ? b.z : b.w;
 }
 
 __device__ __forceinline__ unsigned long long lds64(unsigned a) {
@@ -61,164 +91,336 @@ __device__ __forceinline__ unsigned lds32(unsigned a) {
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
 }
+__device__ __forceinline__ void sts64(unsigned a, unsigned long long v) {
+    asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_or64(unsigned a, unsigned long long v) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"((unsigned)v) : "memory");
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a + 4), "r"((unsigned)(v >> 32)) : "memory");
+}
 
-// length of the 0x20 run ending just before position p (within [0, p))
-__device__ __forceinline__ bool fx_escaped(const uint8_t *in, long long p) {
+// parity of the 0x20 run ending just before position p: 1 = p is a literal
+__device__ __forceinline__ unsigned fx_escaped(const uint8_t *in, long long p) {
     long long r = 0;
     while (p - 1 - r >= 0 && in[p - 1 - r] == 0x20) ++r;
-    return r & 1;
+    return (unsigned)(r & 1);
 }
 
-// Writes `len` (<= 7) bytes of x at global byte address o, byte by byte.
-__device__ __forceinline__ void fx_put_bytes(uint8_t *o, unsigned long long x, int from, int to) {
-    for (int k = from; k < to; ++k) o[k] = (uint8_t)(x >> (8 * k));
-}
-
+// load the 32-byte slice at c0 (cnt valid bytes; the rest read as 0)
 template <bool ALIGNED>
-__global__ void __launch_bounds__(FX_NT) decompress_fx(Job job, const unsigned long long *tab) {
+__device__ __forceinline__ void fx_load(const uint8_t *in, long long c0, int cnt, uint4 &va, uint4 &vb) {
+    if (ALIGNED && cnt == FX_B) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(in + c0);
+        va = __ldcs(src);
+        vb = __ldcs(src + 1);
+    } else {
+        unsigned w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int k = 0; k < FX_B; ++k)
+            if (k < cnt) w[k >> 2] |= (unsigned)in[c0 + k] << (8 * (k & 3));
+        va = make_uint4(w[0], w[1], w[2], w[3]);
+        vb = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+}
+
+// exact walk of one slice with escapes: output bytes, records, literals, bad
+__device__ __forceinline__ void fx_walk_esc(const uint4 &va, const uint4 &vb, int cnt, unsigned esc,
+                                            const uint8_t *explen, unsigned &sum, unsigned &nl,
+                                            unsigned &nesc, unsigned &bad, unsigned &esc_out) {
+    sum = nl = nesc = bad = 0;
+    for (int k = 0; k < cnt; ++k) {
+        const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
+        const unsigned lit = esc;
+        const unsigned L = explen[b];
+        if (lit) {
+            bad |= b == '\n';
+            sum += 1;
+            nesc += 1;
+            esc = 0;
+        } else if (b == 0x20) {
+            esc = 1;
+        } else if (b == '\n') {
+            sum += 1;
+            nl += 1;
+        } else {
+            bad |= L == 0;
+            sum += L;
+        }
+    }
+    esc_out = esc;
+}
+
+// ---------------------------------------------------------------------------
+// fx_count: per-thread output bytes -> u16 tile offsets; tile totals/flags
+// ---------------------------------------------------------------------------
+template <bool ALIGNED>
+__global__ void __launch_bounds__(FX_NT) fx_count(Job job, const unsigned *ctab, FxScratch sc) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ unsigned long long s_tmp64[FX_NT / 32];
-    __shared__ unsigned s_red[3][FX_NT / 32];
-    __shared__ long long s_tile;
-    __shared__ unsigned long long s_pre_out;
-
-    unsigned long long *stab = reinterpret_cast<unsigned long long *>(smem);
-    for (int k = threadIdx.x; k < 256 * FX_REP; k += FX_NT) stab[k] = tab[k >> 4];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const unsigned a_tab = sa(stab) + 8u * (lane & (FX_REP - 1));
+    __shared__ uint8_t s_explen[256];
+    __shared__ unsigned s_flag;
+    unsigned *stab = reinterpret_cast<unsigned *>(smem);
+    for (int k = threadIdx.x; k < 256 * 32; k += FX_NT) stab[k] = ctab[k >> 5];
+    for (int k = threadIdx.x; k < 256; k += FX_NT) s_explen[k] = (uint8_t)(ctab[k] & 0xffu);
+    const int tid = threadIdx.x, lane = tid & 31;
+    const unsigned a_tab = sa(stab) + 4u * lane;
     const bool ends_nl = job.n > 0 && job.in[job.n - 1] == '\n';
-
-    for (;;) {
-        if (tid == 0) s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
-        __syncthreads();
-        const long long t = s_tile;
-        if (t >= job.n_tiles) break;
+    unsigned long long my_nl = 0, my_esc = 0;
+    unsigned any_bad = 0;
+    for (long long t = blockIdx.x; t < job.n_tiles; t += gridDim.x) {
+        __syncthreads();  // s_flag / s_tmp64 reuse
+        if (tid == 0) s_flag = 0;
         const long long c0 = t * (long long)FX_TILE + (long long)tid * FX_B;
         const int cnt = (int)max(0ll, min((long long)FX_B, job.n - c0));
-        uint4 va = make_uint4(0, 0, 0, 0), vb = va;
-        if (cnt == FX_B && ALIGNED) {
-            const uint4 *src = reinterpret_cast<const uint4 *>(job.in + c0);
-            va = __ldcs(src);
-            vb = __ldcs(src + 1);
-        } else if (cnt > 0) {
-            unsigned w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int k = 0; k < cnt; ++k) w[k >> 2] |= (unsigned)job.in[c0 + k] << (8 * (k & 3));
-            va = make_uint4(w[0], w[1], w[2], w[3]);
-            vb = make_uint4(w[4], w[5], w[6], w[7]);
+        uint4 va, vb;
+        fx_load<ALIGNED>(job.in, c0, cnt, va, vb);
+        unsigned acc = 0;
+#pragma unroll
+        for (int k = 0; k < FX_B; ++k) {
+            const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
+            const unsigned e = lds32(a_tab + 128u * b);
+            acc += k < cnt ? e : 0u;
         }
-        // escape state at the chunk start: parity of the 0x20 run before it
+        unsigned sum = acc & 0xffu, bad = (acc >> 8) & 0xffu, marks = (acc >> 16) & 0xffu;
+        unsigned nl = acc >> 24, nesc = 0;
+        // escapes: the byte before the slice, or marks inside it -> exact walk
         const unsigned prev = __shfl_up_sync(0xffffffffu, vb.w >> 24, 1);
-        bool esc0 = false;
+        unsigned esc0 = 0;
         if (cnt > 0 && c0 > 0) {
             const unsigned pb = lane ? prev : job.in[c0 - 1];
             if (pb == 0x20) esc0 = fx_escaped(job.in, c0);
         }
-        // the virtual '\n' closing a final record without one
-        const bool eof_nl = cnt > 0 && c0 + cnt == job.n && !ends_nl;
-
-        // ---- pass 1: output bytes, records, escapes, errors ----
-        unsigned sum = 0, nl = 0, nesc = 0, bad = 0;
-        bool esc = esc0;
-#pragma unroll
-        for (int k = 0; k < FX_B; ++k) {
-            if (k < cnt) {
-                const unsigned b = fx_byte(va, vb, k);
-                const unsigned hi = lds32(a_tab + 8u * FX_REP * b + 4u);
-                const bool lit = esc;
-                const unsigned len = lit ? 1u : (hi >> 24) & 15u;
-                bad |= lit ? (b == '\n') : ((hi >> 28) & 1u);  // literal '\n' / unknown code
-                esc = !lit && ((hi >> 29) & 1u);
-                nl += !lit && ((hi >> 30) & 1u);
-                nesc += lit;
-                sum += len;
-            }
+        __syncthreads();
+        if (marks | esc0) {
+            unsigned esc_out;
+            fx_walk_esc(va, vb, cnt, esc0, s_explen, sum, nl, nesc, bad, esc_out);
+            if (cnt > 0 && c0 + cnt == job.n && esc_out) bad = 1;  // dangling escape at EOF
+            s_flag = 1;
         }
-        if (cnt > 0 && c0 + cnt == job.n && esc) bad = 1;  // dangling escape at EOF
-        if (eof_nl) {
+        if (cnt > 0 && c0 + cnt == job.n && !ends_nl) {  // virtual '\n' closing the last record
             sum += 1;
             nl += 1;
         }
-        if (bad) atomicOr(&job.ctl->overflow, 4ull);
-        // ---- block scan of output bytes; record and escape totals ----
-        unsigned long long tile_out;
-        const unsigned long long my_off = block_exscan_n<unsigned long long, FX_NT>(sum, s_tmp64, tile_out);
-        unsigned r_nl = nl, r_esc = nesc;
+        any_bad |= bad;
+        my_nl += nl;
+        my_esc += nesc;
+        unsigned long long tot;
+        const unsigned long long off = block_exscan_n<unsigned long long, FX_NT>(sum, s_tmp64, tot);
+        sc.off16[t * FX_NT + tid] = (uint16_t)off;
+        if (tid == 0) {
+            sc.tsum[t] = (unsigned)tot;
+            sc.tflag[t] = (uint8_t)(s_flag | (tot + 16 > (unsigned long long)FX_STAGE ? 2u : 0u));
+        }
+    }
+    // per-CTA totals
 #pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            r_nl += __shfl_xor_sync(0xffffffffu, r_nl, o);
-            r_esc += __shfl_xor_sync(0xffffffffu, r_esc, o);
+    for (int o = 16; o; o >>= 1) {
+        my_nl += __shfl_xor_sync(0xffffffffu, my_nl, o);
+        my_esc += __shfl_xor_sync(0xffffffffu, my_esc, o);
+    }
+    any_bad = __any_sync(0xffffffffu, any_bad != 0);
+    if (lane == 0) {
+        if (my_nl) {
+            atomicAdd(&job.ctl->lines, my_nl);
+            atomicAdd(&job.ctl->in_lines, my_nl);
         }
-        if (lane == 0) {
-            s_red[0][wid] = r_nl;
-            s_red[1][wid] = r_esc;
+        if (my_esc) atomicAdd(&job.ctl->escapes, my_esc);
+        if (any_bad) atomicOr(&job.ctl->overflow, 4ull);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// fx_scan: one CTA of 1024 threads, exclusive scan of the tile totals
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) fx_scan(Job job, FxScratch sc) {
+    __shared__ unsigned long long s_w[32];
+    __shared__ unsigned long long s_carry;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (long long base = 0; base < job.n_tiles; base += 1024) {
+        const long long t = base + tid;
+        const unsigned long long v = t < job.n_tiles ? sc.tsum[t] : 0ull;
+        unsigned long long x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
+        if (lane == 31) s_w[wid] = x;
         __syncthreads();
         if (wid == 0) {
-            unsigned a = lane < FX_NT / 32 ? s_red[0][lane] : 0u, e = lane < FX_NT / 32 ? s_red[1][lane] : 0u;
+            unsigned long long w = s_w[lane];
 #pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                a += __shfl_xor_sync(0xffffffffu, a, o);
-                e += __shfl_xor_sync(0xffffffffu, e, o);
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
             }
-            if (lane == 0) lookback_publish(job.ts, t, tile_out, a);
-            unsigned long long po, pl;
-            lookback_resolve(job.ts, t, tile_out, a, po, pl);
-            if (lane == 0) {
-                s_pre_out = po;
-                atomicAdd(&job.ctl->total_out, tile_out);
-                atomicAdd(&job.ctl->lines, (unsigned long long)a);
-                atomicAdd(&job.ctl->in_lines, (unsigned long long)a);
-                if (e) atomicAdd(&job.ctl->escapes, (unsigned long long)e);
-                if (po + tile_out > (unsigned long long)job.out_cap) atomicOr(&job.ctl->overflow, 1ull);
-            }
+            s_w[lane] = w;
         }
         __syncthreads();
-        const unsigned long long pre_out = s_pre_out;
-        if (pre_out + tile_out > (unsigned long long)job.out_cap) continue;
+        const unsigned long long carry = s_carry;
+        const unsigned long long ex = carry + (wid ? s_w[wid - 1] : 0ull) + x - v;
+        if (t < job.n_tiles) sc.toff[t] = ex;
+        __syncthreads();
+        if (tid == 0) s_carry = carry + s_w[31];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        job.ctl->total_out = s_carry;
+        if (s_carry > (unsigned long long)job.out_cap) atomicOr(&job.ctl->overflow, 1ull);
+    }
+}
 
-        // ---- pass 2: expand into aligned 8-byte words ----
-        if (sum) {
-            const unsigned long long o = pre_out + my_off;
-            uint8_t *w = job.out + (o & ~7ull);
-            const int head = (int)(o & 7);
-            unsigned long long lo = 0;
-            int nb = head;
-            bool first = true;
-            esc = esc0;
-#pragma unroll
-            for (int k = 0; k <= FX_B; ++k) {
-                unsigned long long x;
-                unsigned len;
-                if (k < FX_B) {
-                    if (k >= cnt) continue;
-                    const unsigned b = fx_byte(va, vb, k);
-                    const unsigned long long e = lds64(a_tab + 8u * FX_REP * b);
-                    const bool lit = esc;
-                    len = lit ? 1u : (unsigned)(e >> FX_LEN_SHIFT) & 15u;
-                    x = lit ? (unsigned long long)b : (e & FX_BYTES);
-                    esc = !lit && (e & FX_MARK);
-                } else {
-                    if (!eof_nl) continue;
-                    x = '\n';
-                    len = 1;
-                }
-                const int sh = 8 * nb;
-                lo |= x << sh;
-                const unsigned long long spill = (x >> 1) >> (63 - sh);
-                nb += (int)len;
-                if (nb >= 8) {
-                    if (first) {
-                        fx_put_bytes(w, lo, head, 8);
-                        first = false;
-                    } else {
-                        *reinterpret_cast<unsigned long long *>(w) = lo;
-                    }
-                    w += 8;
-                    lo = spill;
-                    nb -= 8;
-                }
+// ---------------------------------------------------------------------------
+// fx_emit: expansions -> staging -> aligned 16-byte stores
+// ---------------------------------------------------------------------------
+
+// append one expansion x (len bytes, <= 7) to the accumulator; whole words go
+// to the staging address `a` (first word of the slice: atomic OR, it is
+// shared with the previous slice)
+struct FxAcc {
+    unsigned long long lo;
+    int nb;        // pending bytes in lo
+    unsigned a;    // smem address of lo's word
+    bool first;
+    __device__ __forceinline__ void put(unsigned long long x, unsigned len) {
+        const int sh = 8 * nb;
+        lo |= x << sh;
+        const unsigned long long spill = (x >> 1) >> (63 - sh);
+        nb += (int)len;
+        if (nb >= 8) {
+            if (first) red_or64(a, lo);
+            else sts64(a, lo);
+            first = false;
+            a += 8;
+            lo = spill;
+            nb -= 8;
+        }
+    }
+    __device__ __forceinline__ void finish() {
+        if (nb > 0) red_or64(a, lo);
+    }
+};
+
+template <bool ALIGNED>
+__global__ void __launch_bounds__(FX_NT) fx_emit(Job job, const unsigned long long *etab, FxScratch sc) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    unsigned long long *stab = reinterpret_cast<unsigned long long *>(smem);
+    uint8_t *stage = smem + 256 * 16 * 8;
+    for (int k = threadIdx.x; k < 256 * 16; k += FX_NT) stab[k] = etab[k >> 4];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const unsigned a_tab = sa(stab) + 8u * (lane & 15);
+    const unsigned a_stage = sa(stage);
+    const bool ends_nl = job.n > 0 && job.in[job.n - 1] == '\n';
+
+    long long t = blockIdx.x;
+    uint4 na = make_uint4(0, 0, 0, 0), nb4 = na;
+    if (t < job.n_tiles) {
+        const long long c0 = t * (long long)FX_TILE + (long long)tid * FX_B;
+        fx_load<ALIGNED>(job.in, c0, (int)max(0ll, min((long long)FX_B, job.n - c0)), na, nb4);
+    }
+    for (; t < job.n_tiles; t += gridDim.x) {
+        const long long c0 = t * (long long)FX_TILE + (long long)tid * FX_B;
+        const int cnt = (int)max(0ll, min((long long)FX_B, job.n - c0));
+        const uint4 va = na, vb = nb4;
+        // prefetch the next tile's slice
+        const long long tn = t + gridDim.x;
+        if (tn < job.n_tiles) {
+            const long long cn = tn * (long long)FX_TILE + (long long)tid * FX_B;
+            fx_load<ALIGNED>(job.in, cn, (int)max(0ll, min((long long)FX_B, job.n - cn)), na, nb4);
+        }
+        const unsigned long long tbase = sc.toff[t];
+        const unsigned tsum = sc.tsum[t];
+        const unsigned flag = sc.tflag[t];
+        const unsigned my_off = sc.off16[t * FX_NT + tid];
+        const bool eof_nl = cnt > 0 && c0 + cnt == job.n && !ends_nl;
+        if (tsum == 0) continue;
+        const bool staged = !(flag & 2u);
+        const int shift = (int)(tbase & 15);  // stage[shift + j] <-> out[tbase + j]
+        if (staged) {
+            __syncthreads();  // previous tile's copy-out is done
+            const int words = (shift + (int)tsum + 15) >> 4;
+            for (int k = tid; k < words; k += FX_NT)
+                asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(a_stage + 16u * k), "r"(0u)
+                             : "memory");
+            __syncthreads();
+        }
+        if (cnt > 0) {
+            unsigned esc = 0;
+            if (flag & 1u) {
+                const unsigned prev = c0 > 0 ? job.in[c0 - 1] : 0u;
+                if (prev == 0x20) esc = fx_escaped(job.in, c0);
             }
-            if (nb > (first ? head : 0)) fx_put_bytes(w, lo, first ? head : 0, nb);
+            if (staged) {
+                const unsigned o = (unsigned)shift + my_off;
+                FxAcc acc{0ull, (int)(o & 7), a_stage + (o & ~7u), true};
+                if (!(flag & 1u)) {
+#pragma unroll
+                    for (int k = 0; k < FX_B; ++k) {
+                        if (k < cnt) {
+                            const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
+                            const unsigned long long e = lds64(a_tab + 128u * b);
+                            acc.put(e & FX_BYTES, (unsigned)(e >> 56));
+                        }
+                    }
+                } else {
+                    for (int k = 0; k < cnt; ++k) {
+                        const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
+                        const unsigned long long e = lds64(a_tab + 128u * b);
+                        if (esc) {
+                            acc.put(b, 1);
+                            esc = 0;
+                        } else if (b == 0x20) {
+                            esc = 1;
+                        } else {
+                            acc.put(e & FX_BYTES, (unsigned)(e >> 56));
+                        }
+                    }
+                }
+                if (eof_nl) acc.put('\n', 1);
+                acc.finish();
+            } else {
+                // tile output larger than the staging buffer: bytes straight to HBM
+                uint8_t *o = job.out + tbase + my_off;
+                for (int k = 0; k < cnt; ++k) {
+                    const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
+                    const unsigned long long e = lds64(a_tab + 128u * b);
+                    if (esc) {
+                        *o++ = (uint8_t)b;
+                        esc = 0;
+                    } else if (b == 0x20) {
+                        esc = 1;
+                    } else {
+                        const unsigned L = (unsigned)(e >> 56);
+                        for (unsigned j = 0; j < L; ++j) o[j] = (uint8_t)(e >> (8 * j));
+                        o += L;
+                    }
+                }
+                if (eof_nl) *o++ = '\n';
+            }
+        }
+        if (staged) {
+            __syncthreads();
+            // aligned 16-byte chunks [g0, g1) of the output; partial ends bytewise
+            const unsigned long long lo = tbase, hi = tbase + tsum;
+            const unsigned long long g0 = (lo + 15) & ~15ull, g1 = hi & ~15ull;
+            const uint4 *s4 = reinterpret_cast<const uint4 *>(stage);
+            if (g0 < g1) {
+                const long long n16 = (long long)((g1 - g0) >> 4);
+                const int s0 = (int)((g0 - (lo & ~15ull)) >> 4);
+                uint4 *d4 = reinterpret_cast<uint4 *>(job.out + g0);
+                for (long long k = tid; k < n16; k += FX_NT) __stcs(d4 + k, s4[s0 + k]);
+                if (tid < 32) {
+                    const unsigned long long hb = min(g0, hi);
+                    for (unsigned long long g = lo + tid; g < hb; g += 32) job.out[g] = stage[shift + (g - lo)];
+                } else if (tid < 64) {
+                    for (unsigned long long g = max(g1, g0) + (tid - 32); g < hi; g += 32)
+                        job.out[g] = stage[shift + (g - lo)];
+                }
+            } else if (tid < 32) {
+                for (unsigned long long g = lo + tid; g < hi; g += 32) job.out[g] = stage[shift + (g - lo)];
+            }
         }
     }
 }
