@@ -22,7 +22,7 @@
 // Tables (built on the host from the reference decode tables,
 // dictionary.py:112-129), replicated per bank so lookups never conflict:
 //   count: u32 [code][32 lanes] = len | invalid << 8 | mark << 16 | nl << 24
-//   emit : u64 [code][16 lanes] = expansion bytes 0-6 | len << 56
+//   emit : u64 [code][16 lanes] = expansion bytes 0-6 | (8 * len) << 56
 // Serves dictionaries whose longest expansion is <= 7 bytes (default: 6).
 #pragma once
 #include "zs_device.cuh"
@@ -33,8 +33,8 @@ constexpr int FX_NT = 256;               // threads per CTA
 constexpr int FX_B = 32;                 // compressed bytes per thread per tile
 constexpr int FX_TILE = FX_NT * FX_B;    // 8 KB of compressed input per tile
 constexpr int FX_STAGE = 24576;          // emit staging bytes (tile output + 16 alignment)
-constexpr int FX_CNT_SMEM = 256 * 32 * 4;
-constexpr int FX_EMIT_SMEM = 256 * 16 * 8 + FX_STAGE;
+constexpr int FX_CNT_SMEM = 0;   // static shared only
+constexpr int FX_EMIT_SMEM = FX_STAGE;  // dynamic: the staging tile
 constexpr unsigned long long FX_BYTES = (1ull << 56) - 1;
 
 // per-slot scratch layout (device): tile totals, tile offsets, tile flags,
@@ -68,10 +68,10 @@ inline unsigned fx_count_entry(int b, const uint8_t *exp_len) {
 }
 inline unsigned long long fx_emit_entry(int b, const uint8_t *exp_len, const uint16_t *exp_off,
                                         const uint8_t *exp_flat) {
-    if (b == '\n') return (unsigned long long)'\n' | (1ull << 56);
+    if (b == '\n') return (unsigned long long)'\n' | (8ull << 56);
     const int L = exp_len[b];
     if (b == 0x20 || L == 0) return 0;
-    unsigned long long e = (unsigned long long)L << 56;
+    unsigned long long e = (unsigned long long)(8 * L) << 56;
     for (int k = 0; k < L && k < 7; ++k) e |= (unsigned long long)exp_flat[exp_off[b] + k] << (8 * k);
     return e;
 }
@@ -153,17 +153,31 @@ __device__ __forceinline__ void fx_walk_esc(const uint4 &va, const uint4 &vb, in
 // ---------------------------------------------------------------------------
 // fx_count: per-thread output bytes -> u16 tile offsets; tile totals/flags
 // ---------------------------------------------------------------------------
+
+// sum of the count-table entries of the slice's bytes (FULL: all 32 valid)
+template <bool FULL>
+__device__ __forceinline__ unsigned fx_count_slice(const unsigned (*tab)[32], int lane, const uint4 &va,
+                                                   const uint4 &vb, int cnt) {
+    unsigned acc = 0;
+#pragma unroll
+    for (int k = 0; k < FX_B; ++k) {
+        if (FULL || k < cnt) {
+            const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
+            acc += tab[b][lane];
+        }
+    }
+    return acc;
+}
+
 template <bool ALIGNED>
 __global__ void __launch_bounds__(FX_NT) fx_count(Job job, const unsigned *ctab, FxScratch sc) {
-    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ unsigned s_tab[256][32];  // replicated per lane: conflict-free
     __shared__ unsigned long long s_tmp64[FX_NT / 32];
     __shared__ uint8_t s_explen[256];
     __shared__ unsigned s_flag;
-    unsigned *stab = reinterpret_cast<unsigned *>(smem);
-    for (int k = threadIdx.x; k < 256 * 32; k += FX_NT) stab[k] = ctab[k >> 5];
+    for (int k = threadIdx.x; k < 256 * 32; k += FX_NT) s_tab[k >> 5][k & 31] = ctab[k >> 5];
     for (int k = threadIdx.x; k < 256; k += FX_NT) s_explen[k] = (uint8_t)(ctab[k] & 0xffu);
     const int tid = threadIdx.x, lane = tid & 31;
-    const unsigned a_tab = sa(stab) + 4u * lane;
     const bool ends_nl = job.n > 0 && job.in[job.n - 1] == '\n';
     unsigned long long my_nl = 0, my_esc = 0;
     unsigned any_bad = 0;
@@ -174,13 +188,8 @@ __global__ void __launch_bounds__(FX_NT) fx_count(Job job, const unsigned *ctab,
         const int cnt = (int)max(0ll, min((long long)FX_B, job.n - c0));
         uint4 va, vb;
         fx_load<ALIGNED>(job.in, c0, cnt, va, vb);
-        unsigned acc = 0;
-#pragma unroll
-        for (int k = 0; k < FX_B; ++k) {
-            const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
-            const unsigned e = lds32(a_tab + 128u * b);
-            acc += k < cnt ? e : 0u;
-        }
+        const unsigned acc = cnt == FX_B ? fx_count_slice<true>(s_tab, lane, va, vb, cnt)
+                                         : fx_count_slice<false>(s_tab, lane, va, vb, cnt);
         unsigned sum = acc & 0xffu, bad = (acc >> 8) & 0xffu, marks = (acc >> 16) & 0xffu;
         unsigned nl = acc >> 24, nesc = 0;
         // escapes: the byte before the slice, or marks inside it -> exact walk
@@ -276,41 +285,67 @@ __global__ void __launch_bounds__(1024) fx_scan(Job job, FxScratch sc) {
 // fx_emit: expansions -> staging -> aligned 16-byte stores
 // ---------------------------------------------------------------------------
 
-// append one expansion x (len bytes, <= 7) to the accumulator; whole words go
-// to the staging address `a` (first word of the slice: atomic OR, it is
-// shared with the previous slice)
+// Append one expansion x (len8 = 8 * its length, <= 56) to the accumulator:
+// lo holds sh/8 pending bytes destined for the smem word at `a`; a whole word
+// leaves with one 8-byte store.  FIRST: the slice's first word is shared
+// with the previous slice (atomic OR into the zeroed staging).
 struct FxAcc {
     unsigned long long lo;
-    int nb;        // pending bytes in lo
-    unsigned a;    // smem address of lo's word
+    unsigned sh;
+    unsigned a;
     bool first;
-    __device__ __forceinline__ void put(unsigned long long x, unsigned len) {
-        const int sh = 8 * nb;
+    template <bool FIRST>
+    __device__ __forceinline__ void put(unsigned long long x, unsigned len8) {
+        const unsigned long long spill = x >> ((64u - sh) & 63u);  // used only on a flush (sh > 0)
         lo |= x << sh;
-        const unsigned long long spill = (x >> 1) >> (63 - sh);
-        nb += (int)len;
-        if (nb >= 8) {
-            if (first) red_or64(a, lo);
-            else sts64(a, lo);
-            first = false;
-            a += 8;
-            lo = spill;
-            nb -= 8;
+        sh += len8;
+        const bool f = sh >= 64u;
+        if (FIRST) {
+            if (f) {
+                if (first) red_or64(a, lo);
+                else sts64(a, lo);
+            }
+            first = first && !f;
+        } else {
+            if (f) sts64(a, lo);
         }
+        a += f ? 8u : 0u;
+        lo = f ? spill : lo;
+        sh -= f ? 64u : 0u;
     }
     __device__ __forceinline__ void finish() {
-        if (nb > 0) red_or64(a, lo);
+        if (sh) red_or64(a, lo);
     }
 };
 
+__device__ __forceinline__ unsigned long long fx_etab(const unsigned long long (*tab)[16], int lane, unsigned b) {
+    return tab[b][lane & 15];
+}
+
+// clean slice (no escapes), FULL = all 32 bytes valid.  Every code emits >= 1
+// byte, so the first (shared) word is complete within the first 8 codes.
+template <bool FULL>
+__device__ __forceinline__ void fx_emit_clean(FxAcc &acc, const unsigned long long (*tab)[16], int lane,
+                                              const uint4 &va, const uint4 &vb, int cnt) {
+#pragma unroll
+    for (int k = 0; k < FX_B; ++k) {
+        if (FULL || k < cnt) {
+            const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
+            const unsigned long long e = fx_etab(tab, lane, b);
+            const unsigned long long x = e & FX_BYTES;
+            const unsigned len8 = (unsigned)(e >> 56);
+            if (k < 8 || !FULL) acc.put<true>(x, len8);
+            else acc.put<false>(x, len8);
+        }
+    }
+}
+
 template <bool ALIGNED>
 __global__ void __launch_bounds__(FX_NT) fx_emit(Job job, const unsigned long long *etab, FxScratch sc) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    unsigned long long *stab = reinterpret_cast<unsigned long long *>(smem);
-    uint8_t *stage = smem + 256 * 16 * 8;
-    for (int k = threadIdx.x; k < 256 * 16; k += FX_NT) stab[k] = etab[k >> 4];
+    __shared__ unsigned long long s_tab[256][16];  // replicated per half-warp lane
+    extern __shared__ __align__(16) uint8_t stage[];  // FX_STAGE bytes
+    for (int k = threadIdx.x; k < 256 * 16; k += FX_NT) s_tab[k >> 4][k & 15] = etab[k >> 4];
     const int tid = threadIdx.x, lane = tid & 31;
-    const unsigned a_tab = sa(stab) + 8u * (lane & 15);
     const unsigned a_stage = sa(stage);
     const bool ends_nl = job.n > 0 && job.in[job.n - 1] == '\n';
 
@@ -354,45 +389,39 @@ __global__ void __launch_bounds__(FX_NT) fx_emit(Job job, const unsigned long lo
             }
             if (staged) {
                 const unsigned o = (unsigned)shift + my_off;
-                FxAcc acc{0ull, (int)(o & 7), a_stage + (o & ~7u), true};
+                FxAcc acc{0ull, 8u * (o & 7u), a_stage + (o & ~7u), true};
                 if (!(flag & 1u)) {
-#pragma unroll
-                    for (int k = 0; k < FX_B; ++k) {
-                        if (k < cnt) {
-                            const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
-                            const unsigned long long e = lds64(a_tab + 128u * b);
-                            acc.put(e & FX_BYTES, (unsigned)(e >> 56));
-                        }
-                    }
+                    if (cnt == FX_B) fx_emit_clean<true>(acc, s_tab, lane, va, vb, cnt);
+                    else fx_emit_clean<false>(acc, s_tab, lane, va, vb, cnt);
                 } else {
                     for (int k = 0; k < cnt; ++k) {
                         const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
-                        const unsigned long long e = lds64(a_tab + 128u * b);
+                        const unsigned long long e = fx_etab(s_tab, lane, b);
                         if (esc) {
-                            acc.put(b, 1);
+                            acc.put<true>(b, 8u);
                             esc = 0;
                         } else if (b == 0x20) {
                             esc = 1;
                         } else {
-                            acc.put(e & FX_BYTES, (unsigned)(e >> 56));
+                            acc.put<true>(e & FX_BYTES, (unsigned)(e >> 56));
                         }
                     }
                 }
-                if (eof_nl) acc.put('\n', 1);
+                if (eof_nl) acc.put<true>('\n', 8u);
                 acc.finish();
             } else {
                 // tile output larger than the staging buffer: bytes straight to HBM
                 uint8_t *o = job.out + tbase + my_off;
                 for (int k = 0; k < cnt; ++k) {
                     const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
-                    const unsigned long long e = lds64(a_tab + 128u * b);
+                    const unsigned long long e = fx_etab(s_tab, lane, b);
                     if (esc) {
                         *o++ = (uint8_t)b;
                         esc = 0;
                     } else if (b == 0x20) {
                         esc = 1;
                     } else {
-                        const unsigned L = (unsigned)(e >> 56);
+                        const unsigned L = (unsigned)(e >> 56) >> 3;
                         for (unsigned j = 0; j < L; ++j) o[j] = (uint8_t)(e >> (8 * j));
                         o += L;
                     }
@@ -407,15 +436,14 @@ __global__ void __launch_bounds__(FX_NT) fx_emit(Job job, const unsigned long lo
             const unsigned long long g0 = (lo + 15) & ~15ull, g1 = hi & ~15ull;
             const uint4 *s4 = reinterpret_cast<const uint4 *>(stage);
             if (g0 < g1) {
-                const long long n16 = (long long)((g1 - g0) >> 4);
+                const int n16 = (int)((g1 - g0) >> 4);
                 const int s0 = (int)((g0 - (lo & ~15ull)) >> 4);
                 uint4 *d4 = reinterpret_cast<uint4 *>(job.out + g0);
-                for (long long k = tid; k < n16; k += FX_NT) __stcs(d4 + k, s4[s0 + k]);
+                for (int k = tid; k < n16; k += FX_NT) __stcs(d4 + k, s4[s0 + k]);
                 if (tid < 32) {
-                    const unsigned long long hb = min(g0, hi);
-                    for (unsigned long long g = lo + tid; g < hb; g += 32) job.out[g] = stage[shift + (g - lo)];
+                    for (unsigned long long g = lo + tid; g < g0; g += 32) job.out[g] = stage[shift + (g - lo)];
                 } else if (tid < 64) {
-                    for (unsigned long long g = max(g1, g0) + (tid - 32); g < hi; g += 32)
+                    for (unsigned long long g = g1 + (tid - 32); g < hi; g += 32)
                         job.out[g] = stage[shift + (g - lo)];
                 }
             } else if (tid < 32) {
