@@ -104,7 +104,9 @@ int zs_build_tables_host(const int32_t *children, const int16_t *term_code, int3
  * t2 uint32[1024*16].  Returns 1 if built, 0 if the dictionary does not fit. */
 int zs_build_t2_host(const int32_t *children, const int16_t *term_code, int32_t n_nodes,
                      uint16_t *dfa2, uint32_t *t2, int32_t *n_windows, int32_t *n_masks);
-/* debug/ablation: 0 forces the key-window DP instead of the transducer */
+/* debug/ablation kernel selection (default 3): bit 0 transducer parse, bit 1
+ * in-place decisions (lane-chunk kernel), bit 2 warp-cooperative decompress
+ * instead of the streaming one, bit 3 queue-based in-place compress kernel */
 int zs_set_transducer(zs_ctx *ctx, int on);
 
 /* ---- fine-grained parity shim (reference kernel layouts, host memory) ---- */

@@ -19,6 +19,7 @@
 #include "../../include/zs.h"
 #include "zs_kernels.cuh"
 #include "zs_fx.cuh"
+#include "zs_cx.cuh"
 
 using namespace zs;
 
@@ -58,6 +59,11 @@ struct HostTables {
     int n_windows = 0, n_masks = 0;
     std::vector<uint16_t> dfa2;
     std::vector<uint32_t> t2;
+    // lane-chunk compress kernel tables (zs_cx.cuh): '\n' column + transducer slot
+    bool cx_ok = false;
+    std::vector<uint16_t> cx_dfa;
+    std::vector<uint32_t> cx_t2;
+    std::vector<uint8_t> cx_codes;
     uint8_t exp_len[256];
     uint16_t exp_off[257];
     std::vector<uint8_t> exp_flat;
@@ -77,7 +83,8 @@ struct zs_ctx {
     HostTables ht;
     Tables tb{};
     int fast_w = 0;
-    DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2, d_fxc, d_fxe;
+    DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2, d_fxc, d_fxe, d_cxdfa, d_cxt2, d_cxcodes;
+    int no_cx = 0;  // debug: force the queue-based compress kernel
     bool fx_ok = false;  // streaming decode kernel serves this dictionary (max expansion <= 7)
     int fx_blocks[2] = {0, 0};  // resident fx_count / fx_emit CTAs per SM
     int no_t2 = 0;  // debug: force the key-window DP
@@ -282,6 +289,40 @@ bool build_t2(HostTables &ht, int W) {
     return true;
 }
 
+// Tables of the lane-chunk kernel: the DFA gets a '\n' column (column
+// c = min(b - 10, 118): 0 = '\n', 22..117 = 0x20..0x7f, the rest = other)
+// whose entry returns to the root with the reserved mask slot CX_NLMASK; the
+// transducer's CX_NLMASK entry of every window resets to the line-end window
+// with code slot 9 (the record separator, cost +1).
+bool build_cx(HostTables &ht, int max_len) {
+    if (!ht.t2_ok || ht.n_masks > CX_NLMASK || max_len > 8) return false;
+    const int ns = ht.n_states, nw = ht.n_windows;
+    if (cx_smem_bytes(ns, nw) > 227 * 1024) return false;
+    ht.cx_dfa.assign((size_t)cx_align16(ns * CX_NCOL * 2) / 2, 0);
+    for (int st = 0; st < ns; ++st)
+        for (int c = 0; c < CX_NCOL; ++c) {
+            uint16_t e;
+            if (c == 0) {
+                e = (uint16_t)(0 | (CX_NLMASK << 8));
+            } else {
+                const int b = c + 10;
+                const int old = (c < 118 && b >= 0x20 && b <= 0x7f) ? b - 0x20 : 96;
+                e = ht.dfa2[(size_t)st * NCOL + old];
+            }
+            ht.cx_dfa[(size_t)st * CX_NCOL + c] = e;
+        }
+    ht.cx_t2 = ht.t2;
+    for (int w = 0; w < nw; ++w)
+        ht.cx_t2[(size_t)w * T2_MASKS + CX_NLMASK] = 0u | (9u << 12) | ((1u + 16u) << 16);
+    ht.cx_codes.assign((size_t)cx_align16(ns * CX_CODES), 0);
+    for (int st = 0; st < ns; ++st) {
+        for (int L = 0; L < FAST_W; ++L) ht.cx_codes[(size_t)st * CX_CODES + L] = ht.codes[(size_t)st * FAST_W + L];
+        ht.cx_codes[(size_t)st * CX_CODES + 8] = '\n';
+    }
+    ht.cx_ok = true;
+    return true;
+}
+
 template <typename K>
 cudaError_t set_smem(K kernel, int bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -315,9 +356,10 @@ BatchKernel batch_kernel(int w) {
 // one whole-buffer launch (device pointers) on `slot`'s buffers and stream
 int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, long long n,
                   uint8_t *d_out, long long out_cap, int flags, bool timed, bool general = false) {
-    const bool ip = compress && ctx->fast_w && ctx->ht.t2_ok && !ctx->no_t2 && !ctx->no_ip;
+    const bool cx = compress && ctx->ht.cx_ok && !general && !ctx->no_cx && !ctx->no_t2 && !ctx->no_ip;
+    const bool ip = compress && !cx && ctx->fast_w && ctx->ht.t2_ok && !ctx->no_t2 && !ctx->no_ip;
     const bool fx = !compress && ctx->fx_ok && !general && ctx->dec_variant == 1;
-    const long long tile = ip ? CTILE : fx ? FX_TILE : TILE;
+    const long long tile = cx ? CX_TILE : ip ? CTILE : fx ? FX_TILE : TILE;
     const long long nt = (n + tile - 1) / tile;
     cudaStream_t st = ctx->stream[slot];
     if (ctx->ctl[slot].reserve(sizeof(Ctl)) || ctx->ts[slot].reserve(sizeof(TileState) * (nt + 1)) ||
@@ -346,7 +388,14 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
     if (nt > 0) {
         const int grid = (int)std::min<long long>(nt, ctx->n_sm);
         if (timed) CK(cudaEventRecord(ctx->ev0, st));
-        if (ip) {
+        if (cx) {
+            const int smem = cx_smem_bytes(ctx->ht.n_states, ctx->ht.n_windows);
+            CK(set_smem(compress_cx, smem));
+            compress_cx<<<grid, CX_NT, smem, st>>>(job, ctx->tb, ctx->d_cxdfa.as<uint16_t>(),
+                                                   ctx->d_cxt2.as<uint32_t>(), ctx->d_cxcodes.as<uint8_t>(),
+                                                   ctx->ht.n_states, ctx->ht.n_windows);
+            ctx->last_kernel = "compress_cx";
+        } else if (ip) {
             const int smem = ip_smem_bytes(ctx->tb.n_states, ctx->ht.n_windows);
             CK(set_smem(compress_tiles_ip, smem));
             compress_tiles_ip<<<grid, NT, smem, st>>>(job, ctx->tb);
@@ -410,7 +459,7 @@ int collect(zs_ctx *ctx, int slot, long long n, const uint8_t *h_last_byte_src, 
         return 1;
     }
     (void)h_last_byte_src;
-    if (c.overflow & 4ull) return 3;  // streaming decode met a bad record: re-run record-aware
+    if (c.overflow & 12ull) return 3;  // fast kernel met a case it hands over: re-run the general one
     zs_result r{};
     r.lines = (long long)c.lines;
     r.in_bytes = n;
@@ -656,7 +705,7 @@ int zs_ctx_destroy(zs_ctx *ctx) {
     if (!ctx) return ZS_OK;
     cudaSetDevice(ctx->dev);
     for (DevBuf *b : {&ctx->d_dfa2, &ctx->d_t2, &ctx->d_dfa, &ctx->d_codes, &ctx->d_children, &ctx->d_term, &ctx->d_explen,
-                      &ctx->d_expoff, &ctx->d_expflat, &ctx->d_fxc, &ctx->d_fxe, &ctx->fxs[0], &ctx->fxs[1], &ctx->ctl[0], &ctx->ctl[1], &ctx->ts[0],
+                      &ctx->d_expoff, &ctx->d_expflat, &ctx->d_fxc, &ctx->d_fxe, &ctx->d_cxdfa, &ctx->d_cxt2, &ctx->d_cxcodes, &ctx->fxs[0], &ctx->fxs[1], &ctx->ctl[0], &ctx->ctl[1], &ctx->ts[0],
                       &ctx->ts[1], &ctx->terr[0], &ctx->terr[1], &ctx->in[0], &ctx->in[1],
                       &ctx->out[0], &ctx->out[1], &ctx->arena[0], &ctx->arena[1], &ctx->s_flat, &ctx->s_starts,
                       &ctx->s_out, &ctx->s_lens, &ctx->s_dec, &ctx->s_stat, &ctx->s_errpos,
@@ -708,7 +757,7 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
     ht.max_len = 0;
     for (auto &p : pats) ht.max_len = std::max<int>(ht.max_len, (int)p.first.size());
     ht.fast = build_dfa(pats, ht.max_len, ht);
-    if (ht.fast) build_t2(ht, std::max(1, ht.max_len));
+    if (ht.fast && build_t2(ht, std::max(1, ht.max_len))) build_cx(ht, ht.max_len);
     // decode tables (dictionary.py:112-129): valid codes have exp_len > 0
     if (exp_off[256] > 65535) {
         ctx->err = "expansion table too large";
@@ -742,6 +791,11 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
     if (ht.t2_ok) {
         CK(up(ctx->d_dfa2, ht.dfa2.data(), ht.dfa2.size() * 2));
         CK(up(ctx->d_t2, ht.t2.data(), ht.t2.size() * 4));
+    }
+    if (ht.cx_ok) {
+        CK(up(ctx->d_cxdfa, ht.cx_dfa.data(), ht.cx_dfa.size() * 2));
+        CK(up(ctx->d_cxt2, ht.cx_t2.data(), ht.cx_t2.size() * 4));
+        CK(up(ctx->d_cxcodes, ht.cx_codes.data(), ht.cx_codes.size()));
     }
     {
         unsigned fxc[256];
@@ -805,6 +859,7 @@ int zs_set_transducer(zs_ctx *ctx, int on) {
     ctx->dec_variant = (on & 4) ? 0 : 1;  // bit 2: warp-cooperative decompress
     ctx->no_t2 = (on & 1) ? 0 : 1;  // bit 0: transducer parse
     ctx->no_ip = (on & 2) ? 0 : 1;  // bit 1: in-place kernel (needs the transducer)
+    ctx->no_cx = (on & 8) ? 1 : 0;  // bit 3: queue-based in-place kernel instead of the lane-chunk one
     return ZS_OK;
 }
 

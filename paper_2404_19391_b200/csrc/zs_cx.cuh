@@ -1,0 +1,653 @@
+// zs_cx.cuh -- lane-chunk compress kernel (the encode hot path).
+//
+// One persistent 512-thread CTA per SM takes 51,200-byte tiles in ticket
+// order.  A tile owns the lines whose terminating '\n' lies inside it (their
+// first bytes may sit in the 2 KB staged before the tile).  Every lane owns
+// a contiguous run of whole lines, ~100 bytes, cut at the newline nearest to
+// its chunk boundary, and walks it in straight loops that all lanes of a
+// warp execute in lock step (no per-line queues, sorting or barriers):
+//
+//   P1  newline bitmap of the staged window (block-cooperative SWAR), lane
+//       ranges from the nearest-newline cuts (two block scans)
+//   P2  tokenizer (smiles.py:83-137 as an 8-state table transducer): CR and
+//       tokenize errors per line, ring-token starts OR'ed into the bitmap
+//   P3  ring pairing + colouring (smiles.py:140-213) walking the bitmap's
+//       events: open rings in 4 register slots, colours 0-9 from per-colour
+//       last-close positions; '%nn' lines are compacted in place with the
+//       freed bytes left as a gap of escape-only filler before the '\n'
+//   --  rare lines (drops, strict errors, lines the fast path cannot renumber,
+//       lines longer than the staged window) are rewritten to escape-only
+//       filler and handled by one thread each (general routine, HBM arena)
+//   P4  min-cost parse right to left across the lane's lines
+//       (numba_impl.py:32-56): per byte one AC-DFA lookup and one lookup in
+//       the cost-window transducer; '\n' is a DFA column whose transducer
+//       entry resets the window and emits the record separator, so the walk
+//       never branches on line ends.  Decisions overwrite the bytes in place.
+//   P5  lane output bytes -> block scan -> decoupled look-back publish
+//   P6  forward walk of the decisions (numba_impl.py:57-69) into an smem
+//       staging buffer, then aligned 16-byte stores at the resolved offset.
+//
+// Escapes keep their literal in place with a bit in `ebits` (which first
+// carries P2's per-line error flags to P3); `rbits` marks newlines and ring
+// tokens for P3; `fbits` marks filler and arena-marker positions for P6.
+#pragma once
+#include "zs_kernels.cuh"
+
+namespace zs {
+
+constexpr int CX_NT = 512;
+constexpr int CX_NW = CX_NT / 32;
+constexpr int CX_CC = 100;                        // 25 words: odd word stride across lanes
+constexpr int CX_TILE = CX_NT * CX_CC;            // 51200
+constexpr int CX_HEAD = 2048;                     // staged before the tile
+constexpr int CX_WIN = CX_HEAD + CX_TILE;         // 53248 (multiple of 32)
+constexpr int CX_WORDS = CX_WIN / 32 + 2;         // bitmap words
+constexpr int CX_NCOL = 119;                      // dcol: umin(b - 10, 118); 0 = '\n'
+constexpr int CX_NLMASK = 15;                     // transducer mask slot of '\n'
+constexpr int CX_CODES = 16;                      // codes per state (slot 8 = '\n')
+constexpr int CX_OUTCAP = 26624;                  // staging (ratio <= ~0.5)
+constexpr int CX_RARE = 128;                      // rare lines per tile
+
+// rare-line kinds
+enum : int { RK_DROP = 1, RK_ARENA = 2, RK_STRICT = 3 };
+
+struct CxRare {
+    int ls, le;        // window positions: first byte, terminating '\n'
+    int kind;          // RK_*
+    int lane;
+    int local;         // line index within the lane
+    int err;           // E_* (strict errors)
+    unsigned aoff;     // arena offset / 16 (RK_ARENA)
+    int glob;          // the line starts before the window (only its '\n' at le is staged)
+    long long gs;      // global offset of the line's first byte (RK_ARENA)
+};
+
+__host__ __device__ inline int cx_align16(int x) { return (x + 15) & ~15; }
+
+__host__ __device__ inline int cx_smem_bytes(int ns, int nw) {
+    return cx_align16(ns * CX_NCOL * 2) + nw * T2_MASKS * 4 + cx_align16(ns * CX_CODES) + 256 + 8 * 256 +
+           cx_align16(CX_WIN + 32) + 3 * CX_WORDS * 4 + CX_OUTCAP + CX_RARE * (int)sizeof(CxRare) +
+           3 * CX_NT * 4;
+}
+
+struct CxSmem {
+    uint16_t *dfa;
+    uint32_t *t2;
+    uint8_t *codes;
+    uint8_t *explen;
+    uint8_t *lut;
+    uint8_t *win;
+    unsigned *rbits, *ebits, *fbits;
+    uint8_t *out;
+    CxRare *rare;
+    int *lane_a, *lane_b, *lane_c;
+};
+
+__device__ inline CxSmem cx_carve(uint8_t *p, int ns, int nw) {
+    CxSmem S;
+    S.dfa = reinterpret_cast<uint16_t *>(p); p += cx_align16(ns * CX_NCOL * 2);
+    S.t2 = reinterpret_cast<uint32_t *>(p); p += nw * T2_MASKS * 4;
+    S.codes = p; p += cx_align16(ns * CX_CODES);
+    S.explen = p; p += 256;
+    S.lut = p; p += 8 * 256;
+    S.win = p; p += cx_align16(CX_WIN + 32);
+    S.rbits = reinterpret_cast<unsigned *>(p); p += CX_WORDS * 4;
+    S.ebits = reinterpret_cast<unsigned *>(p); p += CX_WORDS * 4;
+    S.fbits = reinterpret_cast<unsigned *>(p); p += CX_WORDS * 4;
+    S.out = p; p += CX_OUTCAP;
+    S.rare = reinterpret_cast<CxRare *>(p); p += CX_RARE * sizeof(CxRare);
+    S.lane_a = reinterpret_cast<int *>(p); p += CX_NT * 4;
+    S.lane_b = reinterpret_cast<int *>(p); p += CX_NT * 4;
+    S.lane_c = reinterpret_cast<int *>(p);
+    return S;
+}
+
+__device__ __forceinline__ unsigned cx_bit(const unsigned *bm, int p) { return (bm[p >> 5] >> (p & 31)) & 1u; }
+__device__ __forceinline__ void cx_set(unsigned *bm, int p) { atomicOr(&bm[p >> 5], 1u << (p & 31)); }
+__device__ __forceinline__ void cx_clr(unsigned *bm, int p) { atomicAnd(&bm[p >> 5], ~(1u << (p & 31))); }
+
+// first set bit at position >= p (bm bits beyond the window are never set;
+// callers bound the search by a position known to be set)
+__device__ __forceinline__ int cx_next(const unsigned *bm, int p) {
+    int w = p >> 5;
+    unsigned m = bm[w] & (0xffffffffu << (p & 31));
+    while (!m) m = bm[++w];
+    return (w << 5) + __ffs(m) - 1;
+}
+
+// block-wide inclusive max / min scans (CX_NT threads); tmp: CX_NW ints
+template <bool MAX>
+__device__ __forceinline__ int cx_block_scan_mm(int v, int *tmp, bool exclusive, int ident) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = MAX ? max(x, y) : min(x, y);
+    }
+    if (lane == 31) tmp[wid] = x;
+    __syncthreads();
+    int pre = ident;
+    for (int k = 0; k < wid; ++k) pre = MAX ? max(pre, tmp[k]) : min(pre, tmp[k]);
+    int ex = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) ex = ident;
+    ex = MAX ? max(pre, ex) : min(pre, ex);
+    const int inc = MAX ? max(pre, x) : min(pre, x);
+    __syncthreads();
+    return exclusive ? ex : inc;
+}
+
+// suffix min scan (from the right) via a reversed index
+__device__ __forceinline__ int cx_block_suffix_min(int v, int *tmp) {
+    // lane order reversed: thread t holds v of t; compute min over t' >= t
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_down_sync(0xffffffffu, x, o);
+        if (lane + o < 32) x = min(x, y);
+    }
+    if (lane == 0) tmp[wid] = x;
+    __syncthreads();
+    int post = 0x7fffffff;
+    for (int k = wid + 1; k < CX_NW; ++k) post = min(post, tmp[k]);
+    const int r = min(post, x);
+    __syncthreads();
+    return r;
+}
+
+// emit one arena line (compress_line_global output) at o[w...]; returns escapes
+__device__ __forceinline__ unsigned cx_emit_arena(const Job &job, const uint8_t *explen, unsigned aoff,
+                                                  uint8_t *o, unsigned long long &w, long long raw_gs) {
+    unsigned esc = 0;
+    const uint8_t *blk = job.arena + ((long long)aoff << 4);
+    const ArenaHdr *h = reinterpret_cast<const ArenaHdr *>(blk);
+    const uint8_t *bytes = h->bytes_off < 0 ? job.in + raw_gs : job.arena + h->bytes_off;
+    const uint8_t *dec = job.arena + h->dec_off;
+    for (long long i = 0; i < h->n_pre;) {
+        const uint8_t c = dec[i];
+        if (c == D_ESC) {
+            o[w++] = 0x20;
+            o[w++] = bytes[i];
+            ++esc;
+            ++i;
+        } else {
+            o[w++] = c;
+            i += explen[c];
+        }
+    }
+    o[w++] = '\n';
+    return esc;
+}
+
+// P6 walk of one lane range [p0, p1] into o at w.  SPECIAL: the tile has
+// escapes, filler or arena lines (bit checks); else the plain code walk.
+template <bool SPECIAL>
+__device__ __forceinline__ unsigned cx_emit_range(const Job &job, const CxSmem &S, long long ws, int p0, int p1,
+                                                  uint8_t *o, unsigned long long w, int n_rare) {
+    unsigned esc = 0;
+    const uint8_t *win = S.win;
+    for (int p = p0; p <= p1;) {
+        const unsigned c = win[p];
+        if (SPECIAL && cx_bit(S.ebits, p)) {
+            if (cx_bit(S.fbits, p)) {
+                if (c == 0x02) {  // arena line marker
+                    for (int r = 0; r < n_rare; ++r)
+                        if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p)
+                            esc += cx_emit_arena(job, S.explen, S.rare[r].aoff, o, w, S.rare[r].gs);
+                }
+            } else {
+                o[w++] = 0x20;
+                o[w++] = (uint8_t)c;
+                ++esc;
+            }
+            ++p;
+        } else {
+            o[w++] = (uint8_t)c;
+            p += S.explen[c];
+        }
+    }
+    return esc;
+}
+
+// record a rare line (returns false when the tile's list is full)
+__device__ __forceinline__ void cx_rare(const CxSmem &S, int *n, int ls, int le, int kind, int lane, int local,
+                                        int err, int glob) {
+    const int r = atomicAdd(n, 1);
+    if (r < CX_RARE) {
+        CxRare &R = S.rare[r];
+        R.ls = ls;
+        R.le = le;
+        R.kind = kind;
+        R.lane = lane;
+        R.local = local;
+        R.err = err;
+        R.aoff = 0;
+        R.glob = glob;
+        R.gs = 0;
+    }
+}
+
+__global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, const uint16_t *cx_dfa,
+                                                        const uint32_t *cx_t2, const uint8_t *cx_codes,
+                                                        int cx_ns, int cx_nw) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ int s_tmp[CX_NW];
+    __shared__ unsigned long long s_tmp64[CX_NW];
+    __shared__ long long s_tile;
+    __shared__ int s_head_nl, s_last_nl, s_nrare, s_special, s_err_ord;
+    __shared__ unsigned s_esc, s_skip, s_flag, s_inl;
+    __shared__ unsigned long long s_pre_out, s_pre_lines;
+
+    const CxSmem S = cx_carve(smem, cx_ns, cx_nw);
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(cx_dfa);
+        uint4 *dst = reinterpret_cast<uint4 *>(S.dfa);
+        for (int k = threadIdx.x; k < cx_align16(cx_ns * CX_NCOL * 2) / 16; k += CX_NT) dst[k] = src[k];
+        for (int k = threadIdx.x; k < cx_nw * T2_MASKS; k += CX_NT) S.t2[k] = cx_t2[k];
+        for (int k = threadIdx.x; k < cx_ns * CX_CODES; k += CX_NT) S.codes[k] = cx_codes[k];
+        for (int k = threadIdx.x; k < 256; k += CX_NT) S.explen[k] = k == '\n' ? 1 : tb.exp_len[k];
+        for (int k = threadIdx.x; k < 8 * 256; k += CX_NT) {
+            const unsigned st = k >> 8, b = k & 255;
+            S.lut[k] = b == '\n' ? (uint8_t)128u : tk_entry(st, b);  // '\n': line end (bit 7)
+        }
+    }
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    if (tid == 0) s_esc = 0;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) {
+            if (s_esc) atomicAdd(&job.ctl->escapes, (unsigned long long)s_esc);  // previous tile
+            s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
+            s_nrare = 0;
+            s_special = 0;
+            s_err_ord = 0x7fffffff;
+            s_esc = s_skip = s_flag = 0;
+        }
+        __syncthreads();
+        const long long t = s_tile;
+        if (t >= job.n_tiles) break;
+        const long long T0 = t * (long long)CX_TILE;
+        const long long T1 = min(job.n, T0 + CX_TILE);
+        const long long ws = T0 - CX_HEAD;
+        const int tile_end = (int)(T1 - ws);
+        load_window(job.in, job.n, ws, cx_align16(tile_end), S.win);
+        for (int k = tid; k < CX_WORDS; k += CX_NT) S.ebits[k] = S.fbits[k] = 0u;
+        __syncthreads();
+        // the final tile closes a last line without '\n' with a virtual one
+        int win_end = tile_end;
+        if (T1 == job.n && S.win[tile_end - 1] != '\n') {
+            win_end = tile_end + 1;
+            if (tid == 0) S.win[tile_end] = '\n';
+        }
+        // ---- P1: newline bitmap of [0, win_end) ----
+        for (int wd = tid; wd < CX_WORDS; wd += CX_NT) {
+            unsigned m = 0;
+            const int b0 = wd * 32;
+            if (b0 < win_end) {
+                const unsigned *w4 = reinterpret_cast<const unsigned *>(S.win + b0);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const unsigned x = w4[k] ^ 0x0a0a0a0au;
+                    const unsigned z = ~(((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x | 0x7f7f7f7fu);
+                    const unsigned nib = ((z >> 7) & 1u) | ((z >> 14) & 2u) | ((z >> 21) & 4u) | ((z >> 28) & 8u);
+                    m |= nib << (4 * k);
+                }
+                if (b0 + 32 > win_end) m &= (1u << (win_end - b0)) - 1u;
+            }
+            S.rbits[wd] = m;
+        }
+        __syncthreads();
+        const int c0 = CX_HEAD + tid * CX_CC;
+        const int c1 = min(c0 + CX_CC, win_end);
+        int first_nl = 0x7fffffff, last_nl = -1;
+        for (int wd = c0 >> 5; c0 < c1 && wd <= (c1 - 1) >> 5; ++wd) {
+            unsigned m = S.rbits[wd];
+            const int b0 = wd * 32;
+            if (b0 < c0) m &= 0xffffffffu << (c0 - b0);
+            if (b0 + 32 > c1) m &= (1u << (c1 - b0)) - 1u;
+            if (m) {
+                if (first_nl == 0x7fffffff) first_nl = b0 + __ffs(m) - 1;
+                last_nl = b0 + 31 - __clz(m);
+            }
+        }
+        if (tid < 32) {
+            // last '\n' before the tile (in the staged head); -1: none
+            int best = -1;
+            for (int wd = (CX_HEAD >> 5) - 1 - lane; wd >= 0; wd -= 32) {
+                const unsigned m = S.rbits[wd];
+                best = max(best, m ? wd * 32 + 31 - __clz(m) : -1);
+            }
+            best = __reduce_max_sync(0xffffffffu, best);
+            if (lane == 0) s_head_nl = best;
+        }
+        const int Lx = cx_block_scan_mm<true>(last_nl, s_tmp, true, -1);  // last '\n' before c0
+        const int Rx = cx_block_suffix_min(first_nl, s_tmp);             // first '\n' at/after c0
+        if (tid == CX_NT - 1) s_last_nl = max(Lx, last_nl);              // the tile's last '\n'
+        const int head_nl = s_head_nl;
+        // cut before lane tid: the newline nearest to c0 (lane 0: the head newline)
+        int cut;
+        {
+            const int L = Lx >= 0 ? Lx : head_nl;
+            if (tid == 0 || Rx == 0x7fffffff) cut = L;
+            else if (L < 0) cut = Rx;
+            else cut = (Rx - c0 < c0 - L) ? Rx : L;
+        }
+        S.lane_a[tid] = cut;
+        __syncthreads();
+        // lane range (cut, end]; end = next lane's cut (last lane: the tile's last '\n')
+        const int end = tid + 1 < CX_NT ? S.lane_a[tid + 1] : s_last_nl;
+        // a line that starts before the window is owned by the lane whose
+        // range holds its '\n' (the tile's first newline): a "global" line
+        const bool glob = cut < 0 && end >= CX_HEAD;
+        int start = cut + 1;
+        int gpos = -1;
+        if (end < CX_HEAD) start = end + 1;  // no line of this tile
+        if (glob) {
+            gpos = cx_next(S.rbits, CX_HEAD);
+            start = gpos;
+        }
+        const int first = glob ? gpos + 1 : start;  // first byte of the first in-window line
+
+        // ---- P2: tokenizer; CR / tokenize errors; ring-token bits ----
+        int nlines = glob ? 1 : 0;
+        {
+            unsigned st = TK_OUT0, crs = 0;
+            int ls = first;
+            for (int p = first; ZS_ANY(p <= end); ++p) {
+                if (p > end) continue;
+                const unsigned e = S.lut[(st << 8) | S.win[p]];
+                if (e & (TK_RING | 128u)) {
+                    if (e & 128u) {  // line end
+                        int k = E_NONE;
+                        if (crs & TK_CR) k = E_CR;
+                        else if (job.preprocess && (st == TK_ERR || st >= TK_P1R)) k = E_PERCENT;
+                        else if (job.preprocess && st == TK_IN) k = E_BRACKET;
+                        if (k != E_NONE) {
+                            if (k == E_CR || !job.lenient)
+                                cx_rare(S, &s_nrare, ls, p, job.lenient ? RK_DROP : RK_STRICT, tid, nlines, k, 0);
+                            else
+                                atomicAdd(&s_flag, 1u);  // lenient: the raw line is compressed
+                            cx_set(S.ebits, ls);             // P3: not renumbered
+                        }
+                        ++nlines;
+                        ls = p + 1;
+                        crs = 0;
+                        st = TK_OUT0;
+                        continue;
+                    }
+                    if (job.preprocess) cx_set(S.rbits, p);
+                }
+                st = e & 7u;
+                crs |= e;
+            }
+        }
+        S.lane_b[tid] = nlines;
+        __syncthreads();
+
+        // ---- P3: ring pairing + colouring (smiles.py:140-213) ----
+        int sub = 0;  // filler bytes x 2 to take off the lane's parse cost
+        if (job.preprocess) {
+            int ls = first, pos = first - 1, local = glob ? 1 : 0;
+            unsigned oid = 0xffffffffu;  // 4 slots: open ring id per byte, 0xff = free
+            int opos[4] = {0, 0, 0, 0};
+            int lc[10];
+#pragma unroll
+            for (int k = 0; k < 10; ++k) lc[k] = -1;
+            int n_pct = 0;
+            bool skip = ls <= end && cx_bit(S.ebits, ls), fail = false;
+            for (;;) {
+                const bool more = pos < end;
+                if (!ZS_ANY(more)) break;
+                if (!more) continue;
+                const int q = cx_next(S.rbits, pos + 1);
+                pos = q;
+                const unsigned c = S.win[q];
+                if (c == '\n') {
+                    if (skip) {
+                        cx_clr(S.ebits, ls);
+                    } else if (fail) {
+                        // beyond the fast path (> 4 open rings, colour >= 10): general routine
+                        cx_rare(S, &s_nrare, ls, q, RK_ARENA, tid, local, 0, 0);
+                    } else if (oid != 0xffffffffu) {
+                        // ring ids left open (smiles.py:151-159)
+                        if (job.lenient) {
+                            for (int j = ls; j < q; ++j) S.win[j] = job.in[ws + j];
+                            atomicAdd(&s_flag, 1u);
+                        } else {
+                            cx_rare(S, &s_nrare, ls, q, RK_STRICT, tid, local, E_UNPAIRED, 0);
+                        }
+                    } else if (n_pct) {
+                        // a '%nn' ring token keeps only its colour digit
+                        int w = ls;
+                        for (int r = ls; r < q;) {
+                            if (S.win[r] == '%' && cx_bit(S.rbits, r)) {
+                                S.win[w++] = S.win[r + 1];
+                                r += 3;
+                            } else {
+                                S.win[w++] = S.win[r++];
+                            }
+                        }
+                        for (int j = w; j < q; ++j) {
+                            S.win[j] = 0x01;  // escape-only filler
+                            cx_set(S.fbits, j);
+                        }
+                        sub += 2 * (q - w);
+                        s_special = 1;
+                    }
+                    ls = q + 1;
+                    ++local;
+                    oid = 0xffffffffu;
+#pragma unroll
+                    for (int k = 0; k < 10; ++k) lc[k] = -1;
+                    n_pct = 0;
+                    fail = false;
+                    skip = ls <= end && cx_bit(S.ebits, ls);
+                    continue;
+                }
+                if (skip || fail) continue;
+                const bool pct = c == '%';
+                const unsigned rid = pct ? (S.win[q + 1] - '0') * 10u + (S.win[q + 2] - '0') : c - '0';
+                n_pct += pct;
+                int slot = -1, free_slot = -1;
+#pragma unroll
+                for (int k = 3; k >= 0; --k) {
+                    const unsigned v = (oid >> (8 * k)) & 0xffu;
+                    if (v == rid) slot = k;
+                    if (v == 0xffu) free_slot = k;
+                }
+                if (slot < 0) {
+                    if (free_slot < 0) {
+                        fail = true;
+                        continue;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (k == free_slot) opos[k] = q;
+                    oid = (oid & ~(0xffu << (8 * free_slot))) | (rid << (8 * free_slot));
+                } else {
+                    int o = 0;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (k == slot) o = opos[k];
+                    oid |= 0xffu << (8 * slot);
+                    // smallest colour not taken by a ring closed inside (o, q)
+                    int col = 10;
+#pragma unroll
+                    for (int k = 9; k >= 0; --k)
+                        if (lc[k] <= o) col = k;
+                    if (col == 10) {
+                        fail = true;
+                        continue;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 10; ++k)
+                        if (k == col) lc[k] = q;
+                    S.win[o + (S.win[o] == '%')] = (uint8_t)('0' + col);
+                    S.win[q + pct] = (uint8_t)('0' + col);
+                }
+            }
+        }
+        if (glob) cx_rare(S, &s_nrare, gpos, gpos, RK_ARENA, tid, 0, 0, 1);
+        // lane line bases (strict error ordinals)
+        {
+            int tot;
+            const int nl_mine = S.lane_b[tid];
+            const int base = block_exscan<int>(nl_mine, s_tmp, tot);
+            S.lane_c[tid] = base;
+            S.lane_b[tid] = 0;  // reused: lane output adjustments
+            if (tid == 0) s_inl = (unsigned)tot;
+        }
+        __syncthreads();
+        const int n_rare = min(s_nrare, CX_RARE);
+        if (tid == 0 && s_nrare > CX_RARE) atomicOr(&job.ctl->overflow, 8ull);  // host: general kernel
+
+        // ---- rare lines: general routine, escape-only filler (one thread each) ----
+        for (int r = tid; r < n_rare; r += CX_NT) {
+            CxRare &R = S.rare[r];
+            int adj = 0;
+            if (R.kind == RK_ARENA) {
+                long long ge = ws + R.le, gs = ws + R.ls;
+                if (R.glob) {
+                    gs = ge;
+                    while (gs > 0 && job.in[gs - 1] != '\n') --gs;
+                }
+                unsigned aoff = 0;
+                int kind = E_NONE, eoff = -1;
+                unsigned long long ids[2] = {0, 0};
+                const long long cost = compress_line_global(job, tb, gs, ge - gs, &aoff, &kind, &eoff, ids);
+                R.gs = gs;
+                if (kind == -2) {
+                    R.kind = RK_DROP;  // arena exhausted: the host grows it and re-runs
+                } else if (kind == E_CR || (kind > 0 && !job.lenient)) {
+                    R.kind = job.lenient ? RK_DROP : RK_STRICT;
+                    R.err = kind;
+                } else {
+                    if (kind == -3) atomicAdd(&s_flag, 1u);
+                    R.aoff = aoff;
+                    adj += (int)cost + 1;
+                }
+            }
+            // the parse prices each filler byte at exactly 2 (an escape)
+            const int a = R.glob ? R.le : R.ls;
+            for (int j = a; j <= R.le; ++j) {
+                S.win[j] = 0x01;
+                cx_set(S.fbits, j);
+            }
+            if (R.kind == RK_ARENA) S.win[a] = 0x02;
+            adj -= 2 * (R.le - a + 1);
+            atomicAdd(&S.lane_b[R.lane], adj);
+            if (R.kind == RK_DROP) atomicAdd(&s_skip, 1u);
+            if (R.kind == RK_STRICT) atomicMin(&s_err_ord, S.lane_c[R.lane] + R.local);
+        }
+        if (tid == 0 && n_rare) s_special = 1;
+        __syncthreads();
+
+        // ---- P4: min-cost parse, right to left over the lane's range ----
+        unsigned acc = 0, nesc = 0;
+        {
+            const uint16_t *dfa = S.dfa;
+            const uint32_t *t2 = S.t2;
+            const uint8_t *codes = S.codes;
+            uint8_t *win = S.win;
+            unsigned st = 0, wi = 0;
+            for (int i = end; ZS_ANY(i >= start); --i) {
+                if (i < start) continue;
+                const unsigned b = win[i];
+                const unsigned e = dfa[st * CX_NCOL + umin_(b - 10u, 118u)];
+                st = e & 0xffu;
+                const unsigned x = t2[wi * T2_MASKS + (e >> 8)];
+                wi = x & 0xfffu;
+                const unsigned L = (x >> 12) & 15u;
+                acc += x >> 16;
+                if (L) {
+                    win[i] = codes[st * CX_CODES + L - 1];
+                } else {
+                    cx_set(S.ebits, i);
+                    ++nesc;
+                }
+            }
+        }
+        const int nbytes = end >= start ? end - start + 1 : 0;
+        const long long my_out = (long long)acc - 16ll * nbytes - sub + S.lane_b[tid];
+        if (__syncthreads_or(nesc != 0) && tid == 0) s_special = 1;
+        // ---- P5: tile output bytes; publish ----
+        unsigned long long tile_out;
+        const unsigned long long my_off = block_exscan<unsigned long long>((unsigned long long)my_out, s_tmp64, tile_out);
+        const unsigned tile_lines = s_inl;
+        if (tid == 0) lookback_publish(job.ts, t, tile_out, (unsigned long long)tile_lines);
+        const bool staged = tile_out <= (unsigned long long)CX_OUTCAP;
+        const bool special = s_special != 0;
+        // ---- P6: emit (to staging now, or to HBM after the look-back) ----
+        unsigned esc = 0;
+        if (staged && start <= end)
+            esc = special ? cx_emit_range<true>(job, S, ws, start, end, S.out, my_off, n_rare)
+                          : cx_emit_range<false>(job, S, ws, start, end, S.out, my_off, n_rare);
+        if (tid < 32) {
+            unsigned long long po, pl;
+            lookback_resolve(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
+            if (tid == 0) {
+                s_pre_out = po;
+                s_pre_lines = pl;
+            }
+        }
+        __syncthreads();
+        const unsigned long long pre_out = s_pre_out;
+        const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
+        if (!staged && fits && start <= end)
+            esc = special ? cx_emit_range<true>(job, S, ws, start, end, job.out, pre_out + my_off, n_rare)
+                          : cx_emit_range<false>(job, S, ws, start, end, job.out, pre_out + my_off, n_rare);
+        if (esc) atomicAdd(&s_esc, esc);
+        if (tid == 0) {
+            atomicAdd(&job.ctl->total_out, tile_out);
+            atomicAdd(&job.ctl->lines, (unsigned long long)(tile_lines - s_skip));
+            atomicAdd(&job.ctl->in_lines, (unsigned long long)tile_lines);
+            if (s_skip && job.lenient) atomicAdd(&job.ctl->skipped, (unsigned long long)s_skip);
+            if (s_flag) atomicAdd(&job.ctl->flagged, (unsigned long long)s_flag);
+            if (!fits) atomicOr(&job.ctl->overflow, 1ull);
+        }
+        // ---- strict error: details of the tile's first bad line ----
+        if (tid == 0 && s_err_ord != 0x7fffffff) {
+            const int ord = s_err_ord;
+            long long gs = 0, ge = 0;
+            int kind = E_NONE;
+            for (int r = 0; r < n_rare; ++r) {
+                const CxRare &R = S.rare[r];
+                if (R.kind == RK_STRICT && S.lane_c[R.lane] + R.local == ord) {
+                    ge = ws + R.le;
+                    gs = R.glob ? R.gs : ws + R.ls;
+                    kind = R.err;
+                }
+            }
+            TileErr e = {kind, 0, -1, {0, 0}};
+            bool cr = false;
+            for (long long k = gs; k < ge; ++k) cr |= job.in[k] == '\r';
+            if (cr) {
+                e.kind = E_CR;
+            } else if (job.preprocess) {
+                int nl2, eoff = -1;
+                unsigned long long ids[2] = {0, 0};
+                const long long n_l = ge - gs;
+                const unsigned long long need = (4 * (unsigned long long)n_l + 19) & ~15ull;
+                const unsigned long long a = atomicAdd(&job.ctl->arena_used, need);
+                uint8_t *tmp = a + need <= (unsigned long long)job.arena_cap ? job.arena + a : nullptr;
+                if (!tmp) atomicOr(&job.ctl->overflow, 2ull);
+                const int k = tmp ? preprocess_line(job.in + gs, (int)n_l, tmp, tmp + n_l + 1, &nl2, &eoff, ids)
+                                  : E_NONE;
+                e.kind = k;
+                e.offset = eoff;
+                e.ids[0] = ids[0];
+                e.ids[1] = ids[1];
+            }
+            job.terr[t] = e;
+            __threadfence();
+            atomicMin(&job.ctl->err_key, ((s_pre_lines + (unsigned long long)ord) << 24) |
+                                             (unsigned long long)(t & 0xffffff));
+        }
+        if (fits && staged) store_out(job.out + pre_out, S.out, (int)tile_out);
+    }
+}
+
+}  // namespace zs

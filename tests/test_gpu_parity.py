@@ -335,12 +335,13 @@ def test_device_and_host_api_agree():
     assert (r.lines, r.out_bytes) == (res.lines, res.out_bytes)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 3, 7])
+@pytest.mark.parametrize("mode", [0, 1, 3, 7, 11])
 def test_kernel_variants_bit_exact(corpus_hashes, mode):
     """Every compress kernel variant (0: key-window DP with a decision array,
-    1: + cost-window transducer, 3: + in-place decisions, the default; bit 2
-    selects the warp-cooperative decompress instead of the per-thread-slice
-    one) gives the reference bytes, both directions."""
+    1: + cost-window transducer, 3: + in-place decisions -- the lane-chunk
+    kernel, the default; 11: the queue-based in-place kernel; bit 2 selects
+    the warp-cooperative decompress instead of the streaming one) gives the
+    reference bytes, both directions."""
     ctx = _lib.context()
     try:
         ctx.lib.zs_set_transducer(ctx.h, mode)
