@@ -293,7 +293,8 @@ bool build_t2(HostTables &ht, int W) {
 // c = min(b - 10, 118): 0 = '\n', 22..117 = 0x20..0x7f, the rest = other)
 // whose entry returns to the root with the reserved mask slot CX_NLMASK; the
 // transducer's CX_NLMASK entry of every window resets to the line-end window
-// with code slot 9 (the record separator, cost +1).
+// with code slot 9 (the record separator, cost +1).  Code slot 0 (an escape)
+// is 0x20, so the parse writes every decision without a branch.
 bool build_cx(HostTables &ht, int max_len) {
     if (!ht.t2_ok || ht.n_masks > CX_NLMASK || max_len > 8) return false;
     const int ns = ht.n_states, nw = ht.n_windows;
@@ -314,10 +315,13 @@ bool build_cx(HostTables &ht, int max_len) {
     ht.cx_t2 = ht.t2;
     for (int w = 0; w < nw; ++w)
         ht.cx_t2[(size_t)w * T2_MASKS + CX_NLMASK] = 0u | (9u << 12) | ((1u + 16u) << 16);
+    // code slot L: 0 = escape (0x20, never a code), 1..8 = the match of length L, 9 = '\n'
     ht.cx_codes.assign((size_t)cx_align16(ns * CX_CODES), 0);
     for (int st = 0; st < ns; ++st) {
-        for (int L = 0; L < FAST_W; ++L) ht.cx_codes[(size_t)st * CX_CODES + L] = ht.codes[(size_t)st * FAST_W + L];
-        ht.cx_codes[(size_t)st * CX_CODES + 8] = '\n';
+        ht.cx_codes[(size_t)st * CX_CODES] = 0x20;
+        for (int L = 1; L <= FAST_W; ++L)
+            ht.cx_codes[(size_t)st * CX_CODES + L] = ht.codes[(size_t)st * FAST_W + L - 1];
+        ht.cx_codes[(size_t)st * CX_CODES + 9] = '\n';
     }
     ht.cx_ok = true;
     return true;
@@ -731,7 +735,7 @@ void *zs_stream(zs_ctx *ctx) { return ctx ? (void *)ctx->stream[0] : nullptr; }
 
 int zs_set_phase_timing(zs_ctx *ctx, int on) {
     if (!ctx) return ZS_E_ARG;
-    ctx->timing = on ? 1 : 0;
+    ctx->timing = on;  // 1: per-phase clocks; 2: lane-range statistics (compress_cx)
     return ZS_OK;
 }
 

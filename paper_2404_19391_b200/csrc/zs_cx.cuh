@@ -27,26 +27,28 @@
 //   P6  forward walk of the decisions (numba_impl.py:57-69) into an smem
 //       staging buffer, then aligned 16-byte stores at the resolved offset.
 //
-// Escapes keep their literal in place with a bit in `ebits` (which first
-// carries P2's per-line error flags to P3); `rbits` marks newlines and ring
-// tokens for P3; `fbits` marks filler and arena-marker positions for P6.
+// Escape decisions are the byte 0x20 (never a code); the emit re-reads the
+// literal from the input in HBM.  `rbits` marks newlines and ring tokens for
+// P3, `ebits` carries P2's per-line error flags to P3, `fbits` marks filler
+// and arena-marker positions for P6.
 #pragma once
 #include "zs_kernels.cuh"
 
 namespace zs {
 
-constexpr int CX_NT = 512;
+constexpr int CX_NT = 1024;
 constexpr int CX_NW = CX_NT / 32;
-constexpr int CX_CC = 100;                        // 25 words: odd word stride across lanes
+constexpr int CX_CC = 50;                         // bytes of line ends per lane
 constexpr int CX_TILE = CX_NT * CX_CC;            // 51200
 constexpr int CX_HEAD = 2048;                     // staged before the tile
 constexpr int CX_WIN = CX_HEAD + CX_TILE;         // 53248 (multiple of 32)
-constexpr int CX_WORDS = CX_WIN / 32 + 2;         // bitmap words
+constexpr int CX_WORDS = CX_WIN / 32 + 4;         // bitmap words (multiple of 4: keeps the carve 16-aligned)
 constexpr int CX_NCOL = 119;                      // dcol: umin(b - 10, 118); 0 = '\n'
 constexpr int CX_NLMASK = 15;                     // transducer mask slot of '\n'
-constexpr int CX_CODES = 16;                      // codes per state (slot 8 = '\n')
+constexpr int CX_CODES = 16;                      // code slots per state: 0 escape, 1-8 match, 9 '\n'
 constexpr int CX_OUTCAP = 26624;                  // staging (ratio <= ~0.5)
 constexpr int CX_RARE = 128;                      // rare lines per tile
+constexpr int CX_JOBS = 16;                       // '%nn' compactions per warp and tile
 
 // rare-line kinds
 enum : int { RK_DROP = 1, RK_ARENA = 2, RK_STRICT = 3 };
@@ -67,7 +69,7 @@ __host__ __device__ inline int cx_align16(int x) { return (x + 15) & ~15; }
 __host__ __device__ inline int cx_smem_bytes(int ns, int nw) {
     return cx_align16(ns * CX_NCOL * 2) + nw * T2_MASKS * 4 + cx_align16(ns * CX_CODES) + 256 + 8 * 256 +
            cx_align16(CX_WIN + 32) + 3 * CX_WORDS * 4 + CX_OUTCAP + CX_RARE * (int)sizeof(CxRare) +
-           3 * CX_NT * 4;
+           3 * CX_NT * 4 + CX_NW * CX_JOBS * 16 + CX_NW * 4;
 }
 
 struct CxSmem {
@@ -81,6 +83,8 @@ struct CxSmem {
     uint8_t *out;
     CxRare *rare;
     int *lane_a, *lane_b, *lane_c;
+    int4 *jobs;   // [warp][CX_JOBS] (ls, q, owner lane, local line index)
+    int *njobs;   // [warp]
 };
 
 __device__ inline CxSmem cx_carve(uint8_t *p, int ns, int nw) {
@@ -98,8 +102,34 @@ __device__ inline CxSmem cx_carve(uint8_t *p, int ns, int nw) {
     S.rare = reinterpret_cast<CxRare *>(p); p += CX_RARE * sizeof(CxRare);
     S.lane_a = reinterpret_cast<int *>(p); p += CX_NT * 4;
     S.lane_b = reinterpret_cast<int *>(p); p += CX_NT * 4;
-    S.lane_c = reinterpret_cast<int *>(p);
+    S.lane_c = reinterpret_cast<int *>(p); p += CX_NT * 4;
+    S.jobs = reinterpret_cast<int4 *>(p); p += CX_NW * CX_JOBS * 16;
+    S.njobs = reinterpret_cast<int *>(p);
     return S;
+}
+
+// explicit 32-bit shared addresses in the hot loops (a generic pointer makes
+// the compiler rebuild the shared window base inside every loop trip)
+__device__ __forceinline__ unsigned cx_lb(unsigned a) {
+    unsigned v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ unsigned cx_lh(unsigned a) {
+    unsigned v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ unsigned cx_lw(unsigned a) {
+    unsigned v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void cx_sb(unsigned a, unsigned v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cx_or(unsigned a, unsigned v) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ unsigned cx_bit(const unsigned *bm, int p) { return (bm[p >> 5] >> (p & 31)) & 1u; }
@@ -180,34 +210,70 @@ __device__ __forceinline__ unsigned cx_emit_arena(const Job &job, const uint8_t 
     return esc;
 }
 
-// P6 walk of one lane range [p0, p1] into o at w.  SPECIAL: the tile has
-// escapes, filler or arena lines (bit checks); else the plain code walk.
-template <bool SPECIAL>
+// P6 walk of one lane range [p0, p1] into o at w (STAGED: o is the smem
+// staging buffer).  A decision byte 0x20 is an escape (literal re-read from
+// the input in HBM) unless `fbits` marks the position as filler or as an
+// arena line's marker.
+template <bool STAGED>
 __device__ __forceinline__ unsigned cx_emit_range(const Job &job, const CxSmem &S, long long ws, int p0, int p1,
                                                   uint8_t *o, unsigned long long w, int n_rare) {
     unsigned esc = 0;
-    const uint8_t *win = S.win;
+    const uint8_t *__restrict__ win = S.win;
+    const uint8_t *__restrict__ explen = S.explen;
     for (int p = p0; p <= p1;) {
         const unsigned c = win[p];
-        if (SPECIAL && cx_bit(S.ebits, p)) {
+        if (c == 0x20) {
             if (cx_bit(S.fbits, p)) {
-                if (c == 0x02) {  // arena line marker
-                    for (int r = 0; r < n_rare; ++r)
-                        if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p)
-                            esc += cx_emit_arena(job, S.explen, S.rare[r].aoff, o, w, S.rare[r].gs);
-                }
+                for (int r = 0; r < n_rare; ++r)  // an arena line's marker?
+                    if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p)
+                        esc += cx_emit_arena(job, S.explen, S.rare[r].aoff, o, w, S.rare[r].gs);
             } else {
-                o[w++] = 0x20;
-                o[w++] = (uint8_t)c;
+                o[w] = 0x20;
+                o[w + 1] = job.in[ws + p];
+                w += 2;
                 ++esc;
             }
             ++p;
         } else {
             o[w++] = (uint8_t)c;
-            p += S.explen[c];
+            p += explen[c];
         }
     }
     return esc;
+}
+
+// Stage window bytes [ws, ws+len) (positions before the buffer read as '\n'
+// so offset 0 is a line start; positions past the end as '\n').
+__device__ __forceinline__ void cx_load_window(const uint8_t *in, long long n, long long ws, int len, uint8_t *win) {
+    const bool aligned = ((reinterpret_cast<uintptr_t>(in) & 15) == 0) && ws >= 0 && ws + len <= n && (len & 15) == 0;
+    if (aligned) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(in + ws);
+        uint4 *dst = reinterpret_cast<uint4 *>(win);
+        for (int k = threadIdx.x; k < len / 16; k += CX_NT) dst[k] = __ldcs(src + k);
+    } else {
+        for (int k = threadIdx.x; k < len; k += CX_NT) {
+            const long long g = ws + k;
+            win[k] = g < 0 ? (uint8_t)'\n' : (g < n ? __ldcs(in + g) : (uint8_t)'\n');
+        }
+    }
+}
+
+// Staged tile output -> HBM: bytes until dst is 16-byte aligned, then 16-byte stores.
+__device__ __forceinline__ void cx_store_out(uint8_t *dst, const uint8_t *src, int len) {
+    const int head = min(len, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
+    if ((int)threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
+    const int nvec = (len - head) >> 4;
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst + head);
+    for (int k = threadIdx.x; k < nvec; k += CX_NT) {
+        const uint8_t *q = src + head + 16 * k;
+        uint4 v;
+        v.x = q[0] | (q[1] << 8) | (q[2] << 16) | ((unsigned)q[3] << 24);
+        v.y = q[4] | (q[5] << 8) | (q[6] << 16) | ((unsigned)q[7] << 24);
+        v.z = q[8] | (q[9] << 8) | (q[10] << 16) | ((unsigned)q[11] << 24);
+        v.w = q[12] | (q[13] << 8) | (q[14] << 16) | ((unsigned)q[15] << 24);
+        d4[k] = v;
+    }
+    for (int k = head + (nvec << 4) + threadIdx.x; k < len; k += CX_NT) dst[k] = src[k];
 }
 
 // record a rare line (returns false when the tile's list is full)
@@ -235,7 +301,7 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
     __shared__ int s_tmp[CX_NW];
     __shared__ unsigned long long s_tmp64[CX_NW];
     __shared__ long long s_tile;
-    __shared__ int s_head_nl, s_last_nl, s_nrare, s_special, s_err_ord;
+    __shared__ int s_head_nl, s_last_nl, s_nrare, s_err_ord;
     __shared__ unsigned s_esc, s_skip, s_flag, s_inl;
     __shared__ unsigned long long s_pre_out, s_pre_lines;
 
@@ -249,12 +315,20 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
         for (int k = threadIdx.x; k < 256; k += CX_NT) S.explen[k] = k == '\n' ? 1 : tb.exp_len[k];
         for (int k = threadIdx.x; k < 8 * 256; k += CX_NT) {
             const unsigned st = k >> 8, b = k & 255;
-            S.lut[k] = b == '\n' ? (uint8_t)128u : tk_entry(st, b);  // '\n': line end (bit 7)
+            uint8_t e = tk_entry(st, b);
+            if (b == '\n') {  // line end: back to TK_OUT0; flag an open bracket / a bad '%'
+                e = 128u;
+                if (job.preprocess && st == TK_IN) e |= 0x20u;
+                if (job.preprocess && (st == TK_ERR || st >= TK_P1R)) e |= 0x40u;
+            }
+            S.lut[k] = e;
         }
     }
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     if (tid == 0) s_esc = 0;
+    PhaseClock pc;
+    pc.start();
 
     for (;;) {
         __syncthreads();
@@ -262,7 +336,6 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
             if (s_esc) atomicAdd(&job.ctl->escapes, (unsigned long long)s_esc);  // previous tile
             s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
             s_nrare = 0;
-            s_special = 0;
             s_err_ord = 0x7fffffff;
             s_esc = s_skip = s_flag = 0;
         }
@@ -273,8 +346,10 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
         const long long T1 = min(job.n, T0 + CX_TILE);
         const long long ws = T0 - CX_HEAD;
         const int tile_end = (int)(T1 - ws);
-        load_window(job.in, job.n, ws, cx_align16(tile_end), S.win);
+        cx_load_window(job.in, job.n, ws, cx_align16(tile_end), S.win);
         for (int k = tid; k < CX_WORDS; k += CX_NT) S.ebits[k] = S.fbits[k] = 0u;
+        S.lane_b[tid] = 0;  // lane output adjustments (compaction gaps, arena lines)
+        if (lane == 0) S.njobs[tid >> 5] = 0;
         __syncthreads();
         // the final tile closes a last line without '\n' with a virtual one
         int win_end = tile_end;
@@ -337,6 +412,7 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
         }
         S.lane_a[tid] = cut;
         __syncthreads();
+        pc.mark(job, 0);  // load, newline bitmap, lane cuts
         // lane range (cut, end]; end = next lane's cut (last lane: the tile's last '\n')
         const int end = tid + 1 < CX_NT ? S.lane_a[tid + 1] : s_last_nl;
         // a line that starts before the window is owned by the lane whose
@@ -350,164 +426,316 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
             start = gpos;
         }
         const int first = glob ? gpos + 1 : start;  // first byte of the first in-window line
-
-        // ---- P2: tokenizer; CR / tokenize errors; ring-token bits ----
-        int nlines = glob ? 1 : 0;
-        {
-            unsigned st = TK_OUT0, crs = 0;
-            int ls = first;
-            for (int p = first; ZS_ANY(p <= end); ++p) {
-                if (p > end) continue;
-                const unsigned e = S.lut[(st << 8) | S.win[p]];
-                if (e & (TK_RING | 128u)) {
-                    if (e & 128u) {  // line end
-                        int k = E_NONE;
-                        if (crs & TK_CR) k = E_CR;
-                        else if (job.preprocess && (st == TK_ERR || st >= TK_P1R)) k = E_PERCENT;
-                        else if (job.preprocess && st == TK_IN) k = E_BRACKET;
-                        if (k != E_NONE) {
-                            if (k == E_CR || !job.lenient)
-                                cx_rare(S, &s_nrare, ls, p, job.lenient ? RK_DROP : RK_STRICT, tid, nlines, k, 0);
-                            else
-                                atomicAdd(&s_flag, 1u);  // lenient: the raw line is compressed
-                            cx_set(S.ebits, ls);             // P3: not renumbered
-                        }
-                        ++nlines;
-                        ls = p + 1;
-                        crs = 0;
-                        st = TK_OUT0;
-                        continue;
-                    }
-                    if (job.preprocess) cx_set(S.rbits, p);
-                }
-                st = e & 7u;
-                crs |= e;
+        if (job.timing == 2) {  // debug: lane range statistics
+            const int len = max(0, end - start + 1);
+            const int wmax = __reduce_max_sync(0xffffffffu, len);
+            const int wsum = __reduce_add_sync(0xffffffffu, len);
+            if (lane == 0) {
+                atomicAdd(&job.ctl->phase[0], (unsigned long long)wmax);
+                atomicAdd(&job.ctl->phase[1], (unsigned long long)wsum);
+                atomicAdd(&job.ctl->phase[2], 1ull);
             }
         }
-        S.lane_b[tid] = nlines;
-        __syncthreads();
+
+        // P2 -> P3 -> P4 run per warp without block barriers: a lane only
+        // touches its own range (bitmap words shared with a neighbour are
+        // updated atomically).  Rare lines are turned into escape-only filler
+        // by their owner right away (the parse prices a filler byte at exactly
+        // 2); their general-routine work waits until after the parse.
+        int sub = 0;  // parse cost of the lane's filler bytes (2 each)
+        auto filler = [&](int a, int b) {  // window positions [a, b]
+            for (int j = a; j <= b; ++j) {
+                S.win[j] = 0x01;
+                cx_set(S.fbits, j);
+            }
+            sub += 2 * (b - a + 1);
+        };
+        // ---- P2: tokenizer; CR / tokenize errors; ring-token bits ----
+        // LUT entry: bits 0-2 next state, 3 ring token, 4 '\r', 7 line end;
+        // a line end's bits 5/6 flag an unclosed '[' / a bad '%' (preprocess).
+        // Ring-token bits gather in a register per 32-byte bitmap word.
+        int nlines = glob ? 1 : 0;
+        {
+            const uint8_t *__restrict__ lut = S.lut;
+            const unsigned *__restrict__ w32 = reinterpret_cast<const unsigned *>(S.win);
+            unsigned st = TK_OUT0, crs = 0, rmask = 0;
+            int ls = first;
+            // one tokenizer step at window position p (byte b)
+            auto step = [&](int p, unsigned b) {
+                const unsigned e = lut[(st << 8) | b];
+                rmask |= ((e >> 3) & 1u) << (p & 31);
+                const bool nl = e & 128u;
+                if (nl && ((e & 0x60u) | (crs & TK_CR))) {
+                    const int k = (crs & TK_CR) ? E_CR : (e & 0x40u) ? E_PERCENT : E_BRACKET;
+                    if (k == E_CR || !job.lenient) {
+                        // dropped (lenient CR) or a strict error: filler (P3 fills when it gets there)
+                        cx_rare(S, &s_nrare, ls, p, job.lenient ? RK_DROP : RK_STRICT, tid, nlines, k, 0);
+                        if (job.preprocess) cx_set(S.ebits, p);  // P3: fill
+                        else filler(ls, p);
+                    } else {
+                        atomicAdd(&s_flag, 1u);  // lenient: the raw line is compressed
+                    }
+                    if (job.preprocess) cx_set(S.ebits, ls);  // P3: not renumbered
+                }
+                nlines += nl;
+                ls = nl ? p + 1 : ls;
+                crs = nl ? 0u : (crs | e);
+                st = e & 7u;
+            };
+            auto flush = [&](int p) {  // ring bits of the bitmap word holding p
+                if (rmask && job.preprocess) atomicOr(&S.rbits[p >> 5], rmask);
+                rmask = 0;
+            };
+            if (first <= end) {
+                int p = first;
+                // bytes up to a word boundary, then whole words, then the tail
+                const int w0 = (first + 3) & ~3, w1 = (end + 1) & ~3;
+                if (w0 < w1) {
+                    for (; p < w0; ++p) step(p, S.win[p]);
+                    if (p > first && (p & 31) == 0) flush(p - 1);
+                    unsigned cur = w32[p >> 2];
+                    for (; p < w1; p += 4) {
+                        const unsigned nxt = w32[(p >> 2) + 1];  // prefetch (the window has slack after it)
+                        step(p, cur & 0xffu);
+                        step(p + 1, (cur >> 8) & 0xffu);
+                        step(p + 2, (cur >> 16) & 0xffu);
+                        step(p + 3, cur >> 24);
+                        if (((p + 3) & 31) == 31) flush(p);
+                        cur = nxt;
+                    }
+                }
+                for (; p <= end; ++p) {
+                    step(p, S.win[p]);
+                    if ((p & 31) == 31) flush(p);
+                }
+                flush(end);
+            }
+        }
+        if (glob) {
+            cx_rare(S, &s_nrare, gpos, gpos, RK_ARENA, tid, 0, 0, 1);
+            filler(gpos, gpos);
+        }
+        pc.mark(job, 1);  // warp 0: tokenizer
 
         // ---- P3: ring pairing + colouring (smiles.py:140-213) ----
-        int sub = 0;  // filler bytes x 2 to take off the lane's parse cost
+        // One straight-line step per event (ring token or '\n') so the lanes
+        // of a warp stay converged: open rings in 4 register slots (id,
+        // position), colours 0-3 from their last close positions (a ring
+        // takes the smallest colour not closed inside it).  Lines beyond that
+        // (5+ open rings, colour >= 4, a colour digit that is not an identity
+        // code) go to the general routine.
         if (job.preprocess) {
+            const uint8_t *win = S.win;
             int ls = first, pos = first - 1, local = glob ? 1 : 0;
+            int n_ev = 0, n_cmp = 0;
             unsigned oid = 0xffffffffu;  // 4 slots: open ring id per byte, 0xff = free
-            int opos[4] = {0, 0, 0, 0};
-            int lc[10];
-#pragma unroll
-            for (int k = 0; k < 10; ++k) lc[k] = -1;
-            int n_pct = 0;
+            int op0 = 0, op1 = 0, op2 = 0, op3 = 0;
+            int lc0 = -1, lc1 = -1, lc2 = -1, lc3 = -1;
+            unsigned n_pct = 0;
             bool skip = ls <= end && cx_bit(S.ebits, ls), fail = false;
-            for (;;) {
-                const bool more = pos < end;
-                if (!ZS_ANY(more)) break;
-                if (!more) continue;
+            while (pos < end) {
                 const int q = cx_next(S.rbits, pos + 1);
                 pos = q;
-                const unsigned c = S.win[q];
+                ++n_ev;
+                const unsigned c = win[q];
                 if (c == '\n') {
-                    if (skip) {
-                        cx_clr(S.ebits, ls);
-                    } else if (fail) {
-                        // beyond the fast path (> 4 open rings, colour >= 10): general routine
-                        cx_rare(S, &s_nrare, ls, q, RK_ARENA, tid, local, 0, 0);
-                    } else if (oid != 0xffffffffu) {
-                        // ring ids left open (smiles.py:151-159)
-                        if (job.lenient) {
-                            for (int j = ls; j < q; ++j) S.win[j] = job.in[ws + j];
-                            atomicAdd(&s_flag, 1u);
-                        } else {
-                            cx_rare(S, &s_nrare, ls, q, RK_STRICT, tid, local, E_UNPAIRED, 0);
-                        }
-                    } else if (n_pct) {
-                        // a '%nn' ring token keeps only its colour digit
-                        int w = ls;
-                        for (int r = ls; r < q;) {
-                            if (S.win[r] == '%' && cx_bit(S.rbits, r)) {
-                                S.win[w++] = S.win[r + 1];
-                                r += 3;
+                    n_cmp += n_pct != 0;
+                    if ((skip | fail | (oid != 0xffffffffu) | (n_pct != 0)) && job.timing < 3) {
+                        if (skip) {
+                            // a P2 error line: dropped / strict lines become filler
+                            cx_clr(S.ebits, ls);
+                            if (cx_bit(S.ebits, q)) {
+                                cx_clr(S.ebits, q);
+                                filler(ls, q);
+                            }
+                        } else if (fail) {
+                            cx_rare(S, &s_nrare, ls, q, RK_ARENA, tid, local, 0, 0);
+                            filler(ls, q);
+                        } else if (oid != 0xffffffffu) {
+                            // ring ids left open (smiles.py:151-159)
+                            if (job.lenient) {
+                                for (int j = ls; j < q; ++j) S.win[j] = job.in[ws + j];
+                                atomicAdd(&s_flag, 1u);
                             } else {
-                                S.win[w++] = S.win[r++];
+                                cx_rare(S, &s_nrare, ls, q, RK_STRICT, tid, local, E_UNPAIRED, 0);
+                                filler(ls, q);
+                            }
+                        } else {
+                            // '%nn' ring tokens: compacted below by the whole warp
+                            const int jn = atomicAdd(&S.njobs[tid >> 5], 1);
+                            if (jn < CX_JOBS) {
+                                S.jobs[(tid >> 5) * CX_JOBS + jn] = make_int4(ls, q, tid, local);
+                            } else {
+                                cx_rare(S, &s_nrare, ls, q, RK_ARENA, tid, local, 0, 0);
+                                filler(ls, q);
                             }
                         }
-                        for (int j = w; j < q; ++j) {
-                            S.win[j] = 0x01;  // escape-only filler
-                            cx_set(S.fbits, j);
-                        }
-                        sub += 2 * (q - w);
-                        s_special = 1;
                     }
                     ls = q + 1;
                     ++local;
                     oid = 0xffffffffu;
-#pragma unroll
-                    for (int k = 0; k < 10; ++k) lc[k] = -1;
+                    lc0 = lc1 = lc2 = lc3 = -1;
                     n_pct = 0;
                     fail = false;
                     skip = ls <= end && cx_bit(S.ebits, ls);
                     continue;
                 }
-                if (skip || fail) continue;
+                if (job.timing == 4) continue;
                 const bool pct = c == '%';
-                const unsigned rid = pct ? (S.win[q + 1] - '0') * 10u + (S.win[q + 2] - '0') : c - '0';
+                const unsigned rid = pct ? (win[q + 1] - '0') * 10u + (win[q + 2] - '0') : c - '0';
                 n_pct += pct;
-                int slot = -1, free_slot = -1;
-#pragma unroll
-                for (int k = 3; k >= 0; --k) {
-                    const unsigned v = (oid >> (8 * k)) & 0xffu;
-                    if (v == rid) slot = k;
-                    if (v == 0xffu) free_slot = k;
-                }
+                const unsigned v0 = oid & 0xffu, v1 = (oid >> 8) & 0xffu, v2 = (oid >> 16) & 0xffu,
+                               v3 = oid >> 24;
+                const int slot = v0 == rid ? 0 : v1 == rid ? 1 : v2 == rid ? 2 : v3 == rid ? 3 : -1;
                 if (slot < 0) {
-                    if (free_slot < 0) {
-                        fail = true;
-                        continue;
-                    }
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (k == free_slot) opos[k] = q;
-                    oid = (oid & ~(0xffu << (8 * free_slot))) | (rid << (8 * free_slot));
+                    // opens a ring in the first free slot
+                    const int fs = v0 == 0xffu ? 0 : v1 == 0xffu ? 1 : v2 == 0xffu ? 2 : v3 == 0xffu ? 3 : -1;
+                    fail |= fs < 0;
+                    op0 = fs == 0 ? q : op0;
+                    op1 = fs == 1 ? q : op1;
+                    op2 = fs == 2 ? q : op2;
+                    op3 = fs == 3 ? q : op3;
+                    oid = fs < 0 ? oid : (oid & ~(0xffu << (8 * fs))) | (rid << (8 * fs));
                 } else {
-                    int o = 0;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (k == slot) o = opos[k];
+                    // closes the ring opened at o: the smallest colour not
+                    // closed inside (o, q)
+                    const int o = slot == 0 ? op0 : slot == 1 ? op1 : slot == 2 ? op2 : op3;
                     oid |= 0xffu << (8 * slot);
-                    // smallest colour not taken by a ring closed inside (o, q)
-                    int col = 10;
-#pragma unroll
-                    for (int k = 9; k >= 0; --k)
-                        if (lc[k] <= o) col = k;
-                    if (col == 10) {
-                        fail = true;
-                        continue;
+                    const int col = lc0 <= o ? 0 : lc1 <= o ? 1 : lc2 <= o ? 2 : lc3 <= o ? 3 : 4;
+                    const bool ok = col < 4 && S.explen['0' + col] != 0;
+                    fail |= !ok;
+                    if (ok && !fail && !skip) {
+                        lc0 = col == 0 ? q : lc0;
+                        lc1 = col == 1 ? q : lc1;
+                        lc2 = col == 2 ? q : lc2;
+                        lc3 = col == 3 ? q : lc3;
+                        S.win[o + (win[o] == '%')] = (uint8_t)('0' + col);
+                        S.win[q + pct] = (uint8_t)('0' + col);
                     }
-#pragma unroll
-                    for (int k = 0; k < 10; ++k)
-                        if (k == col) lc[k] = q;
-                    S.win[o + (S.win[o] == '%')] = (uint8_t)('0' + col);
-                    S.win[q + pct] = (uint8_t)('0' + col);
+                }
+            }
+            if (job.timing == 2) {  // debug: event statistics
+                const int wmax = __reduce_max_sync(0xffffffffu, n_ev);
+                const int wsum = __reduce_add_sync(0xffffffffu, n_ev);
+                const int wc = __reduce_add_sync(0xffffffffu, n_cmp);
+                if (lane == 0) {
+                    atomicAdd(&job.ctl->phase[3], (unsigned long long)wmax);
+                    atomicAdd(&job.ctl->phase[4], (unsigned long long)wsum);
+                    atomicAdd(&job.ctl->phase[5], (unsigned long long)wc);
+                }
+            }
+            // ---- '%nn' compaction, the whole warp per line: a ring '%nn'
+            // token keeps only its colour digit (at '%' + 1); the line's bytes
+            // shift left and the freed bytes before its '\n' become escape
+            // filler.  A byte that could be escaped in a shifted line (its
+            // literal is re-read from HBM by position) sends the line to the
+            // general routine instead.
+            __syncwarp();
+            const int nj = min(S.njobs[tid >> 5], CX_JOBS);
+            for (int j = 0; j < nj; ++j) {
+                const int4 J = S.jobs[(tid >> 5) * CX_JOBS + j];
+                const int jls = J.x, jq = J.y;
+                int kept = 0;
+                unsigned carry = 0;  // ring-'%' flags of the previous chunk's last two bytes
+                bool risk = false;
+                for (int c0b = jls; c0b < jq; c0b += 32) {
+                    const int r = c0b + lane;
+                    const bool valid = r < jq;
+                    const unsigned b = valid ? S.win[r] : 0u;
+                    const bool isp = valid && b == '%' && cx_bit(S.rbits, r);
+                    const unsigned M = __ballot_sync(0xffffffffu, isp);
+                    const unsigned M2 = (M << 2) | carry;
+                    const bool drop = isp || ((M2 >> lane) & 1u);
+                    const bool keep = valid && !drop;
+                    risk |= keep && (b >= 0x80u || !S.explen[b]);
+                    const unsigned K = __ballot_sync(0xffffffffu, keep);
+                    __syncwarp();
+                    if (keep) S.win[jls + kept + __popc(K & ((1u << lane) - 1u))] = (uint8_t)b;
+                    __syncwarp();
+                    kept += __popc(K);
+                    carry = M >> 30;
+                }
+                const int gap0 = jls + kept;
+                if (__any_sync(0xffffffffu, risk)) {
+                    if (lane == 0) cx_rare(S, &s_nrare, jls, jq, RK_ARENA, J.z, J.w, 0, 0);
+                    for (int r = jls + lane; r <= jq; r += 32) {
+                        S.win[r] = 0x01;
+                        cx_set(S.fbits, r);
+                    }
+                    if (lane == 0) atomicAdd(&S.lane_b[J.z], -2 * (jq - jls + 1));
+                } else {
+                    for (int r = gap0 + lane; r < jq; r += 32) {
+                        S.win[r] = 0x01;  // escape-only filler
+                        cx_set(S.fbits, r);
+                    }
+                    if (lane == 0) atomicAdd(&S.lane_b[J.z], -2 * (jq - gap0));
                 }
             }
         }
-        if (glob) cx_rare(S, &s_nrare, gpos, gpos, RK_ARENA, tid, 0, 0, 1);
-        // lane line bases (strict error ordinals)
+
+        pc.mark(job, 2);  // warp 0: pairing
+        // ---- P4: min-cost parse, right to left over the lane's range ----
+        // Branch-free: code slot 0 of every state is 0x20, so an escape
+        // decision writes the escape byte (its literal is re-read from HBM by
+        // the emit).  Whole 4-byte words inside the range are read and written
+        // with one 32-bit access each (the words at the range ends bytewise:
+        // they are shared with the neighbouring lanes).
+        unsigned acc = 0;
+        {
+            const uint16_t *__restrict__ dfa = S.dfa;
+            const uint32_t *__restrict__ t2 = S.t2;
+            const uint8_t *__restrict__ codes = S.codes;
+            uint8_t *win = S.win;
+            unsigned st = 0, wi = 0;
+            auto step = [&](unsigned b) -> unsigned {
+                const unsigned e = dfa[st * CX_NCOL + umin_(b - 10u, 118u)];
+                st = e & 0xffu;
+                const unsigned x = t2[wi * T2_MASKS + (e >> 8)];
+                wi = x & 0xfffu;
+                acc += x >> 16;
+                return codes[st * CX_CODES + ((x >> 12) & 15u)];
+            };
+            if (start <= end) {
+                const int lo_w = (start + 3) & ~3;  // first whole word inside the range
+                const int hi_w = (end + 1) & ~3;    // end of the last whole word (exclusive)
+                int i = end;
+                // right end, bytewise
+                for (; i >= max(hi_w, start); --i) win[i] = (uint8_t)step(win[i]);
+                // whole words
+                if (lo_w < hi_w) {
+                    unsigned *w32 = reinterpret_cast<unsigned *>(win);
+                    unsigned cur = w32[(hi_w >> 2) - 1];
+                    for (int wd = (hi_w >> 2) - 1; wd >= (lo_w >> 2); --wd) {
+                        const unsigned nxt = w32[wd - 1];  // prefetch (wd - 1 >= -1 words: slack before the window)
+                        unsigned d = step(cur >> 24) << 24;
+                        d |= step((cur >> 16) & 0xffu) << 16;
+                        d |= step((cur >> 8) & 0xffu) << 8;
+                        d |= step(cur & 0xffu);
+                        w32[wd] = d;
+                        cur = nxt;
+                    }
+                    i = lo_w - 1;
+                }
+                // left end, bytewise
+                for (; i >= start; --i) win[i] = (uint8_t)step(win[i]);
+            }
+        }
+        pc.mark(job, 3);  // warp 0: parse
+        __syncthreads();
+        pc.mark(job, 4);  // wait for the slowest warp
+        // lane line bases (strict error ordinals); lane output adjustments
         {
             int tot;
-            const int nl_mine = S.lane_b[tid];
-            const int base = block_exscan<int>(nl_mine, s_tmp, tot);
+            const int base = block_exscan_n<int, CX_NT>(nlines, s_tmp, tot);
             S.lane_c[tid] = base;
-            S.lane_b[tid] = 0;  // reused: lane output adjustments
             if (tid == 0) s_inl = (unsigned)tot;
         }
         __syncthreads();
         const int n_rare = min(s_nrare, CX_RARE);
         if (tid == 0 && s_nrare > CX_RARE) atomicOr(&job.ctl->overflow, 8ull);  // host: general kernel
-
-        // ---- rare lines: general routine, escape-only filler (one thread each) ----
+        // ---- rare lines: general routine (HBM arena), one thread each ----
         for (int r = tid; r < n_rare; r += CX_NT) {
             CxRare &R = S.rare[r];
-            int adj = 0;
             if (R.kind == RK_ARENA) {
                 long long ge = ws + R.le, gs = ws + R.ls;
                 if (R.glob) {
@@ -527,64 +755,27 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
                 } else {
                     if (kind == -3) atomicAdd(&s_flag, 1u);
                     R.aoff = aoff;
-                    adj += (int)cost + 1;
+                    atomicAdd(&S.lane_b[R.lane], (int)cost + 1);
                 }
             }
-            // the parse prices each filler byte at exactly 2 (an escape)
-            const int a = R.glob ? R.le : R.ls;
-            for (int j = a; j <= R.le; ++j) {
-                S.win[j] = 0x01;
-                cx_set(S.fbits, j);
-            }
-            if (R.kind == RK_ARENA) S.win[a] = 0x02;
-            adj -= 2 * (R.le - a + 1);
-            atomicAdd(&S.lane_b[R.lane], adj);
             if (R.kind == RK_DROP) atomicAdd(&s_skip, 1u);
             if (R.kind == RK_STRICT) atomicMin(&s_err_ord, S.lane_c[R.lane] + R.local);
         }
-        if (tid == 0 && n_rare) s_special = 1;
         __syncthreads();
-
-        // ---- P4: min-cost parse, right to left over the lane's range ----
-        unsigned acc = 0, nesc = 0;
-        {
-            const uint16_t *dfa = S.dfa;
-            const uint32_t *t2 = S.t2;
-            const uint8_t *codes = S.codes;
-            uint8_t *win = S.win;
-            unsigned st = 0, wi = 0;
-            for (int i = end; ZS_ANY(i >= start); --i) {
-                if (i < start) continue;
-                const unsigned b = win[i];
-                const unsigned e = dfa[st * CX_NCOL + umin_(b - 10u, 118u)];
-                st = e & 0xffu;
-                const unsigned x = t2[wi * T2_MASKS + (e >> 8)];
-                wi = x & 0xfffu;
-                const unsigned L = (x >> 12) & 15u;
-                acc += x >> 16;
-                if (L) {
-                    win[i] = codes[st * CX_CODES + L - 1];
-                } else {
-                    cx_set(S.ebits, i);
-                    ++nesc;
-                }
-            }
-        }
         const int nbytes = end >= start ? end - start + 1 : 0;
         const long long my_out = (long long)acc - 16ll * nbytes - sub + S.lane_b[tid];
-        if (__syncthreads_or(nesc != 0) && tid == 0) s_special = 1;
         // ---- P5: tile output bytes; publish ----
         unsigned long long tile_out;
-        const unsigned long long my_off = block_exscan<unsigned long long>((unsigned long long)my_out, s_tmp64, tile_out);
+        const unsigned long long my_off =
+            block_exscan_n<unsigned long long, CX_NT>((unsigned long long)my_out, s_tmp64, tile_out);
         const unsigned tile_lines = s_inl;
         if (tid == 0) lookback_publish(job.ts, t, tile_out, (unsigned long long)tile_lines);
         const bool staged = tile_out <= (unsigned long long)CX_OUTCAP;
-        const bool special = s_special != 0;
+        pc.mark(job, 5);  // output scan
         // ---- P6: emit (to staging now, or to HBM after the look-back) ----
         unsigned esc = 0;
         if (staged && start <= end)
-            esc = special ? cx_emit_range<true>(job, S, ws, start, end, S.out, my_off, n_rare)
-                          : cx_emit_range<false>(job, S, ws, start, end, S.out, my_off, n_rare);
+            esc = cx_emit_range<true>(job, S, ws, start, end, S.out, my_off, n_rare);
         if (tid < 32) {
             unsigned long long po, pl;
             lookback_resolve(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
@@ -594,11 +785,11 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
             }
         }
         __syncthreads();
+        pc.mark(job, 6);  // emit + look-back
         const unsigned long long pre_out = s_pre_out;
         const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
         if (!staged && fits && start <= end)
-            esc = special ? cx_emit_range<true>(job, S, ws, start, end, job.out, pre_out + my_off, n_rare)
-                          : cx_emit_range<false>(job, S, ws, start, end, job.out, pre_out + my_off, n_rare);
+            esc = cx_emit_range<false>(job, S, ws, start, end, job.out, pre_out + my_off, n_rare);
         if (esc) atomicAdd(&s_esc, esc);
         if (tid == 0) {
             atomicAdd(&job.ctl->total_out, tile_out);
@@ -646,7 +837,8 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
             atomicMin(&job.ctl->err_key, ((s_pre_lines + (unsigned long long)ord) << 24) |
                                              (unsigned long long)(t & 0xffffff));
         }
-        if (fits && staged) store_out(job.out + pre_out, S.out, (int)tile_out);
+        if (fits && staged) cx_store_out(job.out + pre_out, S.out, (int)tile_out);
+        pc.mark(job, 7);  // stats, store
     }
 }
 
