@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
         for (int k = threadIdx.x; k < 256; k += CX_NT) S.explen[k] = k == '\n' ? 1 : tb.exp_len[k];
         for (int k = threadIdx.x; k < 8 * 256; k += CX_NT) {
             const unsigned st = k >> 8, b = k & 255;
-            uint8_t e = tk_entry(st, b);
+            uint8_t e = tk_entry(st, b) & ~(TK_ENTER_BR | TK_ENTER_PCT);  // bits 5/6: line-end errors only
             if (b == '\n') {  // line end: back to TK_OUT0; flag an open bracket / a bad '%'
                 e = 128u;
                 if (job.preprocess && st == TK_IN) e |= 0x20u;
@@ -453,14 +453,23 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
         // ---- P2: tokenizer; CR / tokenize errors; ring-token bits ----
         // LUT entry: bits 0-2 next state, 3 ring token, 4 '\r', 7 line end;
         // a line end's bits 5/6 flag an unclosed '[' / a bad '%' (preprocess).
+        // The fast walk only ORs the flags together; a lane whose range holds
+        // a CR or a tokenize error walks it again with the per-line handling.
         // Ring-token bits gather in a register per 32-byte bitmap word.
         int nlines = glob ? 1 : 0;
         {
             const uint8_t *__restrict__ lut = S.lut;
             const unsigned *__restrict__ w32 = reinterpret_cast<const unsigned *>(S.win);
-            unsigned st = TK_OUT0, crs = 0, rmask = 0;
+            unsigned st = TK_OUT0, crs = 0, rmask = 0, flags = 0;
             int ls = first;
-            // one tokenizer step at window position p (byte b)
+            auto step_fast = [&](int p, unsigned b) {
+                const unsigned e = lut[(st << 8) | b];
+                rmask |= ((e >> 3) & 1u) << (p & 31);
+                flags |= e;
+                nlines += e >> 7;
+                st = e & 7u;
+            };
+            // one tokenizer step at window position p (byte b), per-line errors
             auto step = [&](int p, unsigned b) {
                 const unsigned e = lut[(st << 8) | b];
                 rmask |= ((e >> 3) & 1u) << (p & 31);
@@ -486,29 +495,37 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
                 if (rmask && job.preprocess) atomicOr(&S.rbits[p >> 5], rmask);
                 rmask = 0;
             };
-            if (first <= end) {
+            auto walk = [&](auto &&stepfn) {
                 int p = first;
                 // bytes up to a word boundary, then whole words, then the tail
                 const int w0 = (first + 3) & ~3, w1 = (end + 1) & ~3;
                 if (w0 < w1) {
-                    for (; p < w0; ++p) step(p, S.win[p]);
+                    for (; p < w0; ++p) stepfn(p, S.win[p]);
                     if (p > first && (p & 31) == 0) flush(p - 1);
                     unsigned cur = w32[p >> 2];
                     for (; p < w1; p += 4) {
                         const unsigned nxt = w32[(p >> 2) + 1];  // prefetch (the window has slack after it)
-                        step(p, cur & 0xffu);
-                        step(p + 1, (cur >> 8) & 0xffu);
-                        step(p + 2, (cur >> 16) & 0xffu);
-                        step(p + 3, cur >> 24);
+                        stepfn(p, cur & 0xffu);
+                        stepfn(p + 1, (cur >> 8) & 0xffu);
+                        stepfn(p + 2, (cur >> 16) & 0xffu);
+                        stepfn(p + 3, cur >> 24);
                         if (((p + 3) & 31) == 31) flush(p);
                         cur = nxt;
                     }
                 }
                 for (; p <= end; ++p) {
-                    step(p, S.win[p]);
+                    stepfn(p, S.win[p]);
                     if ((p & 31) == 31) flush(p);
                 }
                 flush(end);
+            };
+            if (first <= end) {
+                walk(step_fast);
+                if (flags & 0x70u) {  // a CR or a tokenize error in the range (rare)
+                    nlines = glob ? 1 : 0;
+                    st = TK_OUT0;
+                    walk(step);
+                }
             }
         }
         if (glob) {
