@@ -1,6 +1,6 @@
 // zs_cx.cuh -- lane-chunk compress kernel (the encode hot path).
 //
-// One persistent 512-thread CTA per SM takes 51,200-byte tiles in ticket
+// One persistent 768-thread CTA per SM takes 50,688-byte tiles in ticket
 // order.  A tile owns the lines whose terminating '\n' lies inside it (their
 // first bytes may sit in the 2 KB staged before the tile).  Every lane owns
 // a contiguous run of whole lines, ~100 bytes, cut at the newline nearest to
@@ -36,12 +36,12 @@
 
 namespace zs {
 
-constexpr int CX_NT = 1024;
+constexpr int CX_NT = 768;
 constexpr int CX_NW = CX_NT / 32;
-constexpr int CX_CC = 50;                         // bytes of line ends per lane
-constexpr int CX_TILE = CX_NT * CX_CC;            // 51200
+constexpr int CX_CC = 66;                         // bytes of line ends per lane (tile 50,688 B)
+constexpr int CX_TILE = CX_NT * CX_CC;
 constexpr int CX_HEAD = 2048;                     // staged before the tile
-constexpr int CX_WIN = CX_HEAD + CX_TILE;         // 53248 (multiple of 32)
+constexpr int CX_WIN = CX_HEAD + CX_TILE;         // multiple of 32 (bitmap words)
 constexpr int CX_WORDS = CX_WIN / 32 + 4;         // bitmap words (multiple of 4: keeps the carve 16-aligned)
 constexpr int CX_NCOL = 119;                      // dcol: umin(b - 10, 118); 0 = '\n'
 constexpr int CX_NLMASK = 15;                     // transducer mask slot of '\n'
