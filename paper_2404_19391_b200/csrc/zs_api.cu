@@ -13,6 +13,7 @@
 #include <set>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -553,7 +554,13 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
     CK(cudaSetDevice(ctx->dev));
     memset(res, 0, sizeof *res);
     const bool trailing = n == 0 || h_in[n - 1] == '\n';
-    const long long CH = 256ll << 20;
+    // newline-aligned chunks small enough that chunk k's D2H overlaps chunk
+    // k+1's H2D and kernel (ZS_CHUNK_MB overrides, for measurements)
+    static const long long CH = [] {
+        const char *e = getenv("ZS_CHUNK_MB");
+        const long long mb = e ? atoll(e) : 32;
+        return (mb > 0 ? mb : 32) << 20;
+    }();
     // chunk boundaries just past a newline
     std::vector<long long> cuts{0};
     while (cuts.back() < n) {
