@@ -67,7 +67,7 @@ struct CxRare {
 __host__ __device__ inline int cx_align16(int x) { return (x + 15) & ~15; }
 
 __host__ __device__ inline int cx_smem_bytes(int ns, int nw) {
-    return cx_align16(ns * CX_NCOL * 2) + nw * T2_MASKS * 4 + cx_align16(ns * CX_CODES) + 256 + 8 * 256 +
+    return cx_align16(ns * CX_NCOL * 2) + nw * T2_MASKS * 4 + cx_align16(ns * CX_CODES) +
            cx_align16(CX_WIN + 32) + 3 * CX_WORDS * 4 + CX_OUTCAP + CX_RARE * (int)sizeof(CxRare) +
            3 * CX_NT * 4 + CX_NW * CX_JOBS * 16 + CX_NW * 4;
 }
@@ -92,8 +92,6 @@ __device__ inline CxSmem cx_carve(uint8_t *p, int ns, int nw) {
     S.dfa = reinterpret_cast<uint16_t *>(p); p += cx_align16(ns * CX_NCOL * 2);
     S.t2 = reinterpret_cast<uint32_t *>(p); p += nw * T2_MASKS * 4;
     S.codes = p; p += cx_align16(ns * CX_CODES);
-    S.explen = p; p += 256;
-    S.lut = p; p += 8 * 256;
     S.win = p; p += cx_align16(CX_WIN + 32);
     S.rbits = reinterpret_cast<unsigned *>(p); p += CX_WORDS * 4;
     S.ebits = reinterpret_cast<unsigned *>(p); p += CX_WORDS * 4;
@@ -305,7 +303,11 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
     __shared__ unsigned s_esc, s_skip, s_flag, s_inl;
     __shared__ unsigned long long s_pre_out, s_pre_lines;
 
-    const CxSmem S = cx_carve(smem, cx_ns, cx_nw);
+    __shared__ __align__(16) uint8_t s_lut[8 * 256];  // tokenizer transducer (static: constant addresses)
+    __shared__ __align__(16) uint8_t s_explen[256];
+    CxSmem S = cx_carve(smem, cx_ns, cx_nw);
+    S.lut = s_lut;
+    S.explen = s_explen;
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(cx_dfa);
         uint4 *dst = reinterpret_cast<uint4 *>(S.dfa);
@@ -740,14 +742,6 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
         pc.mark(job, 3);  // warp 0: parse
         __syncthreads();
         pc.mark(job, 4);  // wait for the slowest warp
-        // lane line bases (strict error ordinals); lane output adjustments
-        {
-            int tot;
-            const int base = block_exscan_n<int, CX_NT>(nlines, s_tmp, tot);
-            S.lane_c[tid] = base;
-            if (tid == 0) s_inl = (unsigned)tot;
-        }
-        __syncthreads();
         const int n_rare = min(s_nrare, CX_RARE);
         if (tid == 0 && s_nrare > CX_RARE) atomicOr(&job.ctl->overflow, 8ull);  // host: general kernel
         // ---- rare lines: general routine (HBM arena), one thread each ----
@@ -776,16 +770,18 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
                 }
             }
             if (R.kind == RK_DROP) atomicAdd(&s_skip, 1u);
-            if (R.kind == RK_STRICT) atomicMin(&s_err_ord, S.lane_c[R.lane] + R.local);
+            if (R.kind == RK_STRICT) s_err_ord = 0;  // ordinal resolved after the scan
         }
         __syncthreads();
         const int nbytes = end >= start ? end - start + 1 : 0;
         const long long my_out = (long long)acc - 16ll * nbytes - sub + S.lane_b[tid];
-        // ---- P5: tile output bytes; publish ----
-        unsigned long long tile_out;
-        const unsigned long long my_off =
-            block_exscan_n<unsigned long long, CX_NT>((unsigned long long)my_out, s_tmp64, tile_out);
-        const unsigned tile_lines = s_inl;
+        // ---- P5: tile output bytes and lines (one scan); publish ----
+        unsigned long long tot;
+        const unsigned long long ex = block_exscan_n<unsigned long long, CX_NT>(
+            ((unsigned long long)my_out << 24) | (unsigned long long)nlines, s_tmp64, tot);
+        const unsigned long long my_off = ex >> 24, tile_out = tot >> 24;
+        const unsigned tile_lines = (unsigned)(tot & 0xffffffu);
+        S.lane_c[tid] = (int)(ex & 0xffffffu);  // lane line bases (strict error ordinals)
         if (tid == 0) lookback_publish(job.ts, t, tile_out, (unsigned long long)tile_lines);
         const bool staged = tile_out <= (unsigned long long)CX_OUTCAP;
         pc.mark(job, 5);  // output scan
@@ -818,12 +814,13 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
         }
         // ---- strict error: details of the tile's first bad line ----
         if (tid == 0 && s_err_ord != 0x7fffffff) {
-            const int ord = s_err_ord;
+            int ord = 0x7fffffff;
             long long gs = 0, ge = 0;
             int kind = E_NONE;
             for (int r = 0; r < n_rare; ++r) {
                 const CxRare &R = S.rare[r];
-                if (R.kind == RK_STRICT && S.lane_c[R.lane] + R.local == ord) {
+                if (R.kind == RK_STRICT && S.lane_c[R.lane] + R.local < ord) {
+                    ord = S.lane_c[R.lane] + R.local;
                     ge = ws + R.le;
                     gs = R.glob ? R.gs : ws + R.ls;
                     kind = R.err;
