@@ -394,11 +394,11 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
         const int grid = (int)std::min<long long>(nt, ctx->n_sm);
         if (timed) CK(cudaEventRecord(ctx->ev0, st));
         if (cx) {
-            const int smem = cx_smem_bytes(ctx->ht.n_states, ctx->ht.n_windows);
-            CK(set_smem(compress_cx, smem));
-            compress_cx<<<grid, CX_NT, smem, st>>>(job, ctx->tb, ctx->d_cxdfa.as<uint16_t>(),
-                                                   ctx->d_cxt2.as<uint32_t>(), ctx->d_cxcodes.as<uint8_t>(),
-                                                   ctx->ht.n_states, ctx->ht.n_windows);
+            const CxLayout L = cx_layout(ctx->ht.n_states, ctx->ht.n_windows);
+            CK(set_smem(compress_cx, L.bytes));
+            compress_cx<<<grid, CX_NT, L.bytes, st>>>(job, ctx->tb, ctx->d_cxdfa.as<uint16_t>(),
+                                                      ctx->d_cxt2.as<uint32_t>(), ctx->d_cxcodes.as<uint8_t>(),
+                                                      ctx->ht.n_states, ctx->ht.n_windows, L.o_t2, L.o_codes);
             ctx->last_kernel = "compress_cx";
         } else if (ip) {
             const int smem = ip_smem_bytes(ctx->tb.n_states, ctx->ht.n_windows);

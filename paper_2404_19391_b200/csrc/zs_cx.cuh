@@ -66,11 +66,37 @@ struct CxRare {
 
 __host__ __device__ inline int cx_align16(int x) { return (x + 15) & ~15; }
 
-__host__ __device__ inline int cx_smem_bytes(int ns, int nw) {
-    return cx_align16(ns * CX_NCOL * 2) + nw * T2_MASKS * 4 + cx_align16(ns * CX_CODES) +
-           cx_align16(CX_WIN + 32) + 3 * CX_WORDS * 4 + CX_OUTCAP + CX_RARE * (int)sizeof(CxRare) +
-           3 * CX_NT * 4 + CX_NW * CX_JOBS * 16 + CX_NW * 4;
+// Shared-memory layout: the fixed-size buffers first, at compile-time
+// offsets, then the dictionary tables (their sizes depend on the dictionary;
+// the host passes the table offsets as kernel parameters).  Constant offsets
+// keep the compiler from rebuilding buffer addresses inside the hot loops.
+constexpr int CX_O_WIN = 0;
+constexpr int CX_O_RB = CX_O_WIN + ((CX_WIN + 32 + 15) & ~15);
+constexpr int CX_O_EB = CX_O_RB + CX_WORDS * 4;
+constexpr int CX_O_FB = CX_O_EB + CX_WORDS * 4;
+constexpr int CX_O_OUT = CX_O_FB + CX_WORDS * 4;
+constexpr int CX_O_RARE = CX_O_OUT + CX_OUTCAP;
+constexpr int CX_O_LA = CX_O_RARE + CX_RARE * (int)sizeof(CxRare);
+constexpr int CX_O_LB = CX_O_LA + CX_NT * 4;
+constexpr int CX_O_LC = CX_O_LB + CX_NT * 4;
+constexpr int CX_O_JOBS = CX_O_LC + CX_NT * 4;
+constexpr int CX_O_NJOBS = CX_O_JOBS + CX_NW * CX_JOBS * 16;
+constexpr int CX_O_DFA = (CX_O_NJOBS + CX_NW * 4 + 15) & ~15;
+static_assert(CX_O_JOBS % 16 == 0, "int4 job slots");
+
+struct CxLayout {
+    int o_t2, o_codes, bytes;
+};
+
+__host__ __device__ inline CxLayout cx_layout(int ns, int nw) {
+    CxLayout L;
+    L.o_t2 = CX_O_DFA + cx_align16(ns * CX_NCOL * 2);
+    L.o_codes = L.o_t2 + nw * T2_MASKS * 4;
+    L.bytes = L.o_codes + cx_align16(ns * CX_CODES);
+    return L;
 }
+
+__host__ __device__ inline int cx_smem_bytes(int ns, int nw) { return cx_layout(ns, nw).bytes; }
 
 struct CxSmem {
     uint16_t *dfa;
@@ -87,22 +113,22 @@ struct CxSmem {
     int *njobs;   // [warp]
 };
 
-__device__ inline CxSmem cx_carve(uint8_t *p, int ns, int nw) {
+__device__ inline CxSmem cx_carve(uint8_t *p, int o_t2, int o_codes) {
     CxSmem S;
-    S.dfa = reinterpret_cast<uint16_t *>(p); p += cx_align16(ns * CX_NCOL * 2);
-    S.t2 = reinterpret_cast<uint32_t *>(p); p += nw * T2_MASKS * 4;
-    S.codes = p; p += cx_align16(ns * CX_CODES);
-    S.win = p; p += cx_align16(CX_WIN + 32);
-    S.rbits = reinterpret_cast<unsigned *>(p); p += CX_WORDS * 4;
-    S.ebits = reinterpret_cast<unsigned *>(p); p += CX_WORDS * 4;
-    S.fbits = reinterpret_cast<unsigned *>(p); p += CX_WORDS * 4;
-    S.out = p; p += CX_OUTCAP;
-    S.rare = reinterpret_cast<CxRare *>(p); p += CX_RARE * sizeof(CxRare);
-    S.lane_a = reinterpret_cast<int *>(p); p += CX_NT * 4;
-    S.lane_b = reinterpret_cast<int *>(p); p += CX_NT * 4;
-    S.lane_c = reinterpret_cast<int *>(p); p += CX_NT * 4;
-    S.jobs = reinterpret_cast<int4 *>(p); p += CX_NW * CX_JOBS * 16;
-    S.njobs = reinterpret_cast<int *>(p);
+    S.win = p + CX_O_WIN;
+    S.rbits = reinterpret_cast<unsigned *>(p + CX_O_RB);
+    S.ebits = reinterpret_cast<unsigned *>(p + CX_O_EB);
+    S.fbits = reinterpret_cast<unsigned *>(p + CX_O_FB);
+    S.out = p + CX_O_OUT;
+    S.rare = reinterpret_cast<CxRare *>(p + CX_O_RARE);
+    S.lane_a = reinterpret_cast<int *>(p + CX_O_LA);
+    S.lane_b = reinterpret_cast<int *>(p + CX_O_LB);
+    S.lane_c = reinterpret_cast<int *>(p + CX_O_LC);
+    S.jobs = reinterpret_cast<int4 *>(p + CX_O_JOBS);
+    S.njobs = reinterpret_cast<int *>(p + CX_O_NJOBS);
+    S.dfa = reinterpret_cast<uint16_t *>(p + CX_O_DFA);
+    S.t2 = reinterpret_cast<uint32_t *>(p + o_t2);
+    S.codes = p + o_codes;
     return S;
 }
 
@@ -294,7 +320,7 @@ __device__ __forceinline__ void cx_rare(const CxSmem &S, int *n, int ls, int le,
 
 __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, const uint16_t *cx_dfa,
                                                         const uint32_t *cx_t2, const uint8_t *cx_codes,
-                                                        int cx_ns, int cx_nw) {
+                                                        int cx_ns, int cx_nw, int o_t2, int o_codes) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int s_tmp[CX_NW];
     __shared__ unsigned long long s_tmp64[CX_NW];
@@ -305,7 +331,7 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
 
     __shared__ __align__(16) uint8_t s_lut[8 * 256];  // tokenizer transducer (static: constant addresses)
     __shared__ __align__(16) uint8_t s_explen[256];
-    CxSmem S = cx_carve(smem, cx_ns, cx_nw);
+    CxSmem S = cx_carve(smem, o_t2, o_codes);
     S.lut = s_lut;
     S.explen = s_explen;
     {
