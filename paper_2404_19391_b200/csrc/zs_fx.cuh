@@ -242,42 +242,41 @@ __global__ void __launch_bounds__(FX_NT) fx_count(Job job, const unsigned *ctab,
 // fx_scan: one CTA of 1024 threads, exclusive scan of the tile totals
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) fx_scan(Job job, FxScratch sc) {
+    // each thread owns a contiguous run of tiles: one pass of loads, one block scan
     __shared__ unsigned long long s_w[32];
-    __shared__ unsigned long long s_carry;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) s_carry = 0;
+    const long long nt = job.n_tiles;
+    const long long per = (nt + 1023) / 1024;
+    const long long t0 = min(nt, tid * per), t1 = min(nt, t0 + per);
+    unsigned long long sum = 0;
+    for (long long t = t0; t < t1; ++t) sum += sc.tsum[t];
+    unsigned long long x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[wid] = x;
     __syncthreads();
-    for (long long base = 0; base < job.n_tiles; base += 1024) {
-        const long long t = base + tid;
-        const unsigned long long v = t < job.n_tiles ? sc.tsum[t] : 0ull;
-        unsigned long long x = v;
+    if (wid == 0) {
+        unsigned long long w = s_w[lane];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
         }
-        if (lane == 31) s_w[wid] = x;
-        __syncthreads();
-        if (wid == 0) {
-            unsigned long long w = s_w[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= o) w += y;
-            }
-            s_w[lane] = w;
-        }
-        __syncthreads();
-        const unsigned long long carry = s_carry;
-        const unsigned long long ex = carry + (wid ? s_w[wid - 1] : 0ull) + x - v;
-        if (t < job.n_tiles) sc.toff[t] = ex;
-        __syncthreads();
-        if (tid == 0) s_carry = carry + s_w[31];
-        __syncthreads();
+        s_w[lane] = w;
+    }
+    __syncthreads();
+    unsigned long long run = (wid ? s_w[wid - 1] : 0ull) + x - sum;
+    for (long long t = t0; t < t1; ++t) {
+        sc.toff[t] = run;
+        run += sc.tsum[t];
     }
     if (tid == 0) {
-        job.ctl->total_out = s_carry;
-        if (s_carry > (unsigned long long)job.out_cap) atomicOr(&job.ctl->overflow, 1ull);
+        const unsigned long long total = s_w[31];
+        job.ctl->total_out = total;
+        if (total > (unsigned long long)job.out_cap) atomicOr(&job.ctl->overflow, 1ull);
     }
 }
 

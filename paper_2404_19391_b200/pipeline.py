@@ -88,28 +88,132 @@ def run_buffer(buf, d, direction="compress", *, preprocess=False, lenient=False,
     return out[:res.out_bytes], res
 
 
+SEGMENT_BYTES = 256 << 20
+
+
+def _read_seg(src, n):
+    parts, got = [], 0
+    while got < n:
+        chunk = src.read(n - got)
+        if not chunk:
+            break
+        parts.append(chunk)
+        got += len(chunk)
+    return b"".join(parts)
+
+
 def run_stream(src, dst, d, direction="compress", *, preprocess=False, lenient=False, workers=1,
-               batch_lines=BATCH_LINES, device=None) -> CorpusStats:
+               batch_lines=BATCH_LINES, device=None, segment_bytes=SEGMENT_BYTES) -> CorpusStats:
     """Stream src to dst through the GPU codec; returns exact corpus totals.
 
-    Strict mode raises LineError (1-based) for the first bad line; lenient
-    mode drops undecodable / carriage-return lines (``skipped``) and keeps
-    unpreprocessable ones raw (``flagged``)."""
+    The input is read in `segment_bytes` pieces cut at newlines, so files
+    larger than host or device memory stream through (each segment is one
+    zs_*_host call, itself pipelined in 32 MB chunks).  Output bytes equal the
+    reference's `b"\n".join(kept records) + ("\n" if kept and trailing)`
+    (pipeline.py:148-166) for any segment size: a segment's final '\n' is held
+    back until the next kept record or the end of the input.
+
+    Strict mode raises LineError (1-based) for the first bad line, after
+    writing every complete `batch_lines` batch before it like the reference
+    (pipeline.py:154-161); lenient mode drops undecodable / carriage-return
+    lines (``skipped``) and keeps unpreprocessable ones raw (``flagged``)."""
     if direction not in ("compress", "decompress"):
         raise ValueError(f"bad direction {direction!r}")
     t0 = time.perf_counter()
-    data = _read_all(src)
-    out, res = run_buffer(data, d, direction, preprocess=preprocess, lenient=lenient,
-                          device=device)
-    if res.err_line:
-        cause = from_kind(res.err_kind, res.err_offset, tuple(res.err_ids), res.err_code)
-        _write_partial(dst, data, d, direction, preprocess, lenient, res.err_line, batch_lines,
-                       device)
-        raise LineError(int(res.err_line), cause)
-    if out.size:
-        dst.write(out.tobytes())
-    st = CorpusStats(lines=res.lines, input_bytes=len(data), output_bytes=int(res.out_bytes),
-                     escapes=res.escapes, skipped=res.skipped, flagged=res.flagged)
+    bl = max(1, batch_lines)
+    st = CorpusStats()
+    line_base = 0        # input lines before the current segment (strict mode: = output records)
+    written = 0          # strict mode: output records written (a multiple of batch_lines)
+    pend = bytearray()   # strict mode: records of lines [written, line_base), '\n'-terminated
+    held_nl = False      # the written output's last '\n', held back until more output follows
+
+    def emit(body):
+        nonlocal held_nl
+        if held_nl:
+            dst.write(b"\n")
+            st.output_bytes += 1
+        dst.write(bytes(body))
+        st.output_bytes += len(body)
+        held_nl = False
+    carry = b""
+    last_byte = None
+    while True:
+        chunk = _read_seg(src, max(1, segment_bytes))
+        if chunk:
+            last_byte = chunk[-1]
+            buf = carry + chunk
+            cut = buf.rfind(b"\n") + 1
+            if cut == 0:
+                carry = buf
+                continue
+            seg, carry = buf[:cut], buf[cut:]
+        else:
+            seg, carry = carry, b""
+            if not seg:
+                break
+        final = not chunk
+        st.input_bytes += len(seg)
+        out, res = run_buffer(seg, d, direction, preprocess=preprocess, lenient=lenient,
+                              device=device)
+        if res.err_line:
+            gl = line_base + int(res.err_line)
+            cause = from_kind(res.err_kind, res.err_offset, tuple(res.err_ids), res.err_code)
+            keep = ((gl - 1) // bl) * bl
+            blob = bytearray()
+            if keep > written:
+                nrec = min(keep, line_base) - written
+                if nrec > 0:
+                    pos = 0
+                    for _ in range(nrec):
+                        pos = pend.index(10, pos) + 1
+                    blob += pend[:pos]
+                if keep > line_base:
+                    arr = np.frombuffer(seg, np.uint8)
+                    nl = np.flatnonzero(arr == 0x0A)
+                    end = int(nl[keep - line_base - 1]) + 1
+                    part, _ = run_buffer(arr[:end], d, direction, preprocess=preprocess,
+                                         lenient=lenient, device=device)
+                    blob += part.tobytes()
+            if blob.endswith(b"\n"):
+                blob = blob[:-1]
+            if blob:
+                emit(blob)
+            raise LineError(gl, cause)
+        st.lines += res.lines
+        st.escapes += res.escapes
+        st.skipped += res.skipped
+        st.flagged += res.flagged
+        ob = out.tobytes()
+        if lenient:
+            if ob:
+                nl_end = ob.endswith(b"\n")
+                emit(ob[:-1] if nl_end else ob)
+                held_nl = nl_end
+        else:
+            line_base += int(res.lines)
+            pend += ob
+            if not final or last_byte == 10:
+                # whole batches leave; the rest waits for the next segment
+                flush_to = (line_base // bl) * bl
+                if flush_to > written:
+                    pos = 0
+                    for _ in range(flush_to - written):
+                        pos = pend.index(10, pos) + 1
+                    emit(pend[:pos - 1])
+                    held_nl = True
+                    del pend[:pos]
+                    written = flush_to
+        if final:
+            break
+    tail = bytes(pend)  # strict mode: the records after the last whole batch
+    if tail.endswith(b"\n"):
+        emit(tail[:-1])
+        held_nl = True
+    elif tail:
+        emit(tail)
+    if held_nl and last_byte == 10:
+        dst.write(b"\n")
+        st.output_bytes += 1
     st.elapsed = time.perf_counter() - t0
     return st
 

@@ -426,3 +426,57 @@ def test_streaming_decode_edges():
     for bad in (comp + b"C ", comp[:5000] + b" \n" + comp[5000:], comp[:9000] + b"\x99" + comp[9000:]):
         _oracle_check(bad, d, False, True, "decompress")
         _oracle_check(bad, d, False, False, "decompress")
+
+
+@pytest.mark.parametrize("seg", [5, 97, 4096])
+def test_run_stream_segmented(stream_cases, seg):
+    """run_stream reading the input in small newline-cut segments gives the
+    same bytes, stats and errors as the whole-buffer call."""
+    dicts = [dict_from_json(dj) for dj in stream_cases["dicts"]]
+    for c in stream_cases["cases"][:300]:
+        kw = dict(preprocess=c["preprocess"], lenient=c["lenient"])
+        payload = bytes.fromhex(c["payload"])
+        if "err" in c:
+            with pytest.raises(z.LineError) as ei:
+                z.run_stream(io.BytesIO(payload), io.BytesIO(), dicts[c["dict"]], c["direction"],
+                             segment_bytes=seg, **kw)
+            assert ei.value.line_no == c["line_no"] and str(ei.value) == c["msg"]
+        else:
+            dst = io.BytesIO()
+            st = z.run_stream(io.BytesIO(payload), dst, dicts[c["dict"]], c["direction"],
+                              segment_bytes=seg, **kw)
+            assert dst.getvalue().hex() == c["out"], (seg, c)
+            assert (st.lines, st.input_bytes, st.output_bytes, st.escapes, st.skipped,
+                    st.flagged) == (c["lines"], c["in_bytes"], c["out_bytes"], c["escapes"],
+                                    c["skipped"], c["flagged"])
+
+
+def test_strict_partial_output_segmented():
+    d = z.Dictionary([], "smiles")
+    lines = [b"CCO"] * 300 + [b"C1CC"] + [b"CCO"] * 50
+    for seg in (3, 40, 100, 1000, 1 << 20):
+        for bl in (32, 7, 1000):
+            dst = io.BytesIO()
+            with pytest.raises(z.LineError) as ei:
+                z.run_stream(io.BytesIO(b"\n".join(lines) + b"\n"), dst, d, "compress",
+                             preprocess=True, batch_lines=bl, segment_bytes=seg)
+            assert ei.value.line_no == 301
+            keep = (300 // bl) * bl
+            assert dst.getvalue() == b"\n".join([b"CCO"] * keep), (seg, bl)
+
+
+def test_run_stream_segmented_corpus():
+    """A corpus through 1 MB segments == one whole-buffer call, both ways."""
+    d = z.default_dictionary()
+    buf = synth.generate("skewed", 20000, 2025).tobytes()
+    for tail in (b"", b"C1CC1"):
+        data = buf + tail
+        want, res = z.run_buffer(data, d, "compress", preprocess=True, lenient=True)
+        dst = io.BytesIO()
+        st = z.run_stream(io.BytesIO(data), dst, d, "compress", preprocess=True, lenient=True,
+                          segment_bytes=1 << 20)
+        assert dst.getvalue() == want.tobytes() and st.lines == res.lines
+        back = io.BytesIO()
+        z.run_stream(io.BytesIO(dst.getvalue()), back, d, "decompress", segment_bytes=300000)
+        want_back, _ = z.run_buffer(want.tobytes(), d, "decompress")
+        assert back.getvalue() == want_back.tobytes()
