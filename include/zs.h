@@ -104,6 +104,22 @@ int zs_build_tables_host(const int32_t *children, const int16_t *term_code, int3
  * t2 uint32[1024*16].  Returns 1 if built, 0 if the dictionary does not fit. */
 int zs_build_t2_host(const int32_t *children, const int16_t *term_code, int32_t n_nodes,
                      uint16_t *dfa2, uint32_t *t2, int32_t *n_windows, int32_t *n_masks);
+/* Random access (pkg/README.md:106-110: "grab line i,
+ * decode line i") into a compressed library resident in HBM.
+ * zs_index_build: d_offsets[r] = first byte of record r (records framed by
+ * '\n' as pipeline.py:49-74 splits them), d_offsets[*n_records] = one past
+ * the last record's end + 1; needs cap >= records + 1 (else ZS_E_CAPACITY
+ * with *n_records set).
+ * zs_decode_records: decodes the k records d_idx[] (device) into d_out,
+ * record j at d_out_off[j] (k + 1 offsets), with the reference's per-record
+ * outcome (numba_impl.py:74-139): d_status 0 ok, 1 unknown code, 2 dangling
+ * escape, 3 no such record; d_errpos = offset (| code << 40 for status 1).
+ * *total_out = output bytes (ZS_E_CAPACITY when out_cap is smaller). */
+int zs_index_build(zs_ctx *ctx, const uint8_t *d_comp, int64_t n, uint64_t *d_offsets, int64_t cap,
+                   int64_t *n_records);
+int zs_decode_records(zs_ctx *ctx, const uint8_t *d_comp, const uint64_t *d_offsets, int64_t n_records,
+                      const int64_t *d_idx, int64_t k, uint8_t *d_out, int64_t out_cap, int64_t *d_out_off,
+                      int8_t *d_status, int64_t *d_errpos, int64_t *total_out);
 /* debug/ablation kernel selection (default 3): bit 0 transducer parse, bit 1
  * in-place decisions (lane-chunk kernel), bit 2 warp-cooperative decompress
  * instead of the streaming one, bit 3 queue-based in-place compress kernel */

@@ -25,7 +25,7 @@ EXPORTS = (
     "zs_preprocess_batch", "zs_compress_device", "zs_decompress_device", "zs_compress_host",
     "zs_decompress_host", "zs_compress_bound", "zs_decompress_bound", "zs_last_kernel_ms",
     "zs_build_tables_host", "zs_set_phase_timing", "zs_last_phase_cycles", "zs_build_t2_host",
-    "zs_set_transducer", "zs_last_kernel", "zs_stream",
+    "zs_set_transducer", "zs_last_kernel", "zs_stream", "zs_index_build", "zs_decode_records",
 )
 
 
@@ -84,6 +84,9 @@ def load():
             "zs_last_phase_cycles": (ctypes.c_int, [P, P]),
             "zs_last_kernel": (ctypes.c_char_p, [P]),
             "zs_stream": (P, [P]),
+            "zs_index_build": (ctypes.c_int, [P, P, I64, P, I64, ctypes.POINTER(ctypes.c_int64)]),
+            "zs_decode_records": (ctypes.c_int, [P, P, P, I64, P, I64, P, I64, P, P, P,
+                                                 ctypes.POINTER(ctypes.c_int64)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

@@ -21,6 +21,7 @@
 #include "zs_kernels.cuh"
 #include "zs_fx.cuh"
 #include "zs_cx.cuh"
+#include "zs_ix.cuh"
 
 using namespace zs;
 
@@ -94,6 +95,7 @@ struct zs_ctx {
     // per-slot (double-buffered) work buffers
     DevBuf ctl[2], ts[2], terr[2], in[2], out[2], arena[2];  // arena: per slot
     DevBuf fxs[2];  // streaming-decode scratch per slot
+    DevBuf ixs;     // record-index scratch
     // shim scratch
     DevBuf s_flat, s_starts, s_out, s_lens, s_dec, s_stat, s_errpos, s_tot, s_ids, s_outst;
     Ctl *h_ctl = nullptr;  // pinned, 2 slots
@@ -716,7 +718,7 @@ int zs_ctx_destroy(zs_ctx *ctx) {
     if (!ctx) return ZS_OK;
     cudaSetDevice(ctx->dev);
     for (DevBuf *b : {&ctx->d_dfa2, &ctx->d_t2, &ctx->d_dfa, &ctx->d_codes, &ctx->d_children, &ctx->d_term, &ctx->d_explen,
-                      &ctx->d_expoff, &ctx->d_expflat, &ctx->d_fxc, &ctx->d_fxe, &ctx->d_cxdfa, &ctx->d_cxt2, &ctx->d_cxcodes, &ctx->fxs[0], &ctx->fxs[1], &ctx->ctl[0], &ctx->ctl[1], &ctx->ts[0],
+                      &ctx->d_expoff, &ctx->d_expflat, &ctx->d_fxc, &ctx->d_fxe, &ctx->d_cxdfa, &ctx->d_cxt2, &ctx->d_cxcodes, &ctx->fxs[0], &ctx->fxs[1], &ctx->ixs, &ctx->ctl[0], &ctx->ctl[1], &ctx->ts[0],
                       &ctx->ts[1], &ctx->terr[0], &ctx->terr[1], &ctx->in[0], &ctx->in[1],
                       &ctx->out[0], &ctx->out[1], &ctx->arena[0], &ctx->arena[1], &ctx->s_flat, &ctx->s_starts,
                       &ctx->s_out, &ctx->s_lens, &ctx->s_dec, &ctx->s_stat, &ctx->s_errpos,
@@ -890,6 +892,79 @@ int zs_build_tables_host(const int32_t *children, const int16_t *term_code, int3
     memcpy(dfa, ht.dfa.data(), (size_t)ht.n_states * NCOL * 2);
     memcpy(codes, ht.codes.data(), (size_t)ht.n_states * FAST_W);
     return 1;
+}
+
+int zs_index_build(zs_ctx *ctx, const uint8_t *d_comp, int64_t n, uint64_t *d_offsets, int64_t cap,
+                   int64_t *n_records) {
+    if (!ctx || n < 0 || (n > 0 && !d_comp) || !d_offsets || !n_records) return ZS_E_ARG;
+    CK(cudaSetDevice(ctx->dev));
+    cudaStream_t st = ctx->stream[0];
+    *n_records = 0;
+    if (n == 0) {
+        if (cap < 1) return ZS_E_CAPACITY;
+        CK(cudaMemsetAsync(d_offsets, 0, 8, st));
+        CK(cudaStreamSynchronize(st));
+        return ZS_OK;
+    }
+    const long long nt = (n + IX_TILE - 1) / IX_TILE;
+    if (ctx->ixs.reserve((size_t)nt * 12 + 64)) return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(index)");
+    unsigned *tcount = ctx->ixs.as<unsigned>();
+    unsigned long long *tbase = reinterpret_cast<unsigned long long *>(ctx->ixs.as<uint8_t>() + ((nt * 4 + 15) & ~15ll));
+    unsigned long long *tot = tbase + nt;
+    const int grid = (int)std::min<long long>(nt, (long long)ctx->n_sm * 8);
+    ix_count<<<grid, IX_NT, 0, st>>>(d_comp, n, nt, tcount);
+    ix_scan<unsigned><<<1, 1024, 0, st>>>(tcount, nt, tbase, tot);
+    CK(cudaGetLastError());
+    unsigned long long h_nl = 0;
+    uint8_t last = 0;
+    CK(cudaMemcpyAsync(&h_nl, tot, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&last, d_comp + n - 1, 1, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const long long recs = (long long)h_nl + (last != '\n' ? 1 : 0);
+    *n_records = recs;
+    if (cap < recs + 1) return ZS_E_CAPACITY;
+    ix_write<<<grid, IX_NT, 0, st>>>(d_comp, n, nt, tbase, reinterpret_cast<unsigned long long *>(d_offsets));
+    CK(cudaGetLastError());
+    if (last != '\n') {
+        const unsigned long long end = (unsigned long long)n + 1;
+        CK(cudaMemcpyAsync(d_offsets + recs, &end, 8, cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    return ZS_OK;
+}
+
+int zs_decode_records(zs_ctx *ctx, const uint8_t *d_comp, const uint64_t *d_offsets, int64_t n_records,
+                      const int64_t *d_idx, int64_t k, uint8_t *d_out, int64_t out_cap, int64_t *d_out_off,
+                      int8_t *d_status, int64_t *d_errpos, int64_t *total_out) {
+    if (!ctx || !d_comp || !d_offsets || n_records < 0 || k < 0 || (k > 0 && (!d_idx || !d_out_off || !d_status ||
+        !d_errpos)) || !total_out)
+        return ZS_E_ARG;
+    if (!ctx->have_dict) return ZS_E_NODICT;
+    CK(cudaSetDevice(ctx->dev));
+    cudaStream_t st = ctx->stream[0];
+    *total_out = 0;
+    if (k == 0) return ZS_OK;
+    if (ctx->ixs.reserve((size_t)k * 8 + 64)) return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(index)");
+    long long *len = ctx->ixs.as<long long>();
+    const int grid = (int)std::min<long long>((k + 255) / 256, (long long)ctx->n_sm * 8);
+    ix_sizes<<<grid, 256, 0, st>>>(d_comp, reinterpret_cast<const unsigned long long *>(d_offsets), n_records,
+                                   reinterpret_cast<const long long *>(d_idx), k, ctx->tb.exp_len, len, d_status,
+                                   reinterpret_cast<long long *>(d_errpos));
+    unsigned long long *off = reinterpret_cast<unsigned long long *>(d_out_off);
+    ix_scan<long long><<<1, 1024, 0, st>>>(len, k, off, off + k);
+    CK(cudaGetLastError());
+    unsigned long long h_tot = 0;
+    CK(cudaMemcpyAsync(&h_tot, off + k, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *total_out = (int64_t)h_tot;
+    if ((long long)h_tot > out_cap) return ZS_E_CAPACITY;
+    if (h_tot)
+        ix_fill<<<grid, 256, 0, st>>>(d_comp, reinterpret_cast<const unsigned long long *>(d_offsets),
+                                      reinterpret_cast<const long long *>(d_idx), k, d_status, off, ctx->tb.exp_len,
+                                      ctx->tb.exp_off, ctx->tb.exp_flat, d_out);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return ZS_OK;
 }
 
 int64_t zs_compress_bound(int64_t n) { return 2 * n + 64; }

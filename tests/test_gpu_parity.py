@@ -480,3 +480,38 @@ def test_run_stream_segmented_corpus():
         z.run_stream(io.BytesIO(dst.getvalue()), back, d, "decompress", segment_bytes=300000)
         want_back, _ = z.run_buffer(want.tobytes(), d, "decompress")
         assert back.getvalue() == want_back.tobytes()
+
+
+def test_record_index_random_access():
+    """RecordIndex (zs_index_build + zs_decode_records) == decoding the
+    whole stream, for random record sets, both framings, and the reference
+    decode errors for bad records."""
+    d = z.default_dictionary()
+    rng = random.Random(33)
+    buf = synth.generate("mixed", 30000, 5).tobytes()
+    comp, _ = z.run_buffer(buf, d, "compress", preprocess=True, lenient=True)
+    comp = comp.tobytes()
+    back, _ = z.run_buffer(comp, d, "decompress")
+    lines = back.tobytes().split(b"\n")[:-1]
+    for blob, want in ((comp, lines), (comp[:-1], lines), (b"\n" + comp, [b""] + lines)):
+        ix = z.RecordIndex(blob, d)
+        assert len(ix) == len(want)
+        sel = [rng.randrange(len(want)) for _ in range(5000)] + [0, len(want) - 1]
+        assert ix.decode(sel) == [want[i] for i in sel]
+        assert ix[len(want) // 2] == want[len(want) // 2]
+    # empty records, bad records
+    recs = comp.split(b"\n")[:-1]
+    recs[10] = b"\x05\x80"
+    recs[20] = b"CC "
+    recs[30] = b""
+    ix = z.RecordIndex(b"\n".join(recs) + b"\n", d)
+    assert ix[30] == b"" and ix[31] == lines[31]
+    with pytest.raises(z.UnknownCode) as e1:
+        ix.decode([5, 10])
+    assert (e1.value.code, e1.value.offset) == (5, 0)
+    with pytest.raises(z.TruncatedEscape) as e2:
+        ix.decode([20])
+    assert e2.value.offset == 2
+    with pytest.raises(IndexError):
+        ix.decode([len(ix)])
+    assert len(z.RecordIndex(b"", d)) == 0
