@@ -89,6 +89,7 @@ struct zs_ctx {
     int no_cx = 0;  // debug: force the queue-based compress kernel
     bool fx_ok = false;  // streaming decode kernel serves this dictionary (max expansion <= 7)
     int fx_blocks[2] = {0, 0};  // resident fx_count / fx_emit CTAs per SM
+    int fx_wide = -1;           // fx_blocks were sized for this emit variant
     int no_t2 = 0;  // debug: force the key-window DP
     int no_ip = 0;  // debug: force the decision-array kernel
     int dec_variant = 1;  // 1: per-thread slices (default), 0: warp-cooperative
@@ -421,18 +422,22 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
             if (ctx->fxs[slot].reserve(fx_scratch_bytes(nt)))
                 return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(fx scratch)");
             const FxScratch sc = fx_carve(ctx->fxs[slot].p, nt);
+            const bool wide = ctx->tb.max_exp > 7;
             auto kc = al ? fx_count<true> : fx_count<false>;
-            auto ke = al ? fx_emit<true> : fx_emit<false>;
+            auto ke = wide ? (al ? fx_emit<true, true> : fx_emit<false, true>)
+                           : (al ? fx_emit<true, false> : fx_emit<false, false>);
+            const int esm = fx_emit_smem(wide);
             CK(set_smem(kc, FX_CNT_SMEM));
-            CK(set_smem(ke, FX_EMIT_SMEM));
-            if (!ctx->fx_blocks[0]) {
+            CK(set_smem(ke, esm));
+            if (!ctx->fx_blocks[0] || ctx->fx_wide != (int)wide) {
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->fx_blocks[0], kc, FX_NT, FX_CNT_SMEM));
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->fx_blocks[1], ke, FX_NT, FX_EMIT_SMEM));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->fx_blocks[1], ke, FX_NT, esm));
+                ctx->fx_wide = (int)wide;
             }
             auto grid_of = [&](int b) { return (int)std::min<long long>(nt, (long long)ctx->n_sm * std::max(1, b)); };
             kc<<<grid_of(ctx->fx_blocks[0]), FX_NT, FX_CNT_SMEM, st>>>(job, ctx->d_fxc.as<unsigned>(), sc);
             fx_scan<<<1, 1024, 0, st>>>(job, sc);
-            ke<<<grid_of(ctx->fx_blocks[1]), FX_NT, FX_EMIT_SMEM, st>>>(job, ctx->d_fxe.as<unsigned long long>(), sc);
+            ke<<<grid_of(ctx->fx_blocks[1]), FX_NT, esm, st>>>(job, ctx->d_fxe.as<unsigned long long>(), sc);
             ctx->last_kernel = "fx_count+fx_scan+fx_emit";
         } else {
             const int smem = bp_smem_bytes(ctx->tb.n_flat);
@@ -812,10 +817,14 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
     }
     {
         unsigned fxc[256];
-        unsigned long long fxe[256];
+        unsigned long long fxe[512];
+        int mx = 0;
+        for (int b = 0; b < 256; ++b) mx = std::max<int>(mx, ht.exp_len[b]);
+        const bool wide = mx > 7;
         for (int b = 0; b < 256; ++b) {
             fxc[b] = fx_count_entry(b, ht.exp_len);
-            fxe[b] = fx_emit_entry(b, ht.exp_len, ht.exp_off, ht.exp_flat.data());
+            fxe[b] = fx_emit_entry(b, ht.exp_len, ht.exp_off, ht.exp_flat.data(), wide, 0);
+            fxe[256 + b] = fx_emit_entry(b, ht.exp_len, ht.exp_off, ht.exp_flat.data(), wide, 1);
         }
         CK(up(ctx->d_fxc, fxc, sizeof fxc));
         CK(up(ctx->d_fxe, fxe, sizeof fxe));
@@ -838,7 +847,7 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
     tb.n_flat = (int)exp_off[256];
     tb.max_exp = 0;
     for (int b = 0; b < 256; ++b) tb.max_exp = std::max<int>(tb.max_exp, ht.exp_len[b]);
-    ctx->fx_ok = tb.max_exp <= 7;
+    ctx->fx_ok = tb.max_exp <= 15;
     ctx->fast_w = 0;
     if (ht.fast) {
         const int L = std::max(1, ht.max_len);

@@ -21,9 +21,11 @@
 //
 // Tables (built on the host from the reference decode tables,
 // dictionary.py:112-129), replicated per bank so lookups never conflict:
-//   count: u32 [code][32 lanes] = len | invalid << 8 | mark << 16 | nl << 24
+//   count: u32 [code][32 lanes] = len | invalid << 10 | mark << 16 | nl << 22
 //   emit : u64 [code][16 lanes] = expansion bytes 0-6 | (8 * len) << 56
-// Serves dictionaries whose longest expansion is <= 7 bytes (default: 6).
+//          (WIDE, longest expansion 8..15: a second table, bytes 0-7 in the
+//          first and bytes 8-14 | (8 * len) << 56 in the second)
+// Serves dictionaries whose longest expansion is <= 15 bytes (default: 6).
 #pragma once
 #include "zs_device.cuh"
 
@@ -34,7 +36,8 @@ constexpr int FX_B = 32;                 // compressed bytes per thread per tile
 constexpr int FX_TILE = FX_NT * FX_B;    // 8 KB of compressed input per tile
 constexpr int FX_STAGE = 24576;          // emit staging bytes (tile output + 16 alignment)
 constexpr int FX_CNT_SMEM = 0;   // static shared only
-constexpr int FX_EMIT_SMEM = FX_STAGE;  // dynamic: the staging tile
+constexpr int FX_ETAB = 256 * 16 * 8;  // one replicated emit table
+__host__ __device__ constexpr int fx_emit_smem(bool wide) { return (wide ? 2 : 1) * FX_ETAB + FX_STAGE; }
 constexpr unsigned long long FX_BYTES = (1ull << 56) - 1;
 
 // per-slot scratch layout (device): tile totals, tile offsets, tile flags,
@@ -43,11 +46,11 @@ struct FxScratch {
     unsigned *tsum;            // [n_tiles] output bytes of the tile
     unsigned long long *toff;  // [n_tiles] exclusive prefix
     uint8_t *tflag;            // [n_tiles] bit 0: escapes in the tile
-    uint16_t *off16;           // [n_tiles * FX_NT]
+    unsigned *off32;           // [n_tiles * FX_NT]
 };
 
 inline size_t fx_scratch_bytes(long long nt) {
-    return (size_t)nt * (4 + 8 + 1 + 2 * FX_NT) + 64;
+    return (size_t)nt * (4 + 8 + 1 + 4 * FX_NT) + 64;
 }
 
 inline FxScratch fx_carve(void *p, long long nt) {
@@ -55,24 +58,33 @@ inline FxScratch fx_carve(void *p, long long nt) {
     uint8_t *q = reinterpret_cast<uint8_t *>(p);
     s.toff = reinterpret_cast<unsigned long long *>(q); q += 8 * nt;
     s.tsum = reinterpret_cast<unsigned *>(q); q += 4 * nt;
-    s.off16 = reinterpret_cast<uint16_t *>(q); q += 2 * nt * FX_NT;
+    s.off32 = reinterpret_cast<unsigned *>(q); q += 4 * nt * FX_NT;
     s.tflag = q;
     return s;
 }
 
 // host: table entries per code (a '\n' is a 1-byte code of itself)
 inline unsigned fx_count_entry(int b, const uint8_t *exp_len) {
-    if (b == '\n') return 1u | (1u << 24);
+    if (b == '\n') return 1u | (1u << 22);
     if (b == 0x20) return 1u << 16;
-    return exp_len[b] ? (unsigned)exp_len[b] : (1u << 8);
+    return exp_len[b] ? (unsigned)exp_len[b] : (1u << 10);
 }
+// narrow entry (longest expansion <= 7), or the two WIDE entries (<= 15)
 inline unsigned long long fx_emit_entry(int b, const uint8_t *exp_len, const uint16_t *exp_off,
-                                        const uint8_t *exp_flat) {
-    if (b == '\n') return (unsigned long long)'\n' | (8ull << 56);
-    const int L = exp_len[b];
+                                        const uint8_t *exp_flat, bool wide = false, int part = 0) {
+    const int L = b == '\n' ? 1 : exp_len[b];
     if (b == 0x20 || L == 0) return 0;
-    unsigned long long e = (unsigned long long)(8 * L) << 56;
-    for (int k = 0; k < L && k < 7; ++k) e |= (unsigned long long)exp_flat[exp_off[b] + k] << (8 * k);
+    auto byte = [&](int k) -> unsigned long long { return b == '\n' ? '\n' : exp_flat[exp_off[b] + k]; };
+    unsigned long long e = 0;
+    if (!wide) {
+        e = (unsigned long long)(8 * L) << 56;
+        for (int k = 0; k < L && k < 7; ++k) e |= byte(k) << (8 * k);
+    } else if (part == 0) {
+        for (int k = 0; k < L && k < 8; ++k) e |= byte(k) << (8 * k);
+    } else {
+        e = (unsigned long long)(8 * L) << 56;
+        for (int k = 8; k < L && k < 15; ++k) e |= byte(k) << (8 * (k - 8));
+    }
     return e;
 }
 
@@ -190,8 +202,8 @@ __global__ void __launch_bounds__(FX_NT) fx_count(Job job, const unsigned *ctab,
         fx_load<ALIGNED>(job.in, c0, cnt, va, vb);
         const unsigned acc = cnt == FX_B ? fx_count_slice<true>(s_tab, lane, va, vb, cnt)
                                          : fx_count_slice<false>(s_tab, lane, va, vb, cnt);
-        unsigned sum = acc & 0xffu, bad = (acc >> 8) & 0xffu, marks = (acc >> 16) & 0xffu;
-        unsigned nl = acc >> 24, nesc = 0;
+        unsigned sum = acc & 0x3ffu, bad = (acc >> 10) & 0x3fu, marks = (acc >> 16) & 0x3fu;
+        unsigned nl = (acc >> 22) & 0x3fu, nesc = 0;
         // escapes: the byte before the slice, or marks inside it -> exact walk
         const unsigned prev = __shfl_up_sync(0xffffffffu, vb.w >> 24, 1);
         unsigned esc0 = 0;
@@ -215,7 +227,7 @@ __global__ void __launch_bounds__(FX_NT) fx_count(Job job, const unsigned *ctab,
         my_esc += nesc;
         unsigned long long tot;
         const unsigned long long off = block_exscan_n<unsigned long long, FX_NT>(sum, s_tmp64, tot);
-        sc.off16[t * FX_NT + tid] = (uint16_t)off;
+        sc.off32[t * FX_NT + tid] = (unsigned)off;
         if (tid == 0) {
             sc.tsum[t] = (unsigned)tot;
             sc.tflag[t] = (uint8_t)(s_flag | (tot + 16 > (unsigned long long)FX_STAGE ? 2u : 0u));
@@ -312,6 +324,22 @@ struct FxAcc {
         lo = f ? spill : lo;
         sh -= f ? 64u : 0u;
     }
+    // up to 8 bytes (len8 <= 64); a full 8-byte word is legal, so the spill
+    // must be 0 when nothing was pending
+    __device__ __forceinline__ void put8(unsigned long long x, unsigned len8) {
+        const unsigned long long spill = sh ? x >> (64u - sh) : 0ull;
+        lo |= x << sh;
+        sh += len8;
+        const bool f = sh >= 64u;
+        if (f) {
+            if (first) red_or64(a, lo);
+            else sts64(a, lo);
+        }
+        first = first && !f;
+        a += f ? 8u : 0u;
+        lo = f ? spill : lo;
+        sh -= f ? 64u : 0u;
+    }
     __device__ __forceinline__ void finish() {
         if (sh) red_or64(a, lo);
     }
@@ -339,11 +367,15 @@ __device__ __forceinline__ void fx_emit_clean(FxAcc &acc, const unsigned long lo
     }
 }
 
-template <bool ALIGNED>
+template <bool ALIGNED, bool WIDE>
 __global__ void __launch_bounds__(FX_NT) fx_emit(Job job, const unsigned long long *etab, FxScratch sc) {
-    __shared__ unsigned long long s_tab[256][16];  // replicated per half-warp lane
-    extern __shared__ __align__(16) uint8_t stage[];  // FX_STAGE bytes
+    extern __shared__ __align__(16) uint8_t fsm[];  // emit table(s), then the staging tile
+    auto s_tab = reinterpret_cast<unsigned long long (*)[16]>(fsm);        // replicated per half-warp lane
+    auto s_tabh = reinterpret_cast<unsigned long long (*)[16]>(fsm + FX_ETAB);  // WIDE: bytes 8-14 | len
+    uint8_t *stage = fsm + (WIDE ? 2 : 1) * FX_ETAB;
     for (int k = threadIdx.x; k < 256 * 16; k += FX_NT) s_tab[k >> 4][k & 15] = etab[k >> 4];
+    if (WIDE)
+        for (int k = threadIdx.x; k < 256 * 16; k += FX_NT) s_tabh[k >> 4][k & 15] = etab[256 + (k >> 4)];
     const int tid = threadIdx.x, lane = tid & 31;
     const unsigned a_stage = sa(stage);
     const bool ends_nl = job.n > 0 && job.in[job.n - 1] == '\n';
@@ -367,7 +399,7 @@ __global__ void __launch_bounds__(FX_NT) fx_emit(Job job, const unsigned long lo
         const unsigned long long tbase = sc.toff[t];
         const unsigned tsum = sc.tsum[t];
         const unsigned flag = sc.tflag[t];
-        const unsigned my_off = sc.off16[t * FX_NT + tid];
+        const unsigned my_off = sc.off32[t * FX_NT + tid];
         const bool eof_nl = cnt > 0 && c0 + cnt == job.n && !ends_nl;
         if (tsum == 0) continue;
         const bool staged = !(flag & 2u);
@@ -389,7 +421,22 @@ __global__ void __launch_bounds__(FX_NT) fx_emit(Job job, const unsigned long lo
             if (staged) {
                 const unsigned o = (unsigned)shift + my_off;
                 FxAcc acc{0ull, 8u * (o & 7u), a_stage + (o & ~7u), true};
-                if (!(flag & 1u)) {
+                if (WIDE) {
+                    for (int k = 0; k < cnt; ++k) {
+                        const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
+                        if (esc) {
+                            acc.put8(b, 8u);
+                            esc = 0;
+                        } else if ((flag & 1u) && b == 0x20) {
+                            esc = 1;
+                        } else {
+                            const unsigned long long e0 = s_tab[b][lane & 15], e1 = s_tabh[b][lane & 15];
+                            const unsigned len8 = (unsigned)(e1 >> 56);
+                            acc.put8(e0, min(len8, 64u));
+                            if (len8 > 64u) acc.put8(e1 & FX_BYTES, len8 - 64u);
+                        }
+                    }
+                } else if (!(flag & 1u)) {
                     if (cnt == FX_B) fx_emit_clean<true>(acc, s_tab, lane, va, vb, cnt);
                     else fx_emit_clean<false>(acc, s_tab, lane, va, vb, cnt);
                 } else {
@@ -419,6 +466,11 @@ __global__ void __launch_bounds__(FX_NT) fx_emit(Job job, const unsigned long lo
                         esc = 0;
                     } else if (b == 0x20) {
                         esc = 1;
+                    } else if (WIDE) {
+                        const unsigned long long e1 = s_tabh[b][lane & 15];
+                        const unsigned L = (unsigned)(e1 >> 56) >> 3;
+                        for (unsigned j = 0; j < L; ++j) o[j] = (uint8_t)((j < 8 ? e : e1) >> (8 * (j & 7)));
+                        o += L;
                     } else {
                         const unsigned L = (unsigned)(e >> 56) >> 3;
                         for (unsigned j = 0; j < L; ++j) o[j] = (uint8_t)(e >> (8 * j));
