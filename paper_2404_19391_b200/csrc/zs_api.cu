@@ -63,6 +63,8 @@ struct HostTables {
     std::vector<uint32_t> t2;
     // lane-chunk compress kernel tables (zs_cx.cuh): '\n' column + transducer slot
     bool cx_ok = false;
+    int cx_states = 0, cx_cols = 0;  // minimised DFA: states x byte-class columns
+    std::vector<uint8_t> cx_cmap;     // byte -> column
     std::vector<uint16_t> cx_dfa;
     std::vector<uint32_t> cx_t2;
     std::vector<uint8_t> cx_codes;
@@ -85,7 +87,7 @@ struct zs_ctx {
     HostTables ht;
     Tables tb{};
     int fast_w = 0;
-    DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2, d_fxc, d_fxe, d_cxdfa, d_cxt2, d_cxcodes;
+    DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2, d_fxc, d_fxe, d_cxdfa, d_cxt2, d_cxcodes, d_cxcmap;
     int no_cx = 0;  // debug: force the queue-based compress kernel
     bool fx_ok = false;  // streaming decode kernel serves this dictionary (max expansion <= 7)
     int fx_blocks[2] = {0, 0};  // resident fx_count / fx_emit CTAs per SM
@@ -302,32 +304,96 @@ bool build_t2(HostTables &ht, int W) {
 bool build_cx(HostTables &ht, int max_len) {
     if (!ht.t2_ok || ht.n_masks > CX_NLMASK || max_len > 8) return false;
     const int ns = ht.n_states, nw = ht.n_windows;
-    if (cx_smem_bytes(ns, nw) > 227 * 1024) return false;
-    ht.cx_dfa.assign((size_t)cx_align16(ns * CX_NCOL * 2) / 2, 0);
+    // byte-level machine: next state and (target) mask index per byte; '\n'
+    // gets its own column (back to the root with the reserved mask slot)
+    auto col_of = [](int b) { return (b >= 0x20 && b <= 0x7f) ? b - 0x20 : 96; };
+    std::vector<int> nxt((size_t)ns * 256), mk(ns, 0);
     for (int st = 0; st < ns; ++st)
-        for (int c = 0; c < CX_NCOL; ++c) {
+        for (int b = 0; b < 256; ++b) {
+            const uint16_t e = ht.dfa2[(size_t)st * NCOL + col_of(b)];
+            nxt[(size_t)st * 256 + b] = e & 0xff;
+            mk[e & 0xff] = e >> 8;  // the mask index belongs to the target state
+        }
+    // Moore minimisation.  A state's output is its match-mask index and its
+    // codes for lengths 2..8; the length-1 code is the byte itself (identity
+    // codes map a byte to itself), so the states reached by identity-only
+    // bytes merge.
+    std::vector<int> cls(ns), tmp(ns);
+    {
+        std::map<std::vector<int>, int> ids;
+        for (int st = 0; st < ns; ++st) {
+            std::vector<int> key{mk[st]};
+            for (int L = 2; L <= FAST_W; ++L) key.push_back(ht.codes[(size_t)st * FAST_W + L - 1]);
+            cls[st] = ids.emplace(key, (int)ids.size()).first->second;
+        }
+    }
+    for (int nc = -1;;) {
+        std::map<std::vector<int>, int> ids;
+        for (int st = 0; st < ns; ++st) {
+            std::vector<int> key{cls[st]};
+            for (int b = 0; b < 256; ++b)
+                if (b != '\n') key.push_back(cls[nxt[(size_t)st * 256 + b]]);
+            tmp[st] = ids.emplace(key, (int)ids.size()).first->second;
+        }
+        cls = tmp;
+        if ((int)ids.size() == nc) break;
+        nc = (int)ids.size();
+    }
+    // renumber so the root is state 0
+    std::vector<int> ren(ns, -1);
+    int S = 0;
+    ren[cls[0]] = S++;
+    for (int st = 0; st < ns; ++st)
+        if (ren[cls[st]] < 0) ren[cls[st]] = S++;
+    std::vector<int> rep(S, -1);  // a representative original state per class
+    for (int st = 0; st < ns; ++st)
+        if (rep[ren[cls[st]]] < 0) rep[ren[cls[st]]] = st;
+    // byte columns: bytes with identical transitions from every state
+    std::map<std::vector<int>, int> cols;
+    std::vector<int> cmap(256);
+    cols[std::vector<int>{-1}] = 0;  // column 0: '\n'
+    for (int b = 0; b < 256; ++b) {
+        if (b == '\n') {
+            cmap[b] = 0;
+            continue;
+        }
+        std::vector<int> key;
+        for (int q = 0; q < S; ++q) key.push_back(ren[cls[nxt[(size_t)rep[q] * 256 + b]]]);
+        cmap[b] = cols.emplace(key, (int)cols.size()).first->second;
+    }
+    const int nc = (int)cols.size();
+    if (S > 256 || nc > 255 || cx_smem_bytes(S, nw, nc) > 227 * 1024) return false;
+    ht.cx_states = S;
+    ht.cx_cols = nc;
+    ht.cx_cmap.assign(cmap.begin(), cmap.end());
+    ht.cx_dfa.assign((size_t)cx_align16(S * nc * 2) / 2, 0);
+    for (int q = 0; q < S; ++q)
+        for (int b = 0; b < 256; ++b) {
             uint16_t e;
-            if (c == 0) {
+            if (b == '\n') {
                 e = (uint16_t)(0 | (CX_NLMASK << 8));
             } else {
-                const int b = c + 10;
-                const int old = (c < 118 && b >= 0x20 && b <= 0x7f) ? b - 0x20 : 96;
-                e = ht.dfa2[(size_t)st * NCOL + old];
+                const int t = nxt[(size_t)rep[q] * 256 + b];
+                e = (uint16_t)(ren[cls[t]] | (mk[t] << 8));
             }
-            ht.cx_dfa[(size_t)st * CX_NCOL + c] = e;
+            ht.cx_dfa[(size_t)q * nc + cmap[b]] = e;
         }
     ht.cx_t2 = ht.t2;
     for (int w = 0; w < nw; ++w)
         ht.cx_t2[(size_t)w * T2_MASKS + CX_NLMASK] = 0u | (9u << 12) | ((1u + 16u) << 16);
-    // code slot L: 0 = escape (0x20, never a code), 1..8 = the match of length L, 9 = '\n'
-    ht.cx_codes.assign((size_t)cx_align16(ns * CX_CODES), 0);
-    for (int st = 0; st < ns; ++st) {
-        ht.cx_codes[(size_t)st * CX_CODES] = 0x20;
-        for (int L = 1; L <= FAST_W; ++L)
-            ht.cx_codes[(size_t)st * CX_CODES + L] = ht.codes[(size_t)st * FAST_W + L - 1];
-        ht.cx_codes[(size_t)st * CX_CODES + 9] = '\n';
+    // code slot L: 0 = escape (0x20, never a code), 2..8 = the match of length L,
+    // 9 = '\n'; length 1 is the byte itself
+    ht.cx_codes.assign((size_t)cx_align16(S * CX_CODES), 0);
+    for (int q = 0; q < S; ++q) {
+        ht.cx_codes[(size_t)q * CX_CODES] = 0x20;
+        for (int L = 2; L <= FAST_W; ++L)
+            ht.cx_codes[(size_t)q * CX_CODES + L] = ht.codes[(size_t)rep[q] * FAST_W + L - 1];
+        ht.cx_codes[(size_t)q * CX_CODES + 9] = '\n';
     }
     ht.cx_ok = true;
+    if (getenv("ZS_VERBOSE"))
+        fprintf(stderr, "zs: cx tables: %d -> %d states, %d byte columns, %d windows, %d masks, smem %d B\n", ns, S,
+                nc, nw, ht.n_masks, cx_smem_bytes(S, nw, nc));
     return true;
 }
 
@@ -397,11 +463,13 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
         const int grid = (int)std::min<long long>(nt, ctx->n_sm);
         if (timed) CK(cudaEventRecord(ctx->ev0, st));
         if (cx) {
-            const CxLayout L = cx_layout(ctx->ht.n_states, ctx->ht.n_windows);
+            const CxLayout L = cx_layout(ctx->ht.cx_states, ctx->ht.n_windows, ctx->ht.cx_cols);
             CK(set_smem(compress_cx, L.bytes));
-            compress_cx<<<grid, CX_NT, L.bytes, st>>>(job, ctx->tb, ctx->d_cxdfa.as<uint16_t>(),
-                                                      ctx->d_cxt2.as<uint32_t>(), ctx->d_cxcodes.as<uint8_t>(),
-                                                      ctx->ht.n_states, ctx->ht.n_windows, L.o_t2, L.o_codes);
+            CxTables ct{ctx->d_cxdfa.as<uint16_t>(), ctx->d_cxt2.as<uint32_t>(), ctx->d_cxcodes.as<uint8_t>(),
+                        ctx->d_cxcmap.as<uint8_t>(), ctx->ht.cx_states, ctx->ht.n_windows, ctx->ht.cx_cols,
+                        L.o_t2, L.o_codes};
+            const int g2 = (int)std::min<long long>(nt, (long long)ctx->n_sm * CX_CTAS);
+            compress_cx<<<g2, CX_NT, L.bytes, st>>>(job, ctx->tb, ct);
             ctx->last_kernel = "compress_cx";
         } else if (ip) {
             const int smem = ip_smem_bytes(ctx->tb.n_states, ctx->ht.n_windows);
@@ -723,7 +791,7 @@ int zs_ctx_destroy(zs_ctx *ctx) {
     if (!ctx) return ZS_OK;
     cudaSetDevice(ctx->dev);
     for (DevBuf *b : {&ctx->d_dfa2, &ctx->d_t2, &ctx->d_dfa, &ctx->d_codes, &ctx->d_children, &ctx->d_term, &ctx->d_explen,
-                      &ctx->d_expoff, &ctx->d_expflat, &ctx->d_fxc, &ctx->d_fxe, &ctx->d_cxdfa, &ctx->d_cxt2, &ctx->d_cxcodes, &ctx->fxs[0], &ctx->fxs[1], &ctx->ixs, &ctx->ctl[0], &ctx->ctl[1], &ctx->ts[0],
+                      &ctx->d_expoff, &ctx->d_expflat, &ctx->d_fxc, &ctx->d_fxe, &ctx->d_cxdfa, &ctx->d_cxt2, &ctx->d_cxcodes, &ctx->d_cxcmap, &ctx->fxs[0], &ctx->fxs[1], &ctx->ixs, &ctx->ctl[0], &ctx->ctl[1], &ctx->ts[0],
                       &ctx->ts[1], &ctx->terr[0], &ctx->terr[1], &ctx->in[0], &ctx->in[1],
                       &ctx->out[0], &ctx->out[1], &ctx->arena[0], &ctx->arena[1], &ctx->s_flat, &ctx->s_starts,
                       &ctx->s_out, &ctx->s_lens, &ctx->s_dec, &ctx->s_stat, &ctx->s_errpos,
@@ -811,6 +879,7 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
         CK(up(ctx->d_t2, ht.t2.data(), ht.t2.size() * 4));
     }
     if (ht.cx_ok) {
+        CK(up(ctx->d_cxcmap, ht.cx_cmap.data(), 256));
         CK(up(ctx->d_cxdfa, ht.cx_dfa.data(), ht.cx_dfa.size() * 2));
         CK(up(ctx->d_cxt2, ht.cx_t2.data(), ht.cx_t2.size() * 4));
         CK(up(ctx->d_cxcodes, ht.cx_codes.data(), ht.cx_codes.size()));

@@ -37,6 +37,7 @@
 namespace zs {
 
 constexpr int CX_NT = 768;
+constexpr int CX_CTAS = 1;                        // resident CTAs per SM
 constexpr int CX_NW = CX_NT / 32;
 constexpr int CX_CC = 66;                         // bytes of line ends per lane (tile 50,688 B)
 constexpr int CX_TILE = CX_NT * CX_CC;
@@ -88,15 +89,27 @@ struct CxLayout {
     int o_t2, o_codes, bytes;
 };
 
-__host__ __device__ inline CxLayout cx_layout(int ns, int nw) {
+__host__ __device__ inline CxLayout cx_layout(int ns, int nw, int nc) {
     CxLayout L;
-    L.o_t2 = CX_O_DFA + cx_align16(ns * CX_NCOL * 2);
+    L.o_t2 = CX_O_DFA + cx_align16(ns * nc * 2);
     L.o_codes = L.o_t2 + nw * T2_MASKS * 4;
     L.bytes = L.o_codes + cx_align16(ns * CX_CODES);
     return L;
 }
 
-__host__ __device__ inline int cx_smem_bytes(int ns, int nw) { return cx_layout(ns, nw).bytes; }
+__host__ __device__ inline int cx_smem_bytes(int ns, int nw, int nc) { return cx_layout(ns, nw, nc).bytes; }
+
+// device tables of the lane-chunk kernel (built by build_cx, zs_api.cu): the
+// minimised reversed-pattern DFA over byte-class columns, the cost-window
+// transducer, code slots per state and the byte -> column map
+struct CxTables {
+    const uint16_t *dfa;   // [states][cols] = next | mask index << 8
+    const uint32_t *t2;    // [windows][16]
+    const uint8_t *codes;  // [states][16]
+    const uint8_t *cmap;   // [256]
+    int ns, nw, nc;
+    int o_t2, o_codes;     // smem offsets (cx_layout)
+};
 
 struct CxSmem {
     uint16_t *dfa;
@@ -318,9 +331,7 @@ __device__ __forceinline__ void cx_rare(const CxSmem &S, int *n, int ls, int le,
     }
 }
 
-__global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, const uint16_t *cx_dfa,
-                                                        const uint32_t *cx_t2, const uint8_t *cx_codes,
-                                                        int cx_ns, int cx_nw, int o_t2, int o_codes) {
+__global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb, CxTables ct) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int s_tmp[CX_NW];
     __shared__ unsigned long long s_tmp64[CX_NW];
@@ -331,15 +342,17 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
 
     __shared__ __align__(16) uint8_t s_lut[8 * 256];  // tokenizer transducer (static: constant addresses)
     __shared__ __align__(16) uint8_t s_explen[256];
-    CxSmem S = cx_carve(smem, o_t2, o_codes);
+    __shared__ __align__(16) uint8_t s_cmap[256];
+    CxSmem S = cx_carve(smem, ct.o_t2, ct.o_codes);
     S.lut = s_lut;
     S.explen = s_explen;
     {
-        const uint4 *src = reinterpret_cast<const uint4 *>(cx_dfa);
+        const uint4 *src = reinterpret_cast<const uint4 *>(ct.dfa);
         uint4 *dst = reinterpret_cast<uint4 *>(S.dfa);
-        for (int k = threadIdx.x; k < cx_align16(cx_ns * CX_NCOL * 2) / 16; k += CX_NT) dst[k] = src[k];
-        for (int k = threadIdx.x; k < cx_nw * T2_MASKS; k += CX_NT) S.t2[k] = cx_t2[k];
-        for (int k = threadIdx.x; k < cx_ns * CX_CODES; k += CX_NT) S.codes[k] = cx_codes[k];
+        for (int k = threadIdx.x; k < cx_align16(ct.ns * ct.nc * 2) / 16; k += CX_NT) dst[k] = src[k];
+        for (int k = threadIdx.x; k < ct.nw * T2_MASKS; k += CX_NT) S.t2[k] = ct.t2[k];
+        for (int k = threadIdx.x; k < ct.ns * CX_CODES; k += CX_NT) S.codes[k] = ct.codes[k];
+        for (int k = threadIdx.x; k < 256; k += CX_NT) s_cmap[k] = ct.cmap[k];
         for (int k = threadIdx.x; k < 256; k += CX_NT) S.explen[k] = k == '\n' ? 1 : tb.exp_len[k];
         for (int k = threadIdx.x; k < 8 * 256; k += CX_NT) {
             const unsigned st = k >> 8, b = k & 255;
@@ -730,15 +743,17 @@ __global__ void __launch_bounds__(CX_NT, 1) compress_cx(Job job, Tables tb, cons
             const uint16_t *__restrict__ dfa = S.dfa;
             const uint32_t *__restrict__ t2 = S.t2;
             const uint8_t *__restrict__ codes = S.codes;
+            const int nc = ct.nc;
             uint8_t *win = S.win;
             unsigned st = 0, wi = 0;
             auto step = [&](unsigned b) -> unsigned {
-                const unsigned e = dfa[st * CX_NCOL + umin_(b - 10u, 118u)];
+                const unsigned e = dfa[st * nc + s_cmap[b]];
                 st = e & 0xffu;
                 const unsigned x = t2[wi * T2_MASKS + (e >> 8)];
                 wi = x & 0xfffu;
                 acc += x >> 16;
-                return codes[st * CX_CODES + ((x >> 12) & 15u)];
+                const unsigned L = (x >> 12) & 15u;
+                return L == 1 ? b : codes[st * CX_CODES + L];  // length 1: the identity code is the byte
             };
             if (start <= end) {
                 const int lo_w = (start + 3) & ~3;  // first whole word inside the range
