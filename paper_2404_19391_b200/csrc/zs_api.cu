@@ -66,7 +66,7 @@ struct HostTables {
     int cx_states = 0, cx_cols = 0;  // minimised DFA: states x byte-class columns
     std::vector<uint8_t> cx_cmap;     // byte -> column
     std::vector<uint16_t> cx_dfa;
-    std::vector<uint32_t> cx_t2;
+    std::vector<uint16_t> cx_t2;
     std::vector<uint8_t> cx_codes;
     uint8_t exp_len[256];
     uint16_t exp_off[257];
@@ -378,9 +378,24 @@ bool build_cx(HostTables &ht, int max_len) {
             }
             ht.cx_dfa[(size_t)q * nc + cmap[b]] = e;
         }
-    ht.cx_t2 = ht.t2;
+    // transducer entries as u16: next window (9 bits) | L << 9 | (delta + 4) << 13
+    if (nw > 512) return false;
+    ht.cx_t2.assign((size_t)nw * T2_MASKS, 0);
     for (int w = 0; w < nw; ++w)
-        ht.cx_t2[(size_t)w * T2_MASKS + CX_NLMASK] = 0u | (9u << 12) | ((1u + 16u) << 16);
+        for (int m = 0; m < T2_MASKS; ++m) {
+            const uint32_t x = ht.t2[(size_t)w * T2_MASKS + m];
+            uint32_t e;
+            if (m == CX_NLMASK) {
+                e = 0u | (9u << 9) | ((1u + 4u) << 13);
+            } else if (x == 0xffffffffu) {
+                e = 0;  // unreachable (mask index unused)
+            } else {
+                const int delta = (int)(x >> 16) - 16;
+                if (delta < -4 || delta > 3 || (x & 0xfffu) > 511u) return false;
+                e = (x & 0x1ffu) | (((x >> 12) & 15u) << 9) | ((uint32_t)(delta + 4) << 13);
+            }
+            ht.cx_t2[(size_t)w * T2_MASKS + m] = (uint16_t)e;
+        }
     // code slot L: 0 = escape (0x20, never a code), 2..8 = the match of length L,
     // 9 = '\n'; length 1 is the byte itself
     ht.cx_codes.assign((size_t)cx_align16(S * CX_CODES), 0);
@@ -465,7 +480,7 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
         if (cx) {
             const CxLayout L = cx_layout(ctx->ht.cx_states, ctx->ht.n_windows, ctx->ht.cx_cols);
             CK(set_smem(compress_cx, L.bytes));
-            CxTables ct{ctx->d_cxdfa.as<uint16_t>(), ctx->d_cxt2.as<uint32_t>(), ctx->d_cxcodes.as<uint8_t>(),
+            CxTables ct{ctx->d_cxdfa.as<uint16_t>(), ctx->d_cxt2.as<uint16_t>(), ctx->d_cxcodes.as<uint8_t>(),
                         ctx->d_cxcmap.as<uint8_t>(), ctx->ht.cx_states, ctx->ht.n_windows, ctx->ht.cx_cols,
                         L.o_t2, L.o_codes};
             const int g2 = (int)std::min<long long>(nt, (long long)ctx->n_sm * CX_CTAS);
@@ -881,7 +896,7 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
     if (ht.cx_ok) {
         CK(up(ctx->d_cxcmap, ht.cx_cmap.data(), 256));
         CK(up(ctx->d_cxdfa, ht.cx_dfa.data(), ht.cx_dfa.size() * 2));
-        CK(up(ctx->d_cxt2, ht.cx_t2.data(), ht.cx_t2.size() * 4));
+        CK(up(ctx->d_cxt2, ht.cx_t2.data(), ht.cx_t2.size() * 2));
         CK(up(ctx->d_cxcodes, ht.cx_codes.data(), ht.cx_codes.size()));
     }
     {

@@ -92,7 +92,7 @@ struct CxLayout {
 __host__ __device__ inline CxLayout cx_layout(int ns, int nw, int nc) {
     CxLayout L;
     L.o_t2 = CX_O_DFA + cx_align16(ns * nc * 2);
-    L.o_codes = L.o_t2 + nw * T2_MASKS * 4;
+    L.o_codes = L.o_t2 + cx_align16(nw * T2_MASKS * 2);
     L.bytes = L.o_codes + cx_align16(ns * CX_CODES);
     return L;
 }
@@ -104,7 +104,7 @@ __host__ __device__ inline int cx_smem_bytes(int ns, int nw, int nc) { return cx
 // transducer, code slots per state and the byte -> column map
 struct CxTables {
     const uint16_t *dfa;   // [states][cols] = next | mask index << 8
-    const uint32_t *t2;    // [windows][16]
+    const uint16_t *t2;    // [windows][16] = next window | L << 9 | (cost delta + 4) << 13
     const uint8_t *codes;  // [states][16]
     const uint8_t *cmap;   // [256]
     int ns, nw, nc;
@@ -113,7 +113,7 @@ struct CxTables {
 
 struct CxSmem {
     uint16_t *dfa;
-    uint32_t *t2;
+    uint16_t *t2;
     uint8_t *codes;
     uint8_t *explen;
     uint8_t *lut;
@@ -140,7 +140,7 @@ __device__ inline CxSmem cx_carve(uint8_t *p, int o_t2, int o_codes) {
     S.jobs = reinterpret_cast<int4 *>(p + CX_O_JOBS);
     S.njobs = reinterpret_cast<int *>(p + CX_O_NJOBS);
     S.dfa = reinterpret_cast<uint16_t *>(p + CX_O_DFA);
-    S.t2 = reinterpret_cast<uint32_t *>(p + o_t2);
+    S.t2 = reinterpret_cast<uint16_t *>(p + o_t2);
     S.codes = p + o_codes;
     return S;
 }
@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         unsigned acc = 0;
         {
             const uint16_t *__restrict__ dfa = S.dfa;
-            const uint32_t *__restrict__ t2 = S.t2;
+            const uint16_t *__restrict__ t2 = S.t2;
             const uint8_t *__restrict__ codes = S.codes;
             const int nc = ct.nc;
             uint8_t *win = S.win;
@@ -750,9 +750,9 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 const unsigned e = dfa[st * nc + s_cmap[b]];
                 st = e & 0xffu;
                 const unsigned x = t2[wi * T2_MASKS + (e >> 8)];
-                wi = x & 0xfffu;
-                acc += x >> 16;
-                const unsigned L = (x >> 12) & 15u;
+                wi = x & 0x1ffu;
+                acc += x >> 13;
+                const unsigned L = (x >> 9) & 15u;
                 return L == 1 ? b : codes[st * CX_CODES + L];  // length 1: the identity code is the byte
             };
             if (start <= end) {
@@ -815,7 +815,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         }
         __syncthreads();
         const int nbytes = end >= start ? end - start + 1 : 0;
-        const long long my_out = (long long)acc - 16ll * nbytes - sub + S.lane_b[tid];
+        const long long my_out = (long long)acc - 4ll * nbytes - sub + S.lane_b[tid];
         // ---- P5: tile output bytes and lines (one scan); publish ----
         unsigned long long tot;
         const unsigned long long ex = block_exscan_n<unsigned long long, CX_NT>(
