@@ -560,8 +560,41 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 }
                 flush(end);
             };
+            // the fast walk: whole words of 4 bytes; per word the four LUT
+            // entries are combined once for the flags, the ring-token nibble
+            // and the newline count
+            auto walk_fast = [&]() {
+                int p = first;
+                const int w0 = (first + 3) & ~3, w1 = (end + 1) & ~3;
+                if (w0 < w1) {
+                    for (; p < w0; ++p) step_fast(p, S.win[p]);
+                    if (p > first && (p & 31) == 0) flush(p - 1);
+                    unsigned cur = w32[p >> 2];
+                    for (; p < w1; p += 4) {
+                        const unsigned nxt = w32[(p >> 2) + 1];  // prefetch (the window has slack after it)
+                        const unsigned e0 = lut[(st << 8) | (cur & 0xffu)];
+                        const unsigned e1 = lut[((e0 & 7u) << 8) | ((cur >> 8) & 0xffu)];
+                        const unsigned e2 = lut[((e1 & 7u) << 8) | ((cur >> 16) & 0xffu)];
+                        const unsigned e3 = lut[((e2 & 7u) << 8) | (cur >> 24)];
+                        st = e3 & 7u;
+                        const unsigned ew = e0 | (e1 << 8) | (e2 << 16) | (e3 << 24);
+                        flags |= ew;
+                        nlines += __popc(ew & 0x80808080u);
+                        const unsigned rn = (((ew >> 3) & 0x01010101u) * 0x01020408u) >> 24;  // ring bits, byte k -> bit k
+                        rmask |= (rn & 15u) << (p & 31);
+                        if (((p + 3) & 31) == 31) flush(p);
+                        cur = nxt;
+                    }
+                }
+                for (; p <= end; ++p) {
+                    step_fast(p, S.win[p]);
+                    if ((p & 31) == 31) flush(p);
+                }
+                flush(end);
+                flags |= (flags >> 8) | (flags >> 16) | (flags >> 24);
+            };
             if (first <= end) {
-                walk(step_fast);
+                walk_fast();
                 if (flags & 0x70u) {  // a CR or a tokenize error in the range (rare)
                     nlines = glob ? 1 : 0;
                     st = TK_OUT0;
