@@ -76,6 +76,15 @@ def _load():
                                       ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(_Stats)]
         lib.zo_free.argtypes = [P]
+        lib.zo_count_substrings.restype = I64
+        lib.zo_count_substrings.argtypes = [P, I64, ctypes.c_int, ctypes.c_int,
+                                            ctypes.POINTER(ctypes.c_void_p),
+                                            ctypes.POINTER(ctypes.c_void_p),
+                                            ctypes.POINTER(ctypes.c_void_p)]
+        lib.zo_overlap.restype = I64
+        lib.zo_overlap.argtypes = [P, ctypes.c_int, P, P, ctypes.c_int]
+        lib.zo_select_patterns.restype = I64
+        lib.zo_select_patterns.argtypes = [P, P, P, P, I64, ctypes.c_int, I64, P]
         _lib = lib
     return _lib
 
@@ -211,3 +220,58 @@ def run_stream(t: Tables, payload, direction="compress", preprocess=False, lenie
         data = ctypes.string_at(outp.value, st.out_bytes)
         lib.zo_free(outp)
     return data, stats
+
+
+# --------------------------------------------------------------------------
+# dictionary training (zs_oracle_train.c; dictionary.py:169-320)
+# --------------------------------------------------------------------------
+
+WORKING_SET_CAP = 200_000  # dictionary.py:43
+
+
+def count_substrings(lines, l_min, l_max):
+    """-> (buf, pos i64[m], len i32[m], occ i64[m]) rows in the reference's
+    RankTable order; pattern r = buf[pos[r]:pos[r] + len[r]]."""
+    lib = _load()
+    buf = np.frombuffer(b"\n".join(lines) or b"\0", np.uint8).copy()
+    n = len(b"\n".join(lines))
+    pp, lp, op = ctypes.c_void_p(0), ctypes.c_void_p(0), ctypes.c_void_p(0)
+    m = lib.zo_count_substrings(_p(buf), n, l_min, l_max, ctypes.byref(pp), ctypes.byref(lp),
+                                ctypes.byref(op))
+    pos = np.ctypeslib.as_array((ctypes.c_int64 * m).from_address(pp.value)).copy() if m else \
+        np.zeros(0, np.int64)
+    ln = np.ctypeslib.as_array((ctypes.c_int32 * m).from_address(lp.value)).copy() if m else \
+        np.zeros(0, np.int32)
+    occ = np.ctypeslib.as_array((ctypes.c_int64 * m).from_address(op.value)).copy() if m else \
+        np.zeros(0, np.int64)
+    for q in (pp, lp, op):
+        lib.zo_free(q)
+    return buf, pos, ln, occ
+
+
+def table_entries(lines, l_min, l_max):
+    """[(pattern bytes, occurrences)] in row order."""
+    buf, pos, ln, occ = count_substrings(lines, l_min, l_max)
+    b = buf.tobytes()
+    return [(b[p:p + l], int(o)) for p, l, o in zip(pos.tolist(), ln.tolist(), occ.tolist())]
+
+
+def overlap(p: bytes, selected) -> int:
+    lib = _load()
+    sel = list(dict.fromkeys(bytes(s) for s in selected))
+    flat = np.frombuffer(b"".join(sel) or b"\0", np.uint8).copy()
+    lens = np.array([len(s) for s in sel] or [0], np.int32)
+    src = np.frombuffer(bytes(p) or b"\0", np.uint8).copy()
+    return int(lib.zo_overlap(_p(src), len(p), _p(flat), _p(lens), len(sel)))
+
+
+def train(lines, l_min=2, l_max=8, t=128, cap=WORKING_SET_CAP):
+    """count_substrings + select_patterns on already-preprocessed lines ->
+    learned patterns in code order (dictionary.py:310-320 minus preprocess)."""
+    lib = _load()
+    buf, pos, ln, occ = count_substrings(lines, l_min, l_max)
+    out = np.zeros(max(t, 1), np.int64)
+    k = lib.zo_select_patterns(_p(buf), _p(pos), _p(ln), _p(occ), pos.size, t, cap, _p(out)) \
+        if pos.size else 0
+    b = buf.tobytes()
+    return [b[pos[i]:pos[i] + ln[i]] for i in out[:k].tolist()]

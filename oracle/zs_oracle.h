@@ -51,4 +51,11 @@ int zo_preprocess_line(const uint8_t *s, int64_t n, uint8_t *out, int64_t *out_l
 int zo_run_stream(const zo_tables *tb, const uint8_t *buf, int64_t n, int direction,
                   int preprocess, int lenient, int n_threads, uint8_t **out, zo_stats *st);
 void zo_free(void *p);
+
+/* dictionary training (zs_oracle_train.c): rows malloc'd, free with zo_free */
+int64_t zo_count_substrings(const uint8_t *buf, int64_t n, int lmin, int lmax, int64_t **pos_out,
+                            int32_t **len_out, int64_t **occ_out);
+int64_t zo_overlap(const uint8_t *p, int n, const uint8_t *sel, const int32_t *sel_len, int nsel);
+int64_t zo_select_patterns(const uint8_t *buf, const int64_t *pos, const int32_t *len, const int64_t *occ,
+                           int64_t m, int t, int64_t cap, int64_t *out);
 #endif

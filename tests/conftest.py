@@ -64,3 +64,8 @@ def has_gpu():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+@pytest.fixture(scope="session")
+def train_cases():
+    return load_golden("train_cases.json.gz")

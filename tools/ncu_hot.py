@@ -113,3 +113,33 @@ def section(rep, fname, lo, hi):
 
 if __name__ == "__main__" and len(sys.argv) > 3 and sys.argv[3] == "section":
     section(sys.argv[1], sys.argv[4], int(sys.argv[5]), int(sys.argv[6]))
+
+
+def insts(rep, top=40):
+    """Top CUDA source lines by executed warp instructions (with the thread
+    instructions / warp instructions ratio = average active lanes)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    fname, hdr, src = "?", None, []
+    for r in rows:
+        if len(r) == 2 and r[0] in ("File Path", "File Name"):
+            fname = r[1].rsplit("/", 1)[-1]
+            continue
+        if len(r) > 4 and r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr is None or len(r) != len(hdr) or not r[0]:
+            continue
+        w = num(r[hdr.index("Instructions Executed")])
+        t = num(r[hdr.index("Thread Instructions Executed")]) if "Thread Instructions Executed" in hdr else 0
+        src.append((w, t, f"{fname}:{r[0]}", r[1].strip()))
+    W = sum(s[0] for s in src) or 1
+    T = sum(s[1] for s in src) or 1
+    print(f"warp inst {W:.4g}  thread inst {T:.4g}  lanes/inst {T / W:.1f}")
+    for w, t, loc, text in sorted(src, key=lambda x: -x[0])[:top]:
+        print(f"{100 * w / W:5.1f}% {100 * t / T:5.1f}%t  {loc:20s} {text[:84]}")
+
+
+if __name__ == "__main__" and len(sys.argv) > 3 and sys.argv[3] == "inst":
+    insts(sys.argv[1], int(sys.argv[2]))
