@@ -120,6 +120,28 @@ int zs_index_build(zs_ctx *ctx, const uint8_t *d_comp, int64_t n, uint64_t *d_of
 int zs_decode_records(zs_ctx *ctx, const uint8_t *d_comp, const uint64_t *d_offsets, int64_t n_records,
                       const int64_t *d_idx, int64_t k, uint8_t *d_out, int64_t out_cap, int64_t *d_out_off,
                       int8_t *d_status, int64_t *d_errpos, int64_t *total_out);
+/* ---- dictionary training (dictionary.py:169-320) ----
+ * zs_train_count: census of h_buf = b"\n".join(lines) (count_substrings,
+ * dictionary.py:169-221): every alphabet-only window of length l_min..l_max
+ * (2 <= l_min <= l_max <= 64, n < 2^32), kept on the device as the rank
+ * table; *n_rows = its rows.  zs_train_rows copies the rows to the host in
+ * the reference's RankTable order (length-major, bytewise ascending): row r
+ * is h_buf[pos[r] : pos[r] + len[r]], occurring occ[r] times.
+ * zs_train_load replaces the device rank table with a host one (RankTable
+ * layout: patterns u8[m][width] zero-padded, lengths, occurrences).
+ * zs_train_select: select_patterns(table, t) (dictionary.py:241-307) with
+ * working-set cap `cap` (reference default 200000) -> rows_out[0..*n) in
+ * code order (0x80 + k).
+ * zs_overlap_batch: overlap_batch (numba_impl.py:142-169) on the reference
+ * trie layout (children int32[n_nodes][256], term_len int16[n_nodes]). */
+int zs_train_count(zs_ctx *ctx, const uint8_t *h_buf, int64_t n, int32_t l_min, int32_t l_max, int64_t *n_rows);
+int zs_train_rows(zs_ctx *ctx, int64_t *pos, int32_t *len, int64_t *occ);
+int zs_train_load(zs_ctx *ctx, const uint8_t *patterns, int32_t width, const int64_t *lengths, const int64_t *occ,
+                  int64_t m);
+int zs_train_select(zs_ctx *ctx, int32_t t, int64_t cap, int64_t *rows_out, int32_t *n_selected);
+int zs_overlap_batch(zs_ctx *ctx, const int32_t *children, const int16_t *term_len, int32_t n_nodes,
+                     const uint8_t *pats, int32_t width, const int64_t *lens, int64_t n, int64_t *out);
+
 /* debug/ablation kernel selection (default 3): bit 0 transducer parse, bit 1
  * in-place decisions (lane-chunk kernel), bit 2 warp-cooperative decompress
  * instead of the streaming one, bit 3 queue-based in-place compress kernel */

@@ -26,6 +26,7 @@ EXPORTS = (
     "zs_decompress_host", "zs_compress_bound", "zs_decompress_bound", "zs_last_kernel_ms",
     "zs_build_tables_host", "zs_set_phase_timing", "zs_last_phase_cycles", "zs_build_t2_host",
     "zs_set_transducer", "zs_last_kernel", "zs_stream", "zs_index_build", "zs_decode_records",
+    "zs_train_count", "zs_train_rows", "zs_train_load", "zs_train_select", "zs_overlap_batch",
 )
 
 
@@ -87,6 +88,11 @@ def load():
             "zs_index_build": (ctypes.c_int, [P, P, I64, P, I64, ctypes.POINTER(ctypes.c_int64)]),
             "zs_decode_records": (ctypes.c_int, [P, P, P, I64, P, I64, P, I64, P, P, P,
                                                  ctypes.POINTER(ctypes.c_int64)]),
+            "zs_train_count": (ctypes.c_int, [P, P, I64, I32, I32, ctypes.POINTER(ctypes.c_int64)]),
+            "zs_train_rows": (ctypes.c_int, [P, P, P, P]),
+            "zs_train_load": (ctypes.c_int, [P, P, I32, P, P, I64]),
+            "zs_train_select": (ctypes.c_int, [P, I32, I64, P, ctypes.POINTER(ctypes.c_int32)]),
+            "zs_overlap_batch": (ctypes.c_int, [P, P, P, I32, P, I32, P, I64, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "zs_api.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("zs_api.cu", "zs_kernels.cuh", "zs_device.cuh", "zs_fx.cuh", "zs_cx.cuh", "zs_ix.cuh")] + \
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("zs_api.cu", "zs_kernels.cuh", "zs_device.cuh", "zs_fx.cuh", "zs_cx.cuh", "zs_ix.cuh", "zs_train.cuh")] + \
        [os.path.join(ROOT, "include", "zs.h")]
 OUT = os.path.join(HERE, "libzs.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -22,6 +22,7 @@
 #include "zs_fx.cuh"
 #include "zs_cx.cuh"
 #include "zs_ix.cuh"
+#include "zs_train.cuh"
 
 using namespace zs;
 
@@ -46,6 +47,20 @@ struct DevBuf {
         cap = 0;
     }
     template <typename T> T *as() const { return reinterpret_cast<T *>(p); }
+    // grow to >= n bytes keeping the first `keep` bytes (stream-ordered copy)
+    cudaError_t grow_keep(size_t n, size_t keep, cudaStream_t st) {
+        if (n <= cap) return cudaSuccess;
+        void *q = nullptr;
+        const size_t c = std::max<size_t>(n, 2 * cap);
+        cudaError_t e = cudaMalloc(&q, c);
+        if (e != cudaSuccess) return e;
+        if (keep) e = cudaMemcpyAsync(q, p, keep, cudaMemcpyDeviceToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (p) cudaFree(p);
+        p = q;
+        cap = c;
+        return e;
+    }
 };
 
 struct HostTables {
@@ -99,6 +114,14 @@ struct zs_ctx {
     DevBuf ctl[2], ts[2], terr[2], in[2], out[2], arena[2];  // arena: per slot
     DevBuf fxs[2];  // streaming-decode scratch per slot
     DevBuf ixs;     // record-index scratch
+    // dictionary training (zs_train.cuh): corpus, census scratch, rank table, selection state
+    struct {
+        DevBuf buf, run, pos[2], key[2], lcp, runs, v, ex, bstart, cand, cub, nsel;
+        DevBuf rpos, rocc, rlen;  // rank table rows
+        DevBuf rank[2], idx[2], dead, child, term, ctl, blk, sel;
+        long long n = 0, rows = 0;
+        int lmax = 0;
+    } tr;
     // shim scratch
     DevBuf s_flat, s_starts, s_out, s_lens, s_dec, s_stat, s_errpos, s_tot, s_ids, s_outst;
     Ctl *h_ctl = nullptr;  // pinned, 2 slots
@@ -810,7 +833,12 @@ int zs_ctx_destroy(zs_ctx *ctx) {
                       &ctx->ts[1], &ctx->terr[0], &ctx->terr[1], &ctx->in[0], &ctx->in[1],
                       &ctx->out[0], &ctx->out[1], &ctx->arena[0], &ctx->arena[1], &ctx->s_flat, &ctx->s_starts,
                       &ctx->s_out, &ctx->s_lens, &ctx->s_dec, &ctx->s_stat, &ctx->s_errpos,
-                      &ctx->s_tot, &ctx->s_ids, &ctx->s_outst})
+                      &ctx->s_tot, &ctx->s_ids, &ctx->s_outst, &ctx->tr.buf, &ctx->tr.run, &ctx->tr.pos[0],
+                      &ctx->tr.pos[1], &ctx->tr.key[0], &ctx->tr.key[1], &ctx->tr.lcp, &ctx->tr.runs, &ctx->tr.v,
+                      &ctx->tr.ex, &ctx->tr.bstart, &ctx->tr.cand, &ctx->tr.cub, &ctx->tr.nsel, &ctx->tr.rpos,
+                      &ctx->tr.rocc, &ctx->tr.rlen, &ctx->tr.rank[0], &ctx->tr.rank[1], &ctx->tr.idx[0],
+                      &ctx->tr.idx[1], &ctx->tr.dead, &ctx->tr.child, &ctx->tr.term, &ctx->tr.ctl, &ctx->tr.blk,
+                      &ctx->tr.sel})
         b->release();
     for (int s = 0; s < 2; ++s) {
         if (ctx->stream[s]) cudaStreamDestroy(ctx->stream[s]);
@@ -1216,6 +1244,249 @@ int zs_preprocess_batch(zs_ctx *ctx, const uint8_t *flat, const int64_t *starts,
     CK(cudaMemcpyAsync(status, ctx->s_stat.p, n_lines, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(err_off, ctx->s_errpos.p, 8 * n_lines, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(err_ids, ctx->s_ids.p, 16 * n_lines, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return ZS_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// dictionary training (zs_train.cuh; dictionary.py:169-320)
+// ---------------------------------------------------------------------------
+
+int zs_train_count(zs_ctx *ctx, const uint8_t *h_buf, int64_t n, int32_t l_min, int32_t l_max, int64_t *n_rows) {
+    if (!ctx || n < 0 || (n > 0 && !h_buf) || !n_rows || l_min < 2 || l_min > l_max || l_max > 64 ||
+        n >= (int64_t)0xffffff00ll)
+        return ZS_E_ARG;
+    CK(cudaSetDevice(ctx->dev));
+    cudaStream_t st = ctx->stream[0];
+    auto &T = ctx->tr;
+    *n_rows = 0;
+    T.rows = 0;
+    T.n = n;
+    T.lmax = l_max;
+    if (n == 0) return ZS_OK;
+    auto grid = [&](long long m) { return (int)std::max(1ll, std::min<long long>((m + 255) / 256, (long long)ctx->n_sm * 16)); };
+    if (T.buf.reserve((size_t)n + 16) || T.run.reserve((size_t)n) || T.pos[0].reserve((size_t)n * 4) ||
+        T.pos[1].reserve((size_t)n * 4) || T.nsel.reserve(64))
+        return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(train)");
+    CK(cudaMemcpyAsync(T.buf.p, h_buf, (size_t)n, cudaMemcpyHostToDevice, st));
+    tr_runs<<<grid((n + TR_SPAN - 1) / TR_SPAN), TR_NT, 0, st>>>(T.buf.as<uint8_t>(), n, l_max, T.run.as<uint8_t>());
+    CK(cudaGetLastError());
+    // candidate starts: alphabet run >= l_min
+    size_t tb = 0;
+    thrust::counting_iterator<uint32_t> it(0);
+    const TrAtLeast sel_op{T.run.as<uint8_t>(), l_min};
+    CK(cub::DeviceSelect::If(nullptr, tb, it, T.pos[0].as<uint32_t>(), T.nsel.as<long long>(), n, sel_op, st));
+    if (T.cub.reserve(tb)) return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(cub)");
+    CK(cub::DeviceSelect::If(T.cub.p, tb, it, T.pos[0].as<uint32_t>(), T.nsel.as<long long>(), n, sel_op, st));
+    long long m = 0;
+    CK(cudaMemcpyAsync(&m, T.nsel.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (m == 0) return ZS_OK;
+    if (T.key[0].reserve((size_t)m * 8) || T.key[1].reserve((size_t)m * 8) || T.lcp.reserve((size_t)m) ||
+        T.runs.reserve((size_t)m) || T.v.reserve((size_t)m * 8) || T.ex.reserve((size_t)m * 8) ||
+        T.bstart.reserve((size_t)m * 4 + 8) || T.cand.reserve((size_t)m * 4))
+        return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(train)");
+    // LSD sort of the starts by their first l_max bytes
+    cub::DoubleBuffer<unsigned long long> keys(T.key[0].as<unsigned long long>(), T.key[1].as<unsigned long long>());
+    cub::DoubleBuffer<uint32_t> vals(T.pos[0].as<uint32_t>(), T.pos[1].as<uint32_t>());
+    const int W = (l_max + 7) / 8;
+    for (int w = W - 1; w >= 0; --w) {
+        const int nb = std::min(8, l_max - 8 * w);
+        tr_key<<<grid(m), 256, 0, st>>>(T.buf.as<uint8_t>(), n, vals.Current(), m, w, nb, keys.Current());
+        CK(cudaGetLastError());
+        tb = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, vals, (int)m, 64 - 8 * nb, 64, st));
+        if (T.cub.reserve(tb)) return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(cub)");
+        CK(cub::DeviceRadixSort::SortPairs(T.cub.p, tb, keys, vals, (int)m, 64 - 8 * nb, 64, st));
+    }
+    const uint32_t *pos = vals.Current();
+    tr_lcp<<<grid(m), 256, 0, st>>>(T.buf.as<uint8_t>(), pos, m, T.run.as<uint8_t>(), T.lcp.as<uint8_t>(),
+                                    T.runs.as<uint8_t>());
+    CK(cudaGetLastError());
+    tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, T.v.as<unsigned long long>(), T.ex.as<unsigned long long>(), (int)m, st));
+    if (T.cub.reserve(tb)) return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(cub)");
+    long long rows = 0;
+    for (int L = l_min; L <= l_max; ++L) {
+        if (n < L) break;  // dictionary.py:187-188
+        tr_flags<<<grid(m), 256, 0, st>>>(T.lcp.as<uint8_t>(), T.runs.as<uint8_t>(), m, L, T.v.as<unsigned long long>());
+        CK(cub::DeviceScan::ExclusiveSum(T.cub.p, tb, T.v.as<unsigned long long>(), T.ex.as<unsigned long long>(),
+                                         (int)m, st));
+        unsigned long long tail[2];
+        CK(cudaMemcpyAsync(&tail[0], T.v.as<unsigned long long>() + m - 1, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&tail[1], T.ex.as<unsigned long long>() + m - 1, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const long long c = (long long)((tail[0] & 0xffffffffull) + (tail[1] & 0xffffffffull));
+        if (c == 0) continue;
+        tr_scatter<<<grid(m), 256, 0, st>>>(T.v.as<unsigned long long>(), T.ex.as<unsigned long long>(), m,
+                                            T.bstart.as<uint32_t>(), T.cand.as<uint32_t>());
+        if (T.rpos.grow_keep((size_t)(rows + c) * 4, (size_t)rows * 4, st) ||
+            T.rocc.grow_keep((size_t)(rows + c) * 4, (size_t)rows * 4, st) ||
+            T.rlen.grow_keep((size_t)(rows + c), (size_t)rows, st))
+            return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(rank table)");
+        tr_rows<<<grid(c), 256, 0, st>>>(T.cand.as<uint32_t>(), c, pos, T.ex.as<unsigned long long>(),
+                                         T.bstart.as<uint32_t>(), L, T.rpos.as<uint32_t>() + rows,
+                                         T.rocc.as<uint32_t>() + rows, T.rlen.as<uint8_t>() + rows);
+        CK(cudaGetLastError());
+        rows += c;
+    }
+    CK(cudaStreamSynchronize(st));
+    if (rows >= (long long)0xffffffffll) return fail(ctx, cudaErrorInvalidValue, "rank table over 2^32 rows");
+    T.rows = rows;
+    *n_rows = rows;
+    return ZS_OK;
+}
+
+int zs_train_rows(zs_ctx *ctx, int64_t *pos, int32_t *len, int64_t *occ) {
+    if (!ctx || (ctx->tr.rows && (!pos || !len || !occ))) return ZS_E_ARG;
+    CK(cudaSetDevice(ctx->dev));
+    const long long m = ctx->tr.rows;
+    if (!m) return ZS_OK;
+    std::vector<uint32_t> p((size_t)m), o((size_t)m);
+    std::vector<uint8_t> l((size_t)m);
+    cudaStream_t st = ctx->stream[0];
+    CK(cudaMemcpyAsync(p.data(), ctx->tr.rpos.p, (size_t)m * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(o.data(), ctx->tr.rocc.p, (size_t)m * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(l.data(), ctx->tr.rlen.p, (size_t)m, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (long long i = 0; i < m; ++i) {
+        pos[i] = p[i];
+        len[i] = l[i];
+        occ[i] = o[i];
+    }
+    return ZS_OK;
+}
+
+int zs_train_load(zs_ctx *ctx, const uint8_t *patterns, int32_t width, const int64_t *lengths, const int64_t *occ,
+                  int64_t m) {
+    if (!ctx || m < 0 || width < 1 || width > 64 || (m > 0 && (!patterns || !lengths || !occ)) ||
+        m * (int64_t)width >= (int64_t)0xffffff00ll)
+        return ZS_E_ARG;
+    CK(cudaSetDevice(ctx->dev));
+    auto &T = ctx->tr;
+    T.rows = 0;
+    T.n = m * width;
+    T.lmax = width;
+    if (!m) return ZS_OK;
+    std::vector<uint32_t> p((size_t)m), o((size_t)m);
+    std::vector<uint8_t> l((size_t)m);
+    for (long long i = 0; i < m; ++i) {
+        if (lengths[i] < 1 || lengths[i] > width || occ[i] < 0 || occ[i] > 0xffffffffll) return ZS_E_ARG;
+        p[i] = (uint32_t)(i * width);
+        l[i] = (uint8_t)lengths[i];
+        o[i] = (uint32_t)occ[i];
+    }
+    cudaStream_t st = ctx->stream[0];
+    if (T.buf.reserve((size_t)(m * width) + 16) || T.rpos.reserve((size_t)m * 4) || T.rocc.reserve((size_t)m * 4) ||
+        T.rlen.reserve((size_t)m))
+        return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(train)");
+    CK(cudaMemcpyAsync(T.buf.p, patterns, (size_t)(m * width), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(T.rpos.p, p.data(), (size_t)m * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(T.rocc.p, o.data(), (size_t)m * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(T.rlen.p, l.data(), (size_t)m, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    T.rows = m;
+    return ZS_OK;
+}
+
+int zs_train_select(zs_ctx *ctx, int32_t t, int64_t cap, int64_t *rows_out, int32_t *n_selected) {
+    if (!ctx || t < 0 || t > 128 || cap < 1 || !n_selected || (t > 0 && !rows_out)) return ZS_E_ARG;
+    CK(cudaSetDevice(ctx->dev));
+    auto &T = ctx->tr;
+    cudaStream_t st = ctx->stream[0];
+    *n_selected = 0;
+    const long long M = T.rows;
+    if (t == 0 || M == 0) return ZS_OK;
+    auto grid = [&](long long m) { return (int)std::max(1ll, std::min<long long>((m + 255) / 256, (long long)ctx->n_sm * 16)); };
+    const long long nodes = 1 + (long long)t * T.lmax;
+    if (T.rank[0].reserve((size_t)M * 8) || T.rank[1].reserve((size_t)M * 8) || T.idx[0].reserve((size_t)M * 4) ||
+        T.idx[1].reserve((size_t)M * 4) || T.dead.reserve((size_t)M) ||
+        T.child.reserve((size_t)nodes * TR_TRIE_W * 2) || T.term.reserve((size_t)nodes) ||
+        T.ctl.reserve(sizeof(TrCtl)) || T.sel.reserve(128 * 4))
+        return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(select)");
+    const TrRows R{T.buf.as<uint8_t>(), T.rpos.as<uint32_t>(), T.rlen.as<uint8_t>()};
+    for (;;) {  // select_patterns (dictionary.py:300-307)
+        tr_init_rank<<<grid(M), 256, 0, st>>>(T.rocc.as<uint32_t>(), T.rlen.as<uint8_t>(), M,
+                                              T.rank[0].as<unsigned long long>(), T.idx[0].as<uint32_t>());
+        CK(cudaGetLastError());
+        const uint32_t *ws = T.idx[0].as<uint32_t>();
+        long long nws = M, excluded_max = -1;
+        if (cap < M) {  // working set: top-cap by initial rank, stable (dictionary.py:256-264)
+            size_t tb = 0;
+            CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, T.rank[0].as<unsigned long long>(),
+                                                         T.rank[1].as<unsigned long long>(), T.idx[0].as<uint32_t>(),
+                                                         T.idx[1].as<uint32_t>(), (int)M, 0, 64, st));
+            if (T.cub.reserve(tb)) return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(cub)");
+            CK(cub::DeviceRadixSort::SortPairsDescending(T.cub.p, tb, T.rank[0].as<unsigned long long>(),
+                                                         T.rank[1].as<unsigned long long>(), T.idx[0].as<uint32_t>(),
+                                                         T.idx[1].as<uint32_t>(), (int)M, 0, 64, st));
+            unsigned long long ex = 0;
+            CK(cudaMemcpyAsync(&ex, T.rank[1].as<unsigned long long>() + cap, 8, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            ws = T.idx[1].as<uint32_t>();
+            nws = cap;
+            excluded_max = (long long)ex;
+        }
+        const int nblk = grid(nws);
+        if (T.blk.reserve((size_t)nblk * sizeof(TrBest))) return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(select)");
+        const TrCtl c0{0, 0, 0, 1};
+        CK(cudaMemsetAsync(T.dead.p, 0, (size_t)nws, st));
+        CK(cudaMemsetAsync(T.child.p, 0xff, (size_t)nodes * TR_TRIE_W * 2, st));
+        CK(cudaMemsetAsync(T.term.p, 0, (size_t)nodes, st));
+        CK(cudaMemcpyAsync(T.ctl.p, &c0, sizeof c0, cudaMemcpyHostToDevice, st));
+        for (int k = 0; k < t; ++k) {  // _try_select (dictionary.py:266-297), no host round trip
+            tr_rank<<<nblk, TR_NT, 0, st>>>(R, T.rocc.as<uint32_t>(), ws, nws, T.dead.as<uint8_t>(),
+                                            T.child.as<int16_t>(), T.term.as<uint8_t>(), T.ctl.as<TrCtl>(),
+                                            T.blk.as<TrBest>());
+            tr_pick<<<1, 1024, 0, st>>>(R, T.dead.as<uint8_t>(), T.child.as<int16_t>(), T.term.as<uint8_t>(),
+                                        T.ctl.as<TrCtl>(), T.blk.as<TrBest>(), nblk, excluded_max, T.sel.as<uint32_t>());
+        }
+        CK(cudaGetLastError());
+        TrCtl c1;
+        uint32_t sel[128];
+        CK(cudaMemcpyAsync(&c1, T.ctl.p, sizeof c1, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(sel, T.sel.p, 128 * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (c1.fail) {
+            cap *= 4;
+            continue;
+        }
+        for (int k = 0; k < c1.nsel; ++k) rows_out[k] = sel[k];
+        *n_selected = c1.nsel;
+        return ZS_OK;
+    }
+}
+
+int zs_overlap_batch(zs_ctx *ctx, const int32_t *children, const int16_t *term_len, int32_t n_nodes,
+                     const uint8_t *pats, int32_t width, const int64_t *lens, int64_t n, int64_t *out) {
+    if (!ctx || n < 0 || n_nodes < 1 || width < 0 || !children || !term_len ||
+        (n > 0 && (!lens || !out || (width > 0 && !pats))))
+        return ZS_E_ARG;
+    for (int64_t r = 0; r < n; ++r)
+        if (lens[r] < 0 || lens[r] > width) return ZS_E_ARG;
+    if (n == 0) return ZS_OK;
+    CK(cudaSetDevice(ctx->dev));
+    cudaStream_t st = ctx->stream[0];
+    auto &T = ctx->tr;
+    const size_t cb = (size_t)n_nodes * 256 * 4, tb = (size_t)n_nodes * 2, pb = (size_t)n * width;
+    // scratch: children | term_len | pats | lens | out
+    DevBuf &S = T.cub;
+    if (S.reserve(cb + tb + pb + (size_t)n * 16 + 64)) return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(overlap)");
+    uint8_t *b = S.as<uint8_t>();
+    int32_t *d_ch = reinterpret_cast<int32_t *>(b);
+    int16_t *d_tl = reinterpret_cast<int16_t *>(b + cb);
+    uint8_t *d_p = b + cb + tb;
+    long long *d_l = reinterpret_cast<long long *>(b + ((cb + tb + pb + 15) & ~(size_t)15));
+    long long *d_o = d_l + n;
+    CK(cudaMemcpyAsync(d_ch, children, cb, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_tl, term_len, tb, cudaMemcpyHostToDevice, st));
+    if (pb) CK(cudaMemcpyAsync(d_p, pats, pb, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_l, lens, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    tr_overlap_batch<<<(int)std::min<long long>((n + 255) / 256, (long long)ctx->n_sm * 16), 256, 0, st>>>(
+        d_ch, d_tl, d_p, width, d_l, n, d_o);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, d_o, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return ZS_OK;
 }

@@ -4,10 +4,14 @@ Mirrors the reference's ``Dictionary`` (dictionary.py:65-141), its code
 assignment (identity byte -> itself, learned[i] -> 0x80+i), the table
 builders the codec consumes (``encode_trie``: trie.py layout;
 ``decode_tables``: dictionary.py:112-129) and ZSD1 (de)serialization
-(dictionary.py:322-383).  Dictionary *training* (``generate`` and friends)
-is out of scope for this build (not on the codec path).
+(dictionary.py:322-383), and dictionary *training* on the GPU
+(``GenerationParams``, ``RankTable``, ``count_substrings``,
+``compute_overlap``, ``select_patterns``, ``generate``: dictionary.py:43-63,
+143-320; kernels in csrc/zs_train.cuh) with the reference's results, tie
+rule and working-set cap.
 """
 
+from dataclasses import dataclass
 from functools import cached_property
 
 import numpy as np
@@ -15,6 +19,7 @@ import numpy as np
 from .errors import (
     BadMagic,
     DictionaryFormatError,
+    EmptyCorpus,
     NonAlphabetByteInPattern,
     PatternTooLong,
     TooManyPatterns,
@@ -33,6 +38,31 @@ PREPOPULATE_SETS = {
 }
 
 _MAGIC = b"ZSD1"
+
+# Candidates below this initial-rank cutoff stay out of the selection working
+# set; a pick that does not beat the cutoff restarts with 4x the set
+# (dictionary.py:38-43, 300-307).  Same name so tests can monkeypatch it.
+_WORKING_SET_CAP = 200_000
+
+
+@dataclass(frozen=True)
+class GenerationParams:
+    """Training knobs (dictionary.py:46-62)."""
+    l_min: int = 2
+    l_max: int = 8
+    t: int = 128
+    prepopulate: str = "smiles"
+    preprocess: bool = False
+
+    def __post_init__(self):
+        if not 2 <= self.l_min <= self.l_max <= MAX_PATTERN_LEN:
+            raise ValueError(
+                f"need 2 <= l_min <= l_max <= {MAX_PATTERN_LEN}, "
+                f"got l_min={self.l_min} l_max={self.l_max}")
+        if not 0 <= self.t <= MAX_PATTERNS:
+            raise ValueError(f"need 0 <= t <= {MAX_PATTERNS}, got {self.t}")
+        if self.prepopulate not in PREPOPULATE_SETS:
+            raise ValueError(f"unknown prepopulate mode {self.prepopulate!r}")
 
 
 class Dictionary:
@@ -176,3 +206,143 @@ def default_dictionary() -> Dictionary:
     regenerated by its own trainer in tests/golden/make_golden.py)."""
     from importlib.resources import files
     return deserialize(files(__package__).joinpath("data/default.zsd").read_bytes())
+
+
+# ---------------------------------------------------------------------------
+# training (GPU): dictionary.py:143-320
+# ---------------------------------------------------------------------------
+
+class RankTable:
+    """Substring census (dictionary.py:143-166): rows of ``patterns``
+    zero-padded to l_max, in the reference's order (length-major, bytewise
+    ascending within a length); ``ranks`` = occurrences * length.  The rows
+    also stay resident on the GPU that counted them (``_device``), so
+    ``select_patterns`` runs without re-uploading."""
+
+    def __init__(self, patterns, lengths, occurrences, ranks, _device=None):
+        self.patterns = patterns
+        self.lengths = lengths
+        self.occurrences = occurrences
+        self.ranks = ranks
+        self._device = _device
+
+    def __len__(self):
+        return self.patterns.shape[0]
+
+    def pattern(self, i: int) -> bytes:
+        return self.patterns[i, :self.lengths[i]].tobytes()
+
+    @property
+    def entries(self) -> dict:
+        return {self.pattern(i): (int(self.occurrences[i]), int(self.ranks[i]))
+                for i in range(len(self))}
+
+
+def _ctx():
+    from . import _lib
+    return _lib, _lib.context()
+
+
+def count_substrings(corpus, params: GenerationParams) -> RankTable:
+    """Exact occurrence counts of every alphabet-only substring with length in
+    [l_min, l_max] (dictionary.py:169-221), counted on the GPU: one sort of
+    the window starts by their first l_max bytes, then one boundary sweep per
+    length (csrc/zs_train.cuh)."""
+    lines = list(corpus)
+    if not lines:
+        raise EmptyCorpus("no training lines")
+    joined = b"\n".join(bytes(l) for l in lines)
+    buf = np.frombuffer(joined or b"\0", np.uint8)
+    _lib, ctx = _ctx()
+    import ctypes
+    m = ctypes.c_int64(0)
+    with ctx.lock:
+        ctx.check(ctx.lib.zs_train_count(ctx.h, _lib.ptr(buf), len(joined), params.l_min, params.l_max,
+                                         ctypes.byref(m)), "zs_train_count")
+        n = m.value
+        pos = np.zeros(n, np.int64)
+        lens = np.zeros(n, np.int32)
+        occ = np.zeros(n, np.int64)
+        ctx.check(ctx.lib.zs_train_rows(ctx.h, _lib.ptr(pos), _lib.ptr(lens), _lib.ptr(occ)), "zs_train_rows")
+        ctx._train_gen = getattr(ctx, "_train_gen", 0) + 1
+        token = (id(ctx), ctx._train_gen)
+    width = params.l_max
+    src = np.frombuffer(joined + bytes(width), np.uint8)
+    cols = np.arange(width, dtype=np.int64)
+    patterns = src[pos[:, None] + cols[None, :]] if n else np.zeros((0, width), np.uint8)
+    patterns = np.where(cols[None, :] < lens[:, None], patterns, 0).astype(np.uint8)
+    lengths = lens.astype(np.int64)
+    return RankTable(np.ascontiguousarray(patterns), lengths, occ, occ * lengths, _device=token)
+
+
+def select_patterns(table: RankTable, t: int) -> list:
+    """Repeated argmax of occurrences * (length - greedy overlap with the
+    selected patterns), full overlap recomputation after every pick, ties to
+    the longest then bytewise smallest pattern (dictionary.py:241-307) -- on
+    the GPU, t picks without a host round trip."""
+    import ctypes
+    _lib, ctx = _ctx()
+    out = np.zeros(max(t, 1), np.int64)
+    k = ctypes.c_int32(0)
+    with ctx.lock:
+        if table._device != (id(ctx), getattr(ctx, "_train_gen", 0)):
+            pats = np.ascontiguousarray(table.patterns, np.uint8)
+            width = pats.shape[1] if pats.ndim == 2 and pats.shape[1] else 1
+            if pats.shape[0] == 0:
+                pats = np.zeros((0, width), np.uint8)
+            ctx.check(ctx.lib.zs_train_load(ctx.h, _lib.ptr(pats), width,
+                                            _lib.ptr(np.ascontiguousarray(table.lengths, np.int64)),
+                                            _lib.ptr(np.ascontiguousarray(table.occurrences, np.int64)),
+                                            len(table)), "zs_train_load")
+            ctx._train_gen = getattr(ctx, "_train_gen", 0) + 1
+            table._device = (id(ctx), ctx._train_gen)
+        ctx.check(ctx.lib.zs_train_select(ctx.h, t, _WORKING_SET_CAP, _lib.ptr(out), ctypes.byref(k)),
+                  "zs_train_select")
+    return [table.pattern(int(i)) for i in out[:k.value]]
+
+
+def compute_overlap(p: bytes, selected) -> int:
+    """Bytes of p covered by a greedy longest-match parse against the
+    selected patterns (dictionary.py:224-238), via kernels.overlap_batch."""
+    from . import kernels
+    sel = list(dict.fromkeys(bytes(s) for s in selected))
+    if not sel or not p:
+        return 0
+    trie = PatternTrie.from_patterns([(s, 0) for s in sel])
+    pats = np.zeros((1, max(len(p), 1)), np.uint8)
+    pats[0, :len(p)] = np.frombuffer(bytes(p), np.uint8)
+    out = np.empty(1, np.int64)
+    kernels.overlap_batch(trie.children, trie.term_len, pats, np.array([len(p)], np.int64), out)
+    return int(out[0])
+
+
+def _preprocess_all(lines, mode):
+    """[preprocess_line(l, mode) for l in lines] (dictionary.py:316-317) as
+    one GPU batch: strict raises the first failing line's error; lenient
+    keeps tokenize / pairing failures raw and raises RingIdOverflow."""
+    from .errors import ERR_BRACKET, ERR_PERCENT, ERR_UNPAIRED, from_kind
+    from .smiles import preprocess_batch
+    if mode not in ("strict", "lenient"):
+        raise ValueError(f"unknown mode {mode!r}")
+    out = []
+    for line, (kind, res) in zip(lines, preprocess_batch(lines)):
+        if kind == 0:
+            out.append(res)
+        elif mode == "lenient" and kind in (ERR_BRACKET, ERR_PERCENT, ERR_UNPAIRED):
+            out.append(bytes(line))
+        else:
+            off, ids = res
+            raise from_kind(kind, off, ids)
+    return out
+
+
+def generate(corpus, params: GenerationParams, mode: str = "strict") -> Dictionary:
+    """Train a dictionary on SMILES lines (dictionary.py:310-320), on the GPU."""
+    lines = [bytes(l) for l in corpus]
+    if not lines:
+        raise EmptyCorpus("no training lines")
+    if params.preprocess:
+        lines = _preprocess_all(lines, mode)
+    table = count_substrings(lines, params)
+    learned = select_patterns(table, params.t)
+    return Dictionary(learned, params.prepopulate, l_min=params.l_min, l_max=params.l_max)

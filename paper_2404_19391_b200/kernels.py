@@ -4,8 +4,8 @@ Same callables and array layouts as the reference's ``zsmiles.kernels``
 module (kernels/__init__.py:28-33; numba_impl.py:16-139), backed by the
 sm_100a parity-shim entry points of libzs.so.  There is a single backend
 and no CPU fallback (the north star drops multi-backend dispatch):
-``BACKEND == "sm_100a"``.  ``overlap_batch`` belongs to dictionary training
-and is out of scope.
+``BACKEND == "sm_100a"``.  ``overlap_batch`` (numba_impl.py:142-169) is the
+dictionary trainer's greedy-cover kernel.
 
 The tables arrive in the reference layouts on every call, exactly like the
 numba kernels; they are uploaded to the device once and cached by content.
@@ -147,3 +147,21 @@ def decompress_fill(exp_off, exp_flat, flat, starts, status, out, out_starts) ->
         ctx.check(rc, "zs_decompress_fill")
     if buf is not out:
         out[...] = buf
+
+
+def overlap_batch(children, term_len, pats, lens, out) -> None:
+    """out[r] = bytes of pats[r, :lens[r]] covered by a greedy longest-match
+    parse against the trie; unmatched positions advance one byte."""
+    ctx = _lib.context()
+    children = np.ascontiguousarray(children, np.int32)
+    term_len = np.ascontiguousarray(term_len, np.int16)
+    pats = np.ascontiguousarray(pats, np.uint8)
+    lens = np.ascontiguousarray(lens, np.int64)
+    n = int(lens.shape[0])
+    res = np.zeros(n, np.int64)
+    width = int(pats.shape[1]) if pats.ndim == 2 else 0
+    with ctx.lock:
+        rc = ctx.lib.zs_overlap_batch(ctx.h, _lib.ptr(children), _lib.ptr(term_len), children.shape[0],
+                                      _lib.ptr(pats), width, _lib.ptr(lens), n, _lib.ptr(res))
+        ctx.check(rc, "zs_overlap_batch")
+    out[:n] = res
