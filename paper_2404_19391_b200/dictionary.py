@@ -251,7 +251,7 @@ def count_substrings(corpus, params: GenerationParams) -> RankTable:
     lines = list(corpus)
     if not lines:
         raise EmptyCorpus("no training lines")
-    joined = b"\n".join(bytes(l) for l in lines)
+    joined = b"\n".join(lines)
     buf = np.frombuffer(joined or b"\0", np.uint8)
     _lib, ctx = _ctx()
     import ctypes
@@ -267,9 +267,9 @@ def count_substrings(corpus, params: GenerationParams) -> RankTable:
         ctx._train_gen = getattr(ctx, "_train_gen", 0) + 1
         token = (id(ctx), ctx._train_gen)
     width = params.l_max
-    src = np.frombuffer(joined + bytes(width), np.uint8)
     cols = np.arange(width, dtype=np.int64)
-    patterns = src[pos[:, None] + cols[None, :]] if n else np.zeros((0, width), np.uint8)
+    patterns = buf[np.minimum(pos[:, None] + cols[None, :], buf.size - 1)] if n else \
+        np.zeros((0, width), np.uint8)
     patterns = np.where(cols[None, :] < lens[:, None], patterns, 0).astype(np.uint8)
     lengths = lens.astype(np.int64)
     return RankTable(np.ascontiguousarray(patterns), lengths, occ, occ * lengths, _device=token)
@@ -338,7 +338,7 @@ def _preprocess_all(lines, mode):
 
 def generate(corpus, params: GenerationParams, mode: str = "strict") -> Dictionary:
     """Train a dictionary on SMILES lines (dictionary.py:310-320), on the GPU."""
-    lines = [bytes(l) for l in corpus]
+    lines = list(corpus)
     if not lines:
         raise EmptyCorpus("no training lines")
     if params.preprocess:
