@@ -93,10 +93,11 @@ struct HostTables {
 struct zs_ctx {
     int dev = 0;
     int n_sm = 0;
-    cudaStream_t stream[2] = {nullptr, nullptr};
+    static constexpr int NSLOT = 3;  // host pipeline depth (chunk k+3 reuses chunk k's buffers)
+    cudaStream_t stream[NSLOT] = {};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     const char *last_kernel = "";
-    cudaEvent_t ev_ctl[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+    cudaEvent_t ev_ctl[NSLOT] = {}, ev_out[NSLOT] = {};
     std::string err;
     bool have_dict = false;
     HostTables ht;
@@ -111,8 +112,8 @@ struct zs_ctx {
     int no_ip = 0;  // debug: force the decision-array kernel
     int dec_variant = 1;  // 1: per-thread slices (default), 0: warp-cooperative
     // per-slot (double-buffered) work buffers
-    DevBuf ctl[2], ts[2], terr[2], in[2], out[2], arena[2];  // arena: per slot
-    DevBuf fxs[2];  // streaming-decode scratch per slot
+    DevBuf ctl[NSLOT], ts[NSLOT], terr[NSLOT], in[NSLOT], out[NSLOT], arena[NSLOT];  // arena: per slot
+    DevBuf fxs[NSLOT];  // streaming-decode scratch per slot
     DevBuf ixs;     // record-index scratch
     // dictionary training (zs_train.cuh): corpus, census scratch, rank table, selection state
     struct {
@@ -671,13 +672,23 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
     // k+1's H2D and kernel (ZS_CHUNK_MB overrides, for measurements)
     static const long long CH = [] {
         const char *e = getenv("ZS_CHUNK_MB");
-        const long long mb = e ? atoll(e) : 32;
-        return (mb > 0 ? mb : 32) << 20;
+        const long long mb = e ? atoll(e) : 64;
+        return (mb > 0 ? mb : 64) << 20;
     }();
-    // chunk boundaries just past a newline
+    // chunk boundaries just past a newline.  Sizes ramp up from CH/16 (the
+    // first D2H / kernel starts after a short H2D) and back down over the
+    // last ~CH bytes (a short tail of kernel + D2H after the last H2D);
+    // decompress chunks are 3/8 as large (the output is ~2.6x the input).
+    const long long ch = compress ? CH : std::max<long long>(CH * 3 / 8, 1 << 20);
+    const long long lo = std::max<long long>(ch >> 4, 1 << 18);
+    long long up = lo;
     std::vector<long long> cuts{0};
     while (cuts.back() < n) {
-        long long s = cuts.back(), e = std::min<long long>(n, s + CH);
+        const long long s = cuts.back(), rem = n - s;
+        long long size = std::min(up, ch);
+        up *= 2;
+        if (rem < 2 * size) size = std::max(lo, rem / 2);
+        long long e = std::min<long long>(n, s + size);
         if (e < n) {
             const void *nl = memchr(h_in + e, '\n', (size_t)(n - e));
             e = nl ? (long long)((const uint8_t *)nl - h_in) + 1 : n;
@@ -685,6 +696,19 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
         cuts.push_back(e);
     }
     const int nch = (int)cuts.size() - 1;
+    // ZS_TRACE=1: per-chunk event timeline on stderr (H2D end, kernel end,
+    // D2H end, ms from the call's start) -- a measurement aid
+    static const bool trace = getenv("ZS_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    if (trace) {
+        tev.resize(1 + 3 * (size_t)nch);
+        for (auto &e : tev) cudaEventCreate(&e);
+        cudaEventRecord(tev[0], ctx->stream[0]);
+    }
+    auto mark = [&](int k, int what, int slot) {
+        if (trace) cudaEventRecord(tev[1 + 3 * k + what], ctx->stream[slot]);
+    };
+    std::vector<int> chunk_of_slot(zs_ctx::NSLOT, -1);
     long long written = 0, line_base = 0;
     bool general = false;  // a chunk hit a bad record: the record-aware kernel from then on
     bool capacity_hit = false;
@@ -705,6 +729,7 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
         if (!capacity_hit && written + ob <= out_cap && ob > 0 && !r.err_line)
             CK(cudaMemcpyAsync(h_out + written, ctx->out[slot].p, ob, cudaMemcpyDeviceToHost,
                                ctx->stream[slot]));
+        mark(chunk_of_slot[slot], 2, slot);
         if (written + ob > out_cap) capacity_hit = true;
         CK(cudaEventRecord(ctx->ev_out[slot], ctx->stream[slot]));
         written += ob;
@@ -725,17 +750,20 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
         return ZS_OK;
     };
     for (int k = 0; k < nch && !res->err_line; ++k) {
-        const int slot = k & 1;
+        const int slot = k % zs_ctx::NSLOT;
         const long long cs = cuts[k], cn = cuts[k + 1] - cs;
         // slot reuse: its previous output copy must be done
         CK(cudaEventSynchronize(ctx->ev_out[slot]));
         if (ctx->in[slot].reserve(cn + 16) || ctx->out[slot].reserve(out_bound(cn)))
             return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(chunk)");
         CK(cudaMemcpyAsync(ctx->in[slot].p, h_in + cs, cn, cudaMemcpyHostToDevice, ctx->stream[slot]));
+        chunk_of_slot[slot] = k;
+        mark(k, 0, slot);
         int rc = launch_stream(ctx, slot, compress, ctx->in[slot].as<uint8_t>(), cn,
                                ctx->out[slot].as<uint8_t>(), (long long)ctx->out[slot].cap, flags,
                                false);
         if (rc) return rc;
+        mark(k, 1, slot);
         if (pending >= 0) {
             rc = finish(pending, pend_n, pend_len);
             while (rc >= 10) {  // re-run the previous chunk synchronously with bigger buffers
@@ -775,8 +803,16 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
         }
         if (rc) return rc;
     }
-    CK(cudaStreamSynchronize(ctx->stream[0]));
-    CK(cudaStreamSynchronize(ctx->stream[1]));
+    for (int s = 0; s < zs_ctx::NSLOT; ++s) CK(cudaStreamSynchronize(ctx->stream[s]));
+    if (trace) {
+        for (int k = 0; k < nch; ++k) {
+            float t[3] = {0, 0, 0};
+            for (int w = 0; w < 3; ++w) cudaEventElapsedTime(&t[w], tev[0], tev[1 + 3 * k + w]);
+            fprintf(stderr, "zs_trace %s chunk %d %lld B: h2d %.3f kernel %.3f d2h %.3f ms\n",
+                    compress ? "c" : "d", k, cuts[k + 1] - cuts[k], t[0], t[1], t[2]);
+        }
+        for (auto &e : tev) cudaEventDestroy(e);
+    }
     res->in_bytes = n;
     res->out_bytes = written;
     if (!trailing && res->lines > 0) res->out_bytes -= 1;
@@ -808,7 +844,7 @@ int zs_ctx_create(int device, zs_ctx **out) {
     ctx->dev = device;
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, device);
-    for (int s = 0; s < 2 && e == cudaSuccess; ++s) {
+    for (int s = 0; s < zs_ctx::NSLOT && e == cudaSuccess; ++s) {
         e = cudaStreamCreateWithFlags(&ctx->stream[s], cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_ctl[s], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_out[s], cudaEventDisableTiming);
@@ -816,7 +852,7 @@ int zs_ctx_create(int device, zs_ctx **out) {
     }
     if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
-    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_ctl, 2 * sizeof(Ctl));
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_ctl, zs_ctx::NSLOT * sizeof(Ctl));
     if (e != cudaSuccess) {
         delete ctx;
         return ZS_E_CUDA;
@@ -829,9 +865,7 @@ int zs_ctx_destroy(zs_ctx *ctx) {
     if (!ctx) return ZS_OK;
     cudaSetDevice(ctx->dev);
     for (DevBuf *b : {&ctx->d_dfa2, &ctx->d_t2, &ctx->d_dfa, &ctx->d_codes, &ctx->d_children, &ctx->d_term, &ctx->d_explen,
-                      &ctx->d_expoff, &ctx->d_expflat, &ctx->d_fxc, &ctx->d_fxe, &ctx->d_cxdfa, &ctx->d_cxt2, &ctx->d_cxcodes, &ctx->d_cxcmap, &ctx->fxs[0], &ctx->fxs[1], &ctx->ixs, &ctx->ctl[0], &ctx->ctl[1], &ctx->ts[0],
-                      &ctx->ts[1], &ctx->terr[0], &ctx->terr[1], &ctx->in[0], &ctx->in[1],
-                      &ctx->out[0], &ctx->out[1], &ctx->arena[0], &ctx->arena[1], &ctx->s_flat, &ctx->s_starts,
+                      &ctx->d_expoff, &ctx->d_expflat, &ctx->d_fxc, &ctx->d_fxe, &ctx->d_cxdfa, &ctx->d_cxt2, &ctx->d_cxcodes, &ctx->d_cxcmap, &ctx->ixs, &ctx->s_flat, &ctx->s_starts,
                       &ctx->s_out, &ctx->s_lens, &ctx->s_dec, &ctx->s_stat, &ctx->s_errpos,
                       &ctx->s_tot, &ctx->s_ids, &ctx->s_outst, &ctx->tr.buf, &ctx->tr.run, &ctx->tr.pos[0],
                       &ctx->tr.pos[1], &ctx->tr.key[0], &ctx->tr.key[1], &ctx->tr.lcp, &ctx->tr.runs, &ctx->tr.v,
@@ -840,7 +874,10 @@ int zs_ctx_destroy(zs_ctx *ctx) {
                       &ctx->tr.idx[1], &ctx->tr.dead, &ctx->tr.child, &ctx->tr.term, &ctx->tr.ctl, &ctx->tr.blk,
                       &ctx->tr.sel})
         b->release();
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < zs_ctx::NSLOT; ++s) {
+        for (DevBuf *b : {&ctx->fxs[s], &ctx->ctl[s], &ctx->ts[s], &ctx->terr[s], &ctx->in[s], &ctx->out[s],
+                          &ctx->arena[s]})
+            b->release();
         if (ctx->stream[s]) cudaStreamDestroy(ctx->stream[s]);
         if (ctx->ev_ctl[s]) cudaEventDestroy(ctx->ev_ctl[s]);
         if (ctx->ev_out[s]) cudaEventDestroy(ctx->ev_out[s]);
