@@ -105,6 +105,7 @@ struct zs_ctx {
     int fast_w = 0;
     DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2, d_fxc, d_fxe, d_cxdfa, d_cxt2, d_cxcodes, d_cxcmap;
     int no_cx = 0;  // debug: force the queue-based compress kernel
+    int p4_lane = 0;  // debug: parse per line-lane range instead of byte-exact slices
     bool fx_ok = false;  // streaming decode kernel serves this dictionary (max expansion <= 7)
     int fx_blocks[2] = {0, 0};  // resident fx_count / fx_emit CTAs per SM
     int fx_wide = -1;           // fx_blocks were sized for this emit variant
@@ -506,7 +507,7 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
             CK(set_smem(compress_cx, L.bytes));
             CxTables ct{ctx->d_cxdfa.as<uint16_t>(), ctx->d_cxt2.as<uint16_t>(), ctx->d_cxcodes.as<uint8_t>(),
                         ctx->d_cxcmap.as<uint8_t>(), ctx->ht.cx_states, ctx->ht.n_windows, ctx->ht.cx_cols,
-                        L.o_t2, L.o_codes};
+                        L.o_t2, L.o_codes, ctx->p4_lane ? 0 : 1};
             const int g2 = (int)std::min<long long>(nt, (long long)ctx->n_sm * CX_CTAS);
             compress_cx<<<g2, CX_NT, L.bytes, st>>>(job, ctx->tb, ct);
             ctx->last_kernel = "compress_cx";
@@ -1031,6 +1032,7 @@ int zs_set_transducer(zs_ctx *ctx, int on) {
     ctx->no_t2 = (on & 1) ? 0 : 1;  // bit 0: transducer parse
     ctx->no_ip = (on & 2) ? 0 : 1;  // bit 1: in-place kernel (needs the transducer)
     ctx->no_cx = (on & 8) ? 1 : 0;  // bit 3: queue-based in-place kernel instead of the lane-chunk one
+    ctx->p4_lane = (on & 16) ? 1 : 0;  // bit 4: lane-chunk parse over line-lane ranges (not byte slices)
     return ZS_OK;
 }
 

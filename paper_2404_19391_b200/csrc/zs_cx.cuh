@@ -50,6 +50,8 @@ constexpr int CX_CODES = 16;                      // code slots per state: 0 esc
 constexpr int CX_OUTCAP = 13312;                  // staging (ratio <= ~0.5)
 constexpr int CX_RARE = 64;                       // rare lines per tile
 constexpr int CX_JOBS = 16;                       // '%nn' compactions per warp and tile
+constexpr int CX_WARM = 32;                       // P4 warm-up bytes right of a slice (speculative entry)
+constexpr int CX_XLONG = 4 * CX_CC;               // P4 uses byte-exact slices when a line-lane range is longer
 
 // rare-line kinds
 enum : int { RK_DROP = 1, RK_ARENA = 2, RK_STRICT = 3 };
@@ -109,6 +111,7 @@ struct CxTables {
     const uint8_t *cmap;   // [256]
     int ns, nw, nc;
     int o_t2, o_codes;     // smem offsets (cx_layout)
+    int p4x;               // 1: byte-exact parse slices (default), 0: parse the lane's line range
 };
 
 struct CxSmem {
@@ -336,12 +339,13 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
     __shared__ int s_tmp[CX_NW];
     __shared__ unsigned long long s_tmp64[CX_NW];
     __shared__ long long s_tile;
-    __shared__ int s_head_nl, s_last_nl, s_nrare, s_err_ord;
+    __shared__ int s_head_nl, s_last_nl, s_nrare, s_err_ord, s_r0;
     __shared__ unsigned s_esc, s_skip, s_flag, s_inl;
     __shared__ unsigned long long s_pre_out, s_pre_lines;
 
     __shared__ __align__(16) uint8_t s_lut[8 * 256];  // tokenizer transducer (static: constant addresses)
     __shared__ __align__(16) uint8_t s_explen[256];
+    __shared__ __align__(16) uint8_t s_exp0[256];  // first byte of each code's expansion (P4 re-parse)
     __shared__ __align__(16) uint8_t s_cmap[256];
     CxSmem S = cx_carve(smem, ct.o_t2, ct.o_codes);
     S.lut = s_lut;
@@ -354,6 +358,8 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         for (int k = threadIdx.x; k < ct.ns * CX_CODES; k += CX_NT) S.codes[k] = ct.codes[k];
         for (int k = threadIdx.x; k < 256; k += CX_NT) s_cmap[k] = ct.cmap[k];
         for (int k = threadIdx.x; k < 256; k += CX_NT) S.explen[k] = k == '\n' ? 1 : tb.exp_len[k];
+        for (int k = threadIdx.x; k < 256; k += CX_NT)
+            s_exp0[k] = k == '\n' ? (uint8_t)'\n' : (tb.exp_len[k] ? tb.exp_flat[tb.exp_off[k]] : (uint8_t)k);
         for (int k = threadIdx.x; k < 8 * 256; k += CX_NT) {
             const unsigned st = k >> 8, b = k & 255;
             uint8_t e = tk_entry(st, b) & ~(TK_ENTER_BR | TK_ENTER_PCT);  // bits 5/6: line-end errors only
@@ -378,6 +384,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
             s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
             s_nrare = 0;
             s_err_ord = 0x7fffffff;
+            s_r0 = 0x7fffffff;
             s_esc = s_skip = s_flag = 0;
         }
         __syncthreads();
@@ -765,13 +772,27 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         }
 
         pc.mark(job, 2);  // warp 0: pairing
-        // ---- P4: min-cost parse, right to left over the lane's range ----
+        // ---- P4: min-cost parse, right to left ----
         // Branch-free: code slot 0 of every state is 0x20, so an escape
         // decision writes the escape byte (its literal is re-read from HBM by
-        // the emit).  Whole 4-byte words inside the range are read and written
+        // the emit).  Whole 4-byte words inside a range are read and written
         // with one 32-bit access each (the words at the range ends bytewise:
         // they are shared with the neighbouring lanes).
+        //
+        // Byte-exact slices (ct.p4x): the tile's owned bytes [R0, R1] are cut
+        // into CX_NT equal slices, so every lane parses the same number of
+        // bytes whatever the line lengths.  A slice's right end is entered
+        // with the state a newline leaves (exact) or, when no newline lies
+        // within CX_WARM bytes to its right, with the state of a K-byte
+        // warm-up from a virtual line end (the (DFA state, cost window) pair
+        // resynchronises within a few bytes).  After the parse every slice
+        // publishes its exit state; a speculative entry that differs from
+        // its right neighbour's exit is parsed again from the true state
+        // (bytes rebuilt from the decisions), until none differs.  The
+        // bias-corrected cost of each piece of a slice goes to the line-lane
+        // that owns those bytes (lane_b), so P5 / P6 stay per line-lane.
         unsigned acc = 0;
+        bool p4_exact = false;
         {
             const uint16_t *__restrict__ dfa = S.dfa;
             const uint16_t *__restrict__ t2 = S.t2;
@@ -788,13 +809,13 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 const unsigned L = (x >> 9) & 15u;
                 return L == 1 ? b : codes[st * CX_CODES + L];  // length 1: the identity code is the byte
             };
-            if (start <= end) {
-                const int lo_w = (start + 3) & ~3;  // first whole word inside the range
-                const int hi_w = (end + 1) & ~3;    // end of the last whole word (exclusive)
-                int i = end;
-                // right end, bytewise
-                for (; i >= max(hi_w, start); --i) win[i] = (uint8_t)step(win[i]);
-                // whole words
+            // parse [lo, hi] right to left, decisions in place
+            auto parse_range = [&](int lo, int hi) {
+                if (lo > hi) return;
+                const int lo_w = (lo + 3) & ~3;  // first whole word inside the range
+                const int hi_w = (hi + 1) & ~3;  // end of the last whole word (exclusive)
+                int i = hi;
+                for (; i >= max(hi_w, lo); --i) win[i] = (uint8_t)step(win[i]);
                 if (lo_w < hi_w) {
                     unsigned *w32 = reinterpret_cast<unsigned *>(win);
                     unsigned cur = w32[(hi_w >> 2) - 1];
@@ -809,8 +830,120 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                     }
                     i = lo_w - 1;
                 }
-                // left end, bytewise
-                for (; i >= start; --i) win[i] = (uint8_t)step(win[i]);
+                for (; i >= lo; --i) win[i] = (uint8_t)step(win[i]);
+            };
+            // byte-exact slices pay a warm-up of up to CX_WARM bytes per lane:
+            // worth it only when line-lane ranges are much longer than a slice
+            // (long lines); every warp derives the same decision from lane_a
+            int mx = 0;
+            if (ct.p4x) {
+                for (int k = lane; k < CX_NT; k += 32)
+                    mx = max(mx, (k + 1 < CX_NT ? S.lane_a[k + 1] : s_last_nl) - S.lane_a[k]);
+                mx = __reduce_max_sync(0xffffffffu, mx);
+            }
+            p4_exact = mx > CX_XLONG;
+            if (!p4_exact) {
+                parse_range(start, end);
+            } else {
+                if (start <= end) atomicMin(&s_r0, start);
+                __syncthreads();  // P2 / P3 of every warp done (slices cross line-lanes); R0 known
+                const int R0 = s_r0, R1 = s_last_nl;
+                const int sz = R1 >= R0 ? (R1 - R0 + CX_NT) / CX_NT : 0;
+                const int s0 = R0 + tid * sz, e0 = min(R1, s0 + sz - 1);
+                bool spec = false, found = false;
+                unsigned spec_state = 0, racc = 0;
+                int rlo = s0, rj = 0;
+                if (sz > 0 && s0 <= e0) {
+                    // entry state at e0
+                    if (win[e0] != '\n') {
+                        // every such entry is checked below, also when a newline was
+                        // found (the check does not depend on when the right
+                        // neighbour rewrites these bytes; it rewrites them last)
+                        spec = true;
+                        const int lim = min(e0 + CX_WARM, R1);
+                        int p = e0 + 1;
+                        while (p < lim && win[p] != '\n') ++p;  // R1 is a newline
+                        found = win[p] == '\n';
+                        if (!found) step('\n');                   // a virtual line end right of the warm-up
+                        for (; p > e0; --p) step(win[p]);
+                        spec_state = (wi << 16) | st;
+                    }
+                    __syncwarp();
+                    // the line-lane owning e0: the last lane whose cut lies before it
+                    int lo = 0, hi = CX_NT - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (S.lane_a[mid] < e0) lo = mid;
+                        else hi = mid - 1;
+                    }
+                    int j = lo, h = e0;
+                    bool first_piece = true;
+                    for (;;) {
+                        const int l = max(s0, S.lane_a[j] + 1);
+                        acc = 0;
+                        parse_range(l, h);
+                        atomicAdd(&S.lane_b[j], (int)acc - 4 * (h - l + 1));
+                        if (first_piece) {
+                            racc = acc;
+                            rlo = l;
+                            rj = j;
+                            first_piece = false;
+                        }
+                        if (l <= s0) break;
+                        h = l - 1;
+                        do {
+                            --j;
+                        } while (j > 0 && S.lane_a[j] >= h);
+                    }
+                } else {
+                    __syncwarp();
+                }
+                S.lane_c[tid] = (int)((wi << 16) | st);  // exit state (read by the left neighbour)
+                __syncthreads();
+                // verify speculative entries against the right neighbour's exit
+                for (int round = 0;; ++round) {
+                    unsigned truth = 0;
+                    bool need = false;
+                    if (spec) {
+                        truth = (unsigned)S.lane_c[tid + 1];
+                        need = truth != spec_state;
+                    }
+                    if (job.timing == 6 && round == 0) {  // debug: entries and first-round mismatches by warm-up kind
+                        const unsigned F = 0xffffffffu;
+                        if (lane == 0) {
+                            atomicAdd(&job.ctl->phase[0], (unsigned long long)__popc(__ballot_sync(F, spec && found)));
+                            atomicAdd(&job.ctl->phase[1], (unsigned long long)__popc(__ballot_sync(F, spec && !found)));
+                            atomicAdd(&job.ctl->phase[2], (unsigned long long)__popc(__ballot_sync(F, need && found)));
+                            atomicAdd(&job.ctl->phase[3], (unsigned long long)__popc(__ballot_sync(F, need && !found)));
+                        } else {
+                            __ballot_sync(F, spec && found);
+                            __ballot_sync(F, spec && !found);
+                            __ballot_sync(F, need && found);
+                            __ballot_sync(F, need && !found);
+                        }
+                    }
+                    if (!__syncthreads_or(need)) break;
+                    if (need) {
+                        // rebuild the piece's bytes from its decisions, parse it again
+                        for (int p = rlo; p <= e0; ++p) {
+                            const unsigned d = win[p];
+                            unsigned b;
+                            if (d == 0x20u) b = cx_bit(S.fbits, p) ? 0x01u : job.in[ws + p];
+                            else b = s_exp0[d];
+                            win[p] = (uint8_t)b;
+                        }
+                        st = truth & 0xffffu;
+                        wi = truth >> 16;
+                        acc = 0;
+                        parse_range(rlo, e0);
+                        atomicAdd(&S.lane_b[rj], (int)acc - (int)racc);
+                        racc = acc;
+                        spec_state = truth;
+                        if (rlo == s0) S.lane_c[tid] = (int)((wi << 16) | st);
+                    }
+                    __syncthreads();
+                }
+                acc = 0;
             }
         }
         pc.mark(job, 3);  // warp 0: parse
@@ -847,7 +980,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
             if (R.kind == RK_STRICT) s_err_ord = 0;  // ordinal resolved after the scan
         }
         __syncthreads();
-        const int nbytes = end >= start ? end - start + 1 : 0;
+        const int nbytes = (!p4_exact && end >= start) ? end - start + 1 : 0;  // exact slices: costs are in lane_b
         const long long my_out = (long long)acc - 4ll * nbytes - sub + S.lane_b[tid];
         // ---- P5: tile output bytes and lines (one scan); publish ----
         unsigned long long tot;

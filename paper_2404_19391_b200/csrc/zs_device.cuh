@@ -138,7 +138,7 @@ struct PhaseClock {
     long long t;
     __device__ __forceinline__ void start() { t = clock64(); }
     __device__ __forceinline__ void mark(const Job &job, int k) {
-        if (job.timing != 2 && job.timing && threadIdx.x == 0) {
+        if (job.timing != 2 && job.timing != 6 && job.timing && threadIdx.x == 0) {
             long long now = clock64();
             atomicAdd(&job.ctl->phase[k], (unsigned long long)(now - t));
             t = now;

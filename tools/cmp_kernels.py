@@ -1,5 +1,6 @@
 """Compress kernel comparison (device API, HBM-resident input): lane-chunk
-(mode 3, default) vs queue-based in-place kernel (mode 11).
+(mode 3, default: byte-exact parse slices), lane-chunk parsing line ranges
+(mode 19) and the queue-based in-place kernel (mode 11).
 
     python tools/cmp_kernels.py [lines]
 """
@@ -25,7 +26,7 @@ def main():
         dout = torch.empty(2 * buf.size + 64, dtype=torch.uint8, device="cuda")
         r = _lib.Result()
         outs = {}
-        for mode in (3, 11):
+        for mode in (3, 19, 11):
             ctx.lib.zs_set_transducer(ctx.h, mode)
             for _ in range(3):
                 rc = ctx.lib.zs_compress_device(ctx.h, din.data_ptr(), buf.size, dout.data_ptr(), dout.numel(),
@@ -36,6 +37,7 @@ def main():
             print(f"{kind:9s} {buf.size / 1e6:8.1f} MB mode {mode:2d} {ctx.lib.zs_last_kernel(ctx.h).decode():22s} "
                   f"{ms:8.3f} ms {buf.size / ms / 1e6:8.1f} GB/s")
         assert outs[3] == outs[11], kind
+        assert outs[19] == outs[11], kind
     ctx.lib.zs_set_transducer(ctx.h, 3)
 
 

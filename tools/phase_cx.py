@@ -25,6 +25,7 @@ def main():
     d = z.default_dictionary()
     ctx = _lib.context()
     ctx.set_dictionary(d)
+    ctx.lib.zs_set_transducer(ctx.h, int(os.environ.get("MODE", "3")))
     din = torch.from_numpy(buf).cuda()
     dout = torch.empty(2 * buf.size + 64, dtype=torch.uint8, device="cuda")
     r = _lib.Result()
