@@ -176,6 +176,18 @@ __device__ __forceinline__ unsigned cx_bit(const unsigned *bm, int p) { return (
 __device__ __forceinline__ void cx_set(unsigned *bm, int p) { atomicOr(&bm[p >> 5], 1u << (p & 31)); }
 __device__ __forceinline__ void cx_clr(unsigned *bm, int p) { atomicAnd(&bm[p >> 5], ~(1u << (p & 31))); }
 
+// set bits of bm in window positions [a, b]
+__device__ __forceinline__ int cx_popc_range(const unsigned *bm, int a, int b) {
+    int n = 0;
+    for (int w = a >> 5; a <= b && w <= (b >> 5); ++w) {
+        unsigned m = bm[w];
+        if (w == (a >> 5)) m &= 0xffffffffu << (a & 31);
+        if (w == (b >> 5) && (b & 31) != 31) m &= (2u << (b & 31)) - 1u;
+        n += __popc(m);
+    }
+    return n;
+}
+
 // first set bit at position >= p (bm bits beyond the window are never set;
 // callers bound the search by a position known to be set)
 __device__ __forceinline__ int cx_next(const unsigned *bm, int p) {
@@ -334,12 +346,30 @@ __device__ __forceinline__ void cx_rare(const CxSmem &S, int *n, int ls, int le,
     }
 }
 
+// clear the ring-token bits of window positions [a, b] (newline bits stay)
+__device__ __forceinline__ void cx_clear_ring_bits(const CxSmem &S, int a, int b) {
+    for (int w = a >> 5; a <= b && w <= (b >> 5); ++w) {
+        unsigned m = 0xffffffffu;
+        if (w == (a >> 5)) m &= 0xffffffffu << (a & 31);
+        if (w == (b >> 5) && (b & 31) != 31) m &= (2u << (b & 31)) - 1u;
+        unsigned nl = 0;
+        const unsigned *w4 = reinterpret_cast<const unsigned *>(S.win + w * 32);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const unsigned x = w4[k] ^ 0x0a0a0a0au;
+            const unsigned z = ~(((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x | 0x7f7f7f7fu);
+            nl |= (((z >> 7) & 1u) | ((z >> 14) & 2u) | ((z >> 21) & 4u) | ((z >> 28) & 8u)) << (4 * k);
+        }
+        atomicAnd(&S.rbits[w], ~(m & ~nl));
+    }
+}
+
 __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb, CxTables ct) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int s_tmp[CX_NW];
     __shared__ unsigned long long s_tmp64[CX_NW];
     __shared__ long long s_tile;
-    __shared__ int s_head_nl, s_last_nl, s_nrare, s_err_ord, s_r0;
+    __shared__ int s_head_nl, s_last_nl, s_nrare, s_err_ord, s_r0, s_r2;
     __shared__ unsigned s_esc, s_skip, s_flag, s_inl;
     __shared__ unsigned long long s_pre_out, s_pre_lines;
 
@@ -384,7 +414,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
             s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
             s_nrare = 0;
             s_err_ord = 0x7fffffff;
-            s_r0 = 0x7fffffff;
+            s_r0 = s_r2 = 0x7fffffff;
             s_esc = s_skip = s_flag = 0;
         }
         __syncthreads();
@@ -505,6 +535,17 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         // a CR or a tokenize error walks it again with the per-line handling.
         // Ring-token bits gather in a register per 32-byte bitmap word.
         int nlines = glob ? 1 : 0;
+        // Long line-lane ranges (long lines): P2 and P4 walk byte-exact slices
+        // instead (they pay a warm-up of up to CX_WARM bytes per lane, worth
+        // it only when a line-lane range is much longer than a slice).  Every
+        // warp derives the same decision from lane_a.
+        bool long_ranges = false;
+        if (ct.p4x) {
+            int mx = 0;
+            for (int k = lane; k < CX_NT; k += 32)
+                mx = max(mx, (k + 1 < CX_NT ? S.lane_a[k + 1] : s_last_nl) - S.lane_a[k]);
+            long_ranges = __reduce_max_sync(0xffffffffu, mx) > CX_XLONG;
+        }
         {
             const uint8_t *__restrict__ lut = S.lut;
             const unsigned *__restrict__ w32 = reinterpret_cast<const unsigned *>(S.win);
@@ -570,7 +611,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
             // the fast walk: whole words of 4 bytes; per word the four LUT
             // entries are combined once for the flags, the ring-token nibble
             // and the newline count
-            auto walk_fast = [&]() {
+            auto walk_fast_range = [&](const int first, const int end) {
                 int p = first;
                 const int w0 = (first + 3) & ~3, w1 = (end + 1) & ~3;
                 if (w0 < w1) {
@@ -600,8 +641,70 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 flush(end);
                 flags |= (flags >> 8) | (flags >> 16) | (flags >> 24);
             };
-            if (first <= end) {
-                walk_fast();
+            bool regular = true;
+            if (long_ranges) {
+                // ---- P2 on byte-exact slices ----
+                // A slice is entered in the tokenizer state a newline leaves
+                // (found within CX_WARM bytes to its left, or the region start),
+                // else in the state of a warm-up from TK_OUT0; such a guess is
+                // checked against the left neighbour's exit state and the slice
+                // walked again (its ring bits cleared first) until none
+                // differs.  A CR or a tokenize error anywhere sends every
+                // line-lane through the per-line walk below instead.
+                nlines += cx_popc_range(S.rbits, first, end);  // the bitmap holds only newlines yet
+                if (first <= end) atomicMin(&s_r2, first);
+                __syncthreads();
+                const int R0 = s_r2, R1 = s_last_nl;
+                const int sz = R1 >= R0 ? (R1 - R0 + CX_NT) / CX_NT : 0;
+                const int s0 = R0 + tid * sz, e0 = min(R1, s0 + sz - 1);
+                bool spec = false;
+                unsigned spec_state = TK_OUT0;
+                const int nl_keep = nlines;
+                flags = 0;
+                st = TK_OUT0;
+                if (sz > 0 && s0 <= e0) {
+                    if (s0 > R0 && S.win[s0 - 1] != '\n') {
+                        const int lim = max(R0, s0 - CX_WARM);
+                        int p = s0 - 1;
+                        while (p > lim && S.win[p] != '\n') --p;
+                        if (S.win[p] == '\n') ++p;
+                        else spec = p > R0;  // R0 is a line start
+                        for (; p < s0; ++p) st = lut[(st << 8) | S.win[p]] & 7u;
+                        spec_state = st;
+                    }
+                    walk_fast_range(s0, e0);
+                }
+                S.lane_c[tid] = (int)st;  // exit state (read by the right neighbour)
+                __syncthreads();
+                for (;;) {
+                    bool need = false;
+                    unsigned truth = 0;
+                    if (spec) {
+                        truth = (unsigned)S.lane_c[tid - 1];
+                        need = truth != spec_state;
+                    }
+                    if (!__syncthreads_or(need)) break;
+                    if (need) {
+                        cx_clear_ring_bits(S, s0, e0);
+                        st = truth;
+                        flags = 0;
+                        walk_fast_range(s0, e0);
+                        spec_state = truth;
+                        S.lane_c[tid] = (int)st;
+                    }
+                    __syncthreads();
+                }
+                nlines = nl_keep;
+                regular = __syncthreads_or((flags & 0x70u) != 0u) != 0;
+                if (regular) {  // rare: per-line walks over the line-lanes (ring bits are set again, idempotently)
+                    nlines = glob ? 1 : 0;
+                    st = TK_OUT0;
+                    flags = 0;
+                    rmask = 0;
+                }
+            }
+            if (regular && first <= end) {
+                walk_fast_range(first, end);
                 if (flags & 0x70u) {  // a CR or a tokenize error in the range (rare)
                     nlines = glob ? 1 : 0;
                     st = TK_OUT0;
@@ -832,16 +935,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 }
                 for (; i >= lo; --i) win[i] = (uint8_t)step(win[i]);
             };
-            // byte-exact slices pay a warm-up of up to CX_WARM bytes per lane:
-            // worth it only when line-lane ranges are much longer than a slice
-            // (long lines); every warp derives the same decision from lane_a
-            int mx = 0;
-            if (ct.p4x) {
-                for (int k = lane; k < CX_NT; k += 32)
-                    mx = max(mx, (k + 1 < CX_NT ? S.lane_a[k + 1] : s_last_nl) - S.lane_a[k]);
-                mx = __reduce_max_sync(0xffffffffu, mx);
-            }
-            p4_exact = mx > CX_XLONG;
+            p4_exact = long_ranges;
             if (!p4_exact) {
                 parse_range(start, end);
             } else {
