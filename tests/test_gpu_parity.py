@@ -305,6 +305,35 @@ def test_errors_across_tiles():
     _oracle_check(b"\n".join(recs), d, False, False, "decompress")
 
 
+def test_long_line_tiles_edge_cases():
+    """Tiles of long lines run the byte-exact tokenizer / parse slices
+    (speculative entries, neighbour checks, re-walks) and fall back to the
+    per-line tokenizer on a CR or tokenize error: errors, '%nn' ids, colour
+    overflow, unpaired rings and escaped bytes inside long lines."""
+    d = z.default_dictionary()
+    base = synth.generate("skewed", 12000, 2025).tobytes().split(b"\n")[:-1]
+    rng = random.Random(77)
+    nest = b"C1C2C3C4C5CCCCC5C4C3C2C1"                  # 5 nested rings: colour 4
+    pct = b"C%12CC%34CC%34CC%12"
+    edits = [b"CC\rO", b"C[NH", b"C%1C", b"C1CC", nest, pct, b"C\tC", b"c1cc\xffcc1"]
+    for k, bad in enumerate(edits):
+        lines = list(base)
+        for _ in range(3):
+            i = rng.randrange(len(lines))
+            j = rng.randrange(len(lines[i]) + 1)
+            lines[i] = lines[i][:j] + bad + lines[i][j:]
+        payload = b"\n".join(lines) + (b"\n" if k % 2 == 0 else b"")
+        for lenient in (False, True):
+            _oracle_check(payload, d, True, lenient)
+        _oracle_check(payload, d, False, True)
+    # long lines without any newline for many slices, and one-line tiles
+    mols = [m for m in base if len(m) > 100][:40]
+    payload = b"\n".join(b"C".join(mols[i:i + 8]) for i in range(0, 40, 8)) + b"\n"
+    for pre in (False, True):
+        want = _oracle_check(payload, d, pre, True)
+        _oracle_check(want, d, False, True, "decompress")
+
+
 def test_strict_partial_output_matches_reference_batches():
     d = z.Dictionary([], "smiles")
     lines = [b"CCO"] * 300 + [b"C1CC"] + [b"CCO"] * 50
