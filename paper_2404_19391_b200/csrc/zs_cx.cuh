@@ -63,6 +63,7 @@ struct CxRare {
     int local;         // line index within the lane
     int err;           // E_* (strict errors)
     unsigned aoff;     // arena offset / 16 (RK_ARENA)
+    int out;           // output bytes of the arena line incl. its '\n' (RK_ARENA)
     int glob;          // the line starts before the window (only its '\n' at le is staged)
     long long gs;      // global offset of the line's first byte (RK_ARENA)
 };
@@ -1067,6 +1068,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 } else {
                     if (kind == -3) atomicAdd(&s_flag, 1u);
                     R.aoff = aoff;
+                    R.out = (int)cost + 1;
                     atomicAdd(&S.lane_b[R.lane], (int)cost + 1);
                 }
             }
@@ -1087,9 +1089,85 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         const bool staged = tile_out <= (unsigned long long)CX_OUTCAP;
         pc.mark(job, 5);  // output scan
         // ---- P6: emit (to staging now, or to HBM after the look-back) ----
+        // Long-line tiles emit byte-exact slices: a slice starts at the first
+        // decision at or after its first byte on the path the reference's
+        // forward walk takes (numba_impl.py:57-69) -- found from a line start
+        // within CX_WARM bytes to its left, or guessed from a walk started
+        // CX_WARM bytes left and checked against the left neighbour's exit --
+        // then counts its output bytes (one scan gives the slice offsets) and
+        // emits them.
+        int p6a = start, p6b = end;
+        unsigned long long p6off = my_off;
+        if (long_ranges) {
+            const uint8_t *win = S.win;
+            const int R0 = s_r0, R1 = s_last_nl;
+            const int sz = R1 >= R0 ? (R1 - R0 + CX_NT) / CX_NT : 0;
+            const int s0 = R0 + tid * sz, e0 = min(R1, s0 + sz - 1);
+            auto marker_out = [&](int p) {
+                int o = 0;
+                for (int r = 0; r < n_rare; ++r)
+                    if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p) o += S.rare[r].out;
+                return o;
+            };
+            auto count = [&](int p, unsigned &cnt) {  // walk [p, e0]; returns the exit position
+                cnt = 0;
+                while (p <= e0) {
+                    const unsigned d = win[p];
+                    if (d == 0x20u) {
+                        cnt += cx_bit(S.fbits, p) ? (unsigned)marker_out(p) : 2u;
+                        ++p;
+                    } else {
+                        ++cnt;
+                        p += S.explen[d];
+                    }
+                }
+                return p;
+            };
+            int c = s0, x = s0;
+            bool spec = false;
+            unsigned cnt = 0;
+            if (sz > 0 && s0 <= e0) {
+                if (s0 > R0 && win[s0 - 1] != '\n') {
+                    const int w = max(R0, s0 - CX_WARM);
+                    int p = s0 - 1;
+                    while (p > w && win[p] != '\n') --p;
+                    if (win[p] == '\n') {
+                        c = p + 1;
+                    } else {
+                        c = w;
+                        spec = w > R0;  // R0 starts the path
+                    }
+                    while (c < s0) c += win[c] == 0x20u ? 1 : S.explen[win[c]];
+                }
+                x = count(c, cnt);
+            }
+            __syncthreads();  // lane_a (the cuts) is free from here on
+            S.lane_a[tid] = x;  // exit: first path position of the right neighbour's slice
+            __syncthreads();
+            for (;;) {
+                bool need = false;
+                int truth = 0;
+                if (spec) {
+                    truth = S.lane_a[tid - 1];
+                    need = truth != c;
+                }
+                if (!__syncthreads_or(need)) break;
+                if (need) {
+                    c = truth;
+                    x = count(c, cnt);
+                    S.lane_a[tid] = x;
+                }
+                __syncthreads();
+            }
+            unsigned long long stot;
+            p6off = block_exscan_n<unsigned long long, CX_NT>((unsigned long long)cnt, s_tmp64, stot);
+            p6a = c;
+            p6b = e0;
+            if (!(sz > 0 && s0 <= e0)) p6b = p6a - 1;  // empty slice
+        }
         unsigned esc = 0;
-        if (staged && start <= end)
-            esc = cx_emit_range<true>(job, S, ws, start, end, S.out, my_off, n_rare);
+        if (staged && p6a <= p6b)
+            esc = cx_emit_range<true>(job, S, ws, p6a, p6b, S.out, p6off, n_rare);
         if (tid < 32) {
             unsigned long long po, pl;
             lookback_resolve(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
@@ -1102,8 +1180,8 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         pc.mark(job, 6);  // emit + look-back
         const unsigned long long pre_out = s_pre_out;
         const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
-        if (!staged && fits && start <= end)
-            esc = cx_emit_range<false>(job, S, ws, start, end, job.out, pre_out + my_off, n_rare);
+        if (!staged && fits && p6a <= p6b)
+            esc = cx_emit_range<false>(job, S, ws, p6a, p6b, job.out, pre_out + p6off, n_rare);
         if (esc) atomicAdd(&s_esc, esc);
         if (tid == 0) {
             atomicAdd(&job.ctl->total_out, tile_out);
