@@ -61,7 +61,7 @@ def main():
     rnd = sys.argv[1]
     dst = os.path.join(ROOT, "profiles", rnd)
     os.makedirs(dst, exist_ok=True)
-    for f in ("bench.json", "bench_ref.json", "gpu_tests.log", "smoke.log"):
+    for f in ("bench.json", "bench_ref.json", "gpu_tests.log", "smoke.log", "configs.json", "train.json"):
         if os.path.exists(os.path.join(OUT, f)):
             shutil.copy(os.path.join(OUT, f), os.path.join(dst, f))
     launches(dst)

@@ -19,3 +19,5 @@ if [ $rc -eq 0 ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^fx_(count|emit)" -s 6 -c 2 \
     -o gpurun_out/full_decompress $CMD > gpurun_out/ncu_d.log 2>&1; echo ncu_decompress=$?
 fi
+timeout 1500 python tools/configs.py > gpurun_out/configs.json 2> gpurun_out/configs.err; echo configs=$?
+timeout 600 python tools/train_bench.py gpurun_out/train.json > gpurun_out/train.log 2>&1; echo train=$?
