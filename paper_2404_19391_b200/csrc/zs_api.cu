@@ -105,6 +105,7 @@ struct zs_ctx {
     int fast_w = 0;
     DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2, d_fxc, d_fxe, d_cxdfa, d_cxt2, d_cxcodes, d_cxcmap;
     int no_cx = 0;  // debug: force the queue-based compress kernel
+    int nk[NSLOT] = {};  // kernels the last launch_stream on a slot issued (zs_result.gpu_launches)
     int p4_lane = 0;  // debug: parse per line-lane range instead of byte-exact slices
     bool fx_ok = false;  // streaming decode kernel serves this dictionary (max expansion <= 7)
     int fx_blocks[2] = {0, 0};  // resident fx_count / fx_emit CTAs per SM
@@ -499,6 +500,7 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
     job.arena = ctx->arena[slot].as<uint8_t>();
     job.arena_cap = (long long)ctx->arena[slot].cap;
     job.timing = ctx->timing;
+    ctx->nk[slot] = nt > 0 ? 1 : 0;
     if (nt > 0) {
         const int grid = (int)std::min<long long>(nt, ctx->n_sm);
         if (timed) CK(cudaEventRecord(ctx->ev0, st));
@@ -547,6 +549,7 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
             fx_scan<<<1, 1024, 0, st>>>(job, sc);
             ke<<<grid_of(ctx->fx_blocks[1]), FX_NT, esm, st>>>(job, ctx->d_fxe.as<unsigned long long>(), sc);
             ctx->last_kernel = "fx_count+fx_scan+fx_emit";
+            ctx->nk[slot] = 3;
         } else {
             const int smem = bp_smem_bytes(ctx->tb.n_flat);
             if (ctx->dec_variant == 1) {
@@ -617,9 +620,9 @@ int collect(zs_ctx *ctx, int slot, long long n, const uint8_t *h_last_byte_src, 
             res->err_ids[0] = r.err_ids[0];
             res->err_ids[1] = r.err_ids[1];
         }
-        res->gpu_launches += 1;
+        res->gpu_launches += ctx->nk[slot];
     } else {
-        r.gpu_launches = 1;
+        r.gpu_launches = ctx->nk[slot];
         *res = r;
     }
     return (c.overflow & 1ull) ? 2 : ZS_OK;
@@ -738,7 +741,7 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
         res->escapes += r.escapes;
         res->skipped += r.skipped;
         res->flagged += r.flagged;
-        res->gpu_launches += 1;
+        res->gpu_launches += ctx->nk[slot];
         if (!res->err_line && r.err_line) {
             res->err_line = r.err_line;
             res->err_kind = r.err_kind;

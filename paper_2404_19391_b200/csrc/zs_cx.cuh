@@ -735,8 +735,14 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
             int lc0 = -1, lc1 = -1, lc2 = -1, lc3 = -1;
             unsigned n_pct = 0;
             bool skip = ls <= end && cx_bit(S.ebits, ls), fail = false;
+            // event iterator: the current bitmap word stays in a register
+            // (events come in position order; the range ends with a '\n' event)
+            int ew = (pos + 1) >> 5;
+            unsigned em = pos < end ? S.rbits[ew] & (0xffffffffu << ((pos + 1) & 31)) : 0u;
             while (pos < end) {
-                const int q = cx_next(S.rbits, pos + 1);
+                while (!em) em = S.rbits[++ew];
+                const int q = (ew << 5) + __ffs(em) - 1;
+                em &= em - 1u;
                 pos = q;
                 ++n_ev;
                 const unsigned c = win[q];
