@@ -78,6 +78,11 @@ struct HostTables {
     std::vector<uint32_t> t2;
     // lane-chunk compress kernel tables (zs_cx.cuh): '\n' column + transducer slot
     bool cx_ok = false;
+    // lane-chunk kernel, key-window parse for patterns of up to 16 bytes (build_kw)
+    bool kw_ok = false;
+    int kw_states = 0, kw_cols = 0;
+    std::vector<uint8_t> kw_cmap, kw_codes;
+    std::vector<uint32_t> kw_dfa;
     int cx_states = 0, cx_cols = 0;  // minimised DFA: states x byte-class columns
     std::vector<uint8_t> cx_cmap;     // byte -> column
     std::vector<uint16_t> cx_dfa;
@@ -327,6 +332,118 @@ bool build_t2(HostTables &ht, int W) {
 // transducer's CX_NLMASK entry of every window resets to the line-end window
 // with code slot 9 (the record separator, cost +1).  Code slot 0 (an escape)
 // is 0x20, so the parse writes every decision without a branch.
+// Key-window parse tables for patterns of up to 16 bytes (the lane-chunk
+// kernel's P4 when the cost-window transducer does not apply): the reversed
+// Aho-Corasick DFA with 16-bit match masks, Moore-minimised, over byte-class
+// columns; entry = next state << 16 | match mask of the target state (bit
+// L-1: a pattern of length L starts at the byte just read).  Codes per state
+// for L = 2..16 (a length-1 match is the identity code: the byte itself).
+bool build_kw(const std::vector<std::pair<std::string, int>> &pats, int max_len, HostTables &ht) {
+    constexpr int KW = 16;
+    if (max_len < 1 || max_len > KW) return false;
+    for (auto &pc : pats)
+        for (unsigned char c : pc.first)
+            if (c < 0x21 || c > 0x7e) return false;
+    std::vector<std::array<int, 256>> go(1);
+    go[0].fill(-1);
+    std::vector<uint32_t> own(1, 0);
+    std::vector<std::array<int, KW>> own_code(1);
+    own_code[0].fill(-1);
+    for (auto &pc : pats) {
+        int node = 0;
+        for (auto it = pc.first.rbegin(); it != pc.first.rend(); ++it) {
+            const unsigned char c = (unsigned char)*it;
+            if (go[node][c] < 0) {
+                go[node][c] = (int)go.size();
+                go.emplace_back();
+                go.back().fill(-1);
+                own.push_back(0);
+                own_code.emplace_back();
+                own_code.back().fill(-1);
+            }
+            node = go[node][c];
+        }
+        const int L = (int)pc.first.size();
+        own[node] |= 1u << (L - 1);
+        own_code[node][L - 1] = pc.second;
+    }
+    const int ns = (int)go.size();
+    if (ns > 65535) return false;
+    std::vector<int> failv(ns, 0), order{0};
+    std::vector<uint32_t> outm(own);
+    std::vector<std::array<int, KW>> code(own_code);
+    for (size_t qi = 0; qi < order.size(); ++qi) {
+        const int st = order[qi];
+        for (int c = 0; c < 256; ++c) {
+            const int ch = go[st][c];
+            if (ch >= 0) {
+                failv[ch] = st == 0 ? 0 : go[failv[st]][c];
+                outm[ch] = own[ch] | outm[failv[ch]];
+                for (int L = 0; L < KW; ++L)
+                    code[ch][L] = own_code[ch][L] >= 0 ? own_code[ch][L] : code[failv[ch]][L];
+                order.push_back(ch);
+            } else {
+                go[st][c] = st == 0 ? 0 : go[failv[st]][c];
+            }
+        }
+    }
+    // Moore minimisation (outputs: match mask, codes for L >= 2)
+    std::vector<int> cls(ns), tmp(ns);
+    {
+        std::map<std::vector<int>, int> ids;
+        for (int st = 0; st < ns; ++st) {
+            std::vector<int> key{(int)outm[st]};
+            for (int L = 2; L <= KW; ++L) key.push_back(code[st][L - 1]);
+            cls[st] = ids.emplace(key, (int)ids.size()).first->second;
+        }
+    }
+    for (int nc = -1;;) {
+        std::map<std::vector<int>, int> ids;
+        for (int st = 0; st < ns; ++st) {
+            std::vector<int> key{cls[st]};
+            for (int b = 0; b < 256; ++b)
+                if (b != '\n') key.push_back(cls[go[st][b]]);
+            tmp[st] = ids.emplace(key, (int)ids.size()).first->second;
+        }
+        cls = tmp;
+        if ((int)ids.size() == nc) break;
+        nc = (int)ids.size();
+    }
+    std::vector<int> ren(ns, -1);
+    int S = 0;
+    ren[cls[0]] = S++;
+    for (int st = 0; st < ns; ++st)
+        if (ren[cls[st]] < 0) ren[cls[st]] = S++;
+    std::vector<int> rep(S, -1);
+    for (int st = 0; st < ns; ++st)
+        if (rep[ren[cls[st]]] < 0) rep[ren[cls[st]]] = st;
+    std::map<std::vector<int>, int> cols;
+    std::vector<int> cmap(256);
+    for (int b = 0; b < 256; ++b) {
+        std::vector<int> key;
+        for (int q = 0; q < S; ++q) key.push_back(ren[cls[go[rep[q]][b]]]);
+        cmap[b] = cols.emplace(key, (int)cols.size()).first->second;
+    }
+    const int nc = (int)cols.size();
+    if (nc > 255) return false;
+    ht.kw_states = S;
+    ht.kw_cols = nc;
+    ht.kw_cmap.assign(cmap.begin(), cmap.end());
+    ht.kw_dfa.assign((size_t)S * nc, 0);
+    ht.kw_codes.assign((size_t)S * KW, 0);
+    for (int q = 0; q < S; ++q) {
+        for (int b = 0; b < 256; ++b) {
+            const int t = go[rep[q]][b];
+            ht.kw_dfa[(size_t)q * nc + cmap[b]] = ((uint32_t)ren[cls[t]] << 16) | outm[t];
+        }
+        for (int L = 2; L <= KW; ++L) {
+            const int c = code[rep[q]][L - 1];
+            ht.kw_codes[(size_t)q * KW + L - 1] = (uint8_t)(c < 0 ? 0 : c);
+        }
+    }
+    return true;
+}
+
 bool build_cx(HostTables &ht, int max_len) {
     if (!ht.t2_ok || ht.n_masks > CX_NLMASK || max_len > 8) return false;
     const int ns = ht.n_states, nw = ht.n_windows;
@@ -471,7 +588,8 @@ BatchKernel batch_kernel(int w) {
 // one whole-buffer launch (device pointers) on `slot`'s buffers and stream
 int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, long long n,
                   uint8_t *d_out, long long out_cap, int flags, bool timed, bool general = false) {
-    const bool cx = compress && ctx->ht.cx_ok && !general && !ctx->no_cx && !ctx->no_t2 && !ctx->no_ip;
+    const bool cx = compress && (ctx->ht.cx_ok || ctx->ht.kw_ok) && !general && !ctx->no_cx && !ctx->no_t2 &&
+                    !ctx->no_ip;
     const bool ip = compress && !cx && ctx->fast_w && ctx->ht.t2_ok && !ctx->no_t2 && !ctx->no_ip;
     const bool fx = !compress && ctx->fx_ok && !general && ctx->dec_variant == 1;
     const long long tile = cx ? CX_TILE : ip ? CTILE : fx ? FX_TILE : TILE;
@@ -505,14 +623,19 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
         const int grid = (int)std::min<long long>(nt, ctx->n_sm);
         if (timed) CK(cudaEventRecord(ctx->ev0, st));
         if (cx) {
-            const CxLayout L = cx_layout(ctx->ht.cx_states, ctx->ht.n_windows, ctx->ht.cx_cols);
-            CK(set_smem(compress_cx, L.bytes));
-            CxTables ct{ctx->d_cxdfa.as<uint16_t>(), ctx->d_cxt2.as<uint16_t>(), ctx->d_cxcodes.as<uint8_t>(),
-                        ctx->d_cxcmap.as<uint8_t>(), ctx->ht.cx_states, ctx->ht.n_windows, ctx->ht.cx_cols,
-                        L.o_t2, L.o_codes, ctx->p4_lane ? 0 : 1};
+            const bool kw = !ctx->ht.cx_ok;
+            const CxLayout L = kw ? cx_layout(ctx->ht.kw_states, 0, 2 * ctx->ht.kw_cols)
+                                  : cx_layout(ctx->ht.cx_states, ctx->ht.n_windows, ctx->ht.cx_cols);
+            const int smem = L.bytes + (kw ? cx_kw_ring_bytes() : 0);
+            CK(set_smem(compress_cx, smem));
+            CxTables ct{ctx->d_cxdfa.as<uint16_t>(), kw ? nullptr : ctx->d_cxt2.as<uint16_t>(),
+                        ctx->d_cxcodes.as<uint8_t>(), ctx->d_cxcmap.as<uint8_t>(),
+                        kw ? ctx->ht.kw_states : ctx->ht.cx_states, kw ? 0 : ctx->ht.n_windows,
+                        kw ? 2 * ctx->ht.kw_cols : ctx->ht.cx_cols, L.o_t2, L.o_codes, ctx->p4_lane ? 0 : 1,
+                        kw ? 1 : 0, L.bytes};
             const int g2 = (int)std::min<long long>(nt, (long long)ctx->n_sm * CX_CTAS);
-            compress_cx<<<g2, CX_NT, L.bytes, st>>>(job, ctx->tb, ct);
-            ctx->last_kernel = "compress_cx";
+            compress_cx<<<g2, CX_NT, smem, st>>>(job, ctx->tb, ct);
+            ctx->last_kernel = kw ? "compress_cx<kw16>" : "compress_cx";
         } else if (ip) {
             const int smem = ip_smem_bytes(ctx->tb.n_states, ctx->ht.n_windows);
             CK(set_smem(compress_tiles_ip, smem));
@@ -927,7 +1050,12 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
     ht.max_len = 0;
     for (auto &p : pats) ht.max_len = std::max<int>(ht.max_len, (int)p.first.size());
     ht.fast = build_dfa(pats, ht.max_len, ht);
+    ht.cx_ok = ht.kw_ok = false;
     if (ht.fast && build_t2(ht, std::max(1, ht.max_len))) build_cx(ht, ht.max_len);
+    if (!ht.cx_ok && build_kw(pats, ht.max_len, ht)) {
+        const CxLayout L = cx_layout(ht.kw_states, 0, 2 * ht.kw_cols);
+        ht.kw_ok = L.bytes + cx_kw_ring_bytes() <= 227 * 1024;
+    }
     // decode tables (dictionary.py:112-129): valid codes have exp_len > 0
     if (exp_off[256] > 65535) {
         ctx->err = "expansion table too large";
@@ -961,6 +1089,11 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
     if (ht.t2_ok) {
         CK(up(ctx->d_dfa2, ht.dfa2.data(), ht.dfa2.size() * 2));
         CK(up(ctx->d_t2, ht.t2.data(), ht.t2.size() * 4));
+    }
+    if (ht.kw_ok) {
+        CK(up(ctx->d_cxcmap, ht.kw_cmap.data(), 256));
+        CK(up(ctx->d_cxdfa, ht.kw_dfa.data(), ht.kw_dfa.size() * 4));
+        CK(up(ctx->d_cxcodes, ht.kw_codes.data(), ht.kw_codes.size()));
     }
     if (ht.cx_ok) {
         CK(up(ctx->d_cxcmap, ht.cx_cmap.data(), 256));

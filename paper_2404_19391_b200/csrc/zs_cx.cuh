@@ -113,7 +113,13 @@ struct CxTables {
     int ns, nw, nc;
     int o_t2, o_codes;     // smem offsets (cx_layout)
     int p4x;               // 1: byte-exact parse slices (default), 0: parse the lane's line range
+    int kw;                // 1: key-window parse (patterns up to 16 bytes; dfa = u32 [states][nc/2])
+    int o_ring;            // kw: per-thread key rings (cx_kw_ring_bytes) at this smem offset
 };
+
+// kw: a 32-entry key ring per thread (stride 33 words: conflict-free banks)
+constexpr int CX_KW_RING = 33;
+__host__ __device__ inline int cx_kw_ring_bytes() { return CX_NT * CX_KW_RING * 4; }
 
 struct CxSmem {
     uint16_t *dfa;
@@ -654,6 +660,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 // line-lane through the per-line walk below instead.
                 nlines += cx_popc_range(S.rbits, first, end);  // the bitmap holds only newlines yet
                 if (first <= end) atomicMin(&s_r2, first);
+                if (start <= end) atomicMin(&s_r0, start);  // P4 / P6 slices
                 __syncthreads();
                 const int R0 = s_r2, R1 = s_last_nl;
                 const int sz = R1 >= R0 ? (R1 - R0 + CX_NT) / CX_NT : 0;
@@ -942,12 +949,60 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 }
                 for (; i >= lo; --i) win[i] = (uint8_t)step(win[i]);
             };
-            p4_exact = long_ranges;
-            if (!p4_exact) {
+            p4_exact = long_ranges && !ct.kw;
+            if (ct.kw) {
+                // Key-window parse (dp_fast restated for W = 16): key(j) =
+                // cost[j] * 16 - j, kept in a 32-entry ring per thread; the
+                // cheapest candidate, longer on ties (numba_impl.py:50), wins.
+                // A '\n' closes the line to its right (its cost + 1 for the
+                // separator) and starts the next one with key = -position.
+                const uint32_t *__restrict__ dfa32 = reinterpret_cast<const uint32_t *>(S.dfa);
+                const int ncol = ct.nc >> 1;
+                unsigned *ring = reinterpret_cast<unsigned *>(smem + ct.o_ring) + tid * CX_KW_RING;
+                constexpr int INF = 0x3fffffff;
+                // the range normally ends with its last line's '\n'; a rare
+                // line's filler replaces that '\n', so the walk starts from a
+                // virtual line end past the range (no separator byte of its own)
+                int k1 = -(end + 1);  // key(i + 1)
+                for (int L = 1; L <= 16; ++L) ring[(end + 1 + L) & 31] = (unsigned)INF;
+                ring[(end + 1) & 31] = (unsigned)k1;
+                bool virt = true;     // the line being parsed has no '\n' of its own
+                unsigned long long tot = 0;
+                for (int i = end; i >= start; --i) {
+                    const unsigned b = win[i];
+                    if (b == '\n') {
+                        tot += (unsigned)(((k1 + i + 1) >> 4) + (virt ? 0 : 1));
+                        virt = false;
+                        k1 = -i;   // cost 0 at the line end
+                        st = 0;
+                        ring[i & 31] = (unsigned)(-i);
+                        // positions right of the line end must never be candidates
+                        for (int L = 1; L <= 16; ++L) ring[(i + L) & 31] = (unsigned)INF;
+                        continue;  // the decision byte stays '\n'
+                    }
+                    const unsigned e = dfa32[st * ncol + s_cmap[b]];
+                    st = e >> 16;
+                    unsigned m = e & 0xffffu;
+                    int mm = INF;
+                    while (m) {
+                        const int L = __ffs(m);
+                        m &= m - 1u;
+                        mm = min(mm, (int)ring[(i + L) & 31]);
+                    }
+                    const int esc = k1 + 32;
+                    const int best = min(esc, mm + 16);
+                    const int t = best + i + 16;
+                    const int L = 16 - (t & 15);
+                    k1 = (t & ~15) - i;
+                    ring[i & 31] = (unsigned)k1;
+                    win[i] = (uint8_t)(esc < mm + 16 ? 0x20u : (L == 1 ? b : codes[st * CX_CODES + L - 1]));
+                }
+                if (end >= start) tot += (unsigned)(((k1 + start) >> 4) + (virt ? 0 : 1));
+                acc = (unsigned)(tot + 4ull * (unsigned)(end >= start ? end - start + 1 : 0));
+            } else if (!p4_exact) {
                 parse_range(start, end);
             } else {
-                if (start <= end) atomicMin(&s_r0, start);
-                __syncthreads();  // P2 / P3 of every warp done (slices cross line-lanes); R0 known
+                __syncthreads();  // P2 / P3 of every warp done (slices cross line-lanes); R0 set in P2
                 const int R0 = s_r0, R1 = s_last_nl;
                 const int sz = R1 >= R0 ? (R1 - R0 + CX_NT) / CX_NT : 0;
                 const int s0 = R0 + tid * sz, e0 = min(R1, s0 + sz - 1);

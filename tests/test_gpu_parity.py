@@ -326,6 +326,12 @@ def test_long_line_tiles_edge_cases():
         for lenient in (False, True):
             _oracle_check(payload, d, True, lenient)
         _oracle_check(payload, d, False, True)
+    # the key-window parse (patterns of 9-15 bytes) on long-line tiles
+    dk = z.deserialize(golden_dict_bytes("t128_l15.zsd"))
+    payload = b"\n".join(base[:4000]) + b"\n"
+    for lenient in (False, True):
+        _oracle_check(payload, dk, True, lenient)
+    _oracle_check(payload, dk, False, True)
     # long lines without any newline for many slices, and one-line tiles
     mols = [m for m in base if len(m) > 100][:40]
     payload = b"\n".join(b"C".join(mols[i:i + 8]) for i in range(0, 40, 8)) + b"\n"
