@@ -444,6 +444,23 @@ bool build_kw(const std::vector<std::pair<std::string, int>> &pats, int max_len,
     return true;
 }
 
+// dynamic shared memory compress_cx can opt into on this device (the
+// opt-in maximum minus the kernel's static shared memory)
+int cx_dyn_smem_limit() {
+    static int lim = -1;
+    if (lim < 0) {
+        int dev = 0, optin = 0;
+        cudaFuncAttributes fa{};
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess &&
+            cudaFuncGetAttributes(&fa, compress_cx) == cudaSuccess)
+            lim = optin - (int)fa.sharedSizeBytes;
+        else
+            lim = 227 * 1024 - 16 * 1024;  // no device: a conservative bound
+    }
+    return lim;
+}
+
 bool build_cx(HostTables &ht, int max_len) {
     if (!ht.t2_ok || ht.n_masks > CX_NLMASK || max_len > 8) return false;
     const int ns = ht.n_states, nw = ht.n_windows;
@@ -505,7 +522,7 @@ bool build_cx(HostTables &ht, int max_len) {
         cmap[b] = cols.emplace(key, (int)cols.size()).first->second;
     }
     const int nc = (int)cols.size();
-    if (S > 256 || nc > 255 || cx_smem_bytes(S, nw, nc) > 227 * 1024) return false;
+    if (S > 256 || nc > 255 || cx_smem_bytes(S, nw, nc) > cx_dyn_smem_limit()) return false;
     ht.cx_states = S;
     ht.cx_cols = nc;
     ht.cx_cmap.assign(cmap.begin(), cmap.end());
@@ -1054,7 +1071,7 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
     if (ht.fast && build_t2(ht, std::max(1, ht.max_len))) build_cx(ht, ht.max_len);
     if (!ht.cx_ok && build_kw(pats, ht.max_len, ht)) {
         const CxLayout L = cx_layout(ht.kw_states, 0, 2 * ht.kw_cols);
-        ht.kw_ok = L.bytes + cx_kw_ring_bytes() <= 227 * 1024;
+        ht.kw_ok = L.bytes + cx_kw_ring_bytes() <= cx_dyn_smem_limit();
     }
     // decode tables (dictionary.py:112-129): valid codes have exp_len > 0
     if (exp_off[256] > 65535) {

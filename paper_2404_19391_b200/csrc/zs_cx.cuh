@@ -39,7 +39,7 @@ namespace zs {
 constexpr int CX_NT = 384;
 constexpr int CX_CTAS = 2;                        // resident CTAs per SM
 constexpr int CX_NW = CX_NT / 32;
-constexpr int CX_CC = 66;                         // bytes of line ends per lane (tile 50,688 B)
+constexpr int CX_CC = 78;                         // bytes of line ends per lane (tile 29,952 B)
 constexpr int CX_TILE = CX_NT * CX_CC;
 constexpr int CX_HEAD = 2048;                     // staged before the tile
 constexpr int CX_WIN = CX_HEAD + CX_TILE;         // multiple of 32 (bitmap words)
@@ -47,7 +47,7 @@ constexpr int CX_WORDS = CX_WIN / 32 + 4;         // bitmap words (multiple of 4
 constexpr int CX_NCOL = 119;                      // dcol: umin(b - 10, 118); 0 = '\n'
 constexpr int CX_NLMASK = 15;                     // transducer mask slot of '\n'
 constexpr int CX_CODES = 16;                      // code slots per state: 0 escape, 1-8 match, 9 '\n'
-constexpr int CX_OUTCAP = 13312;                  // staging (ratio <= ~0.5)
+constexpr int CX_OUTCAP = 17408;                  // staging (tile output up to ratio ~0.55)
 constexpr int CX_RARE = 64;                       // rare lines per tile
 constexpr int CX_JOBS = 16;                       // '%nn' compactions per warp and tile
 constexpr int CX_WARM = 32;                       // P4 warm-up bytes right of a slice (speculative entry)

@@ -27,6 +27,6 @@ for kind, n, seed in (("aromatic", 2_000_000, 2024), ("skewed", 500_000, 2025)):
     cyc = np.zeros(8, np.uint64)
     ctx.lib.zs_last_phase_cycles(ctx.h, cyc.ctypes.data)
     ctx.lib.zs_set_phase_timing(ctx.h, 0)
-    tiles = (buf.size + 25343) // 25344
+    tiles = (buf.size + 29951) // 29952
     print(f"{kind}: per tile: newline-warmed {cyc[0] / tiles:.1f} (mismatch {cyc[2] / tiles:.2f}), "
           f"virtual {cyc[1] / tiles:.1f} (mismatch {cyc[3] / tiles:.2f})")
