@@ -177,6 +177,11 @@ int zs_compress_host(zs_ctx *ctx, const uint8_t *h_in, int64_t n, uint8_t *h_out
 int zs_decompress_host(zs_ctx *ctx, const uint8_t *h_in, int64_t n, uint8_t *h_out,
                        int64_t out_cap, int flags, zs_result *res);
 
+/* page-locked host memory for the host-pointer calls (cudaHostAlloc):
+ * full PCIe rate for run_stream's segments */
+int zs_host_alloc(zs_ctx *ctx, int64_t bytes, void **p);
+int zs_host_free(zs_ctx *ctx, void *p);
+
 /* upper bound of the output size for an n-byte input (for buffer sizing) */
 int64_t zs_compress_bound(int64_t n);
 int64_t zs_decompress_bound(zs_ctx *ctx, int64_t n);

@@ -27,6 +27,7 @@ EXPORTS = (
     "zs_build_tables_host", "zs_set_phase_timing", "zs_last_phase_cycles", "zs_build_t2_host",
     "zs_set_transducer", "zs_last_kernel", "zs_stream", "zs_index_build", "zs_decode_records",
     "zs_train_count", "zs_train_rows", "zs_train_load", "zs_train_select", "zs_overlap_batch",
+    "zs_host_alloc", "zs_host_free",
 )
 
 
@@ -93,6 +94,8 @@ def load():
             "zs_train_load": (ctypes.c_int, [P, P, I32, P, P, I64]),
             "zs_train_select": (ctypes.c_int, [P, I32, I64, P, ctypes.POINTER(ctypes.c_int32)]),
             "zs_overlap_batch": (ctypes.c_int, [P, P, P, I32, P, I32, P, I64, P]),
+            "zs_host_alloc": (ctypes.c_int, [P, I64, ctypes.POINTER(ctypes.c_void_p)]),
+            "zs_host_free": (ctypes.c_int, [P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -131,6 +134,22 @@ class Context:
         self.lock = threading.RLock()
         self._dict_key = None
         self._keep = None
+        self._pinned = {}
+
+    def pinned(self, slot: str, nbytes: int) -> np.ndarray:
+        """A page-locked uint8 buffer of at least `nbytes`, cached per
+        context and slot name (grown on demand, freed with the context)."""
+        have = self._pinned.get(slot)
+        if have is not None and have[1].size >= nbytes:
+            return have[1]
+        if have is not None:
+            self.lib.zs_host_free(self.h, have[0])
+        p = ctypes.c_void_p()
+        size = max(int(nbytes) + (int(nbytes) >> 3), 1 << 20)  # headroom: segments vary a little
+        self.check(self.lib.zs_host_alloc(self.h, size, ctypes.byref(p)), "zs_host_alloc")
+        arr = np.ctypeslib.as_array((ctypes.c_uint8 * size).from_address(p.value))
+        self._pinned[slot] = (p, arr)
+        return arr
 
     def check(self, rc, what):
         if rc == ZS_OK:
@@ -166,6 +185,9 @@ class Context:
 
     def close(self):
         if self.h:
+            for p, _ in self._pinned.values():
+                self.lib.zs_host_free(self.h, p)
+            self._pinned = {}
             self.lib.zs_ctx_destroy(self.h)
             self.h = None
 

@@ -1280,6 +1280,20 @@ int zs_decode_records(zs_ctx *ctx, const uint8_t *d_comp, const uint64_t *d_offs
     return ZS_OK;
 }
 
+int zs_host_alloc(zs_ctx *ctx, int64_t bytes, void **p) {
+    if (!ctx || bytes < 0 || !p) return ZS_E_ARG;
+    *p = nullptr;
+    CK(cudaSetDevice(ctx->dev));
+    CK(cudaHostAlloc(p, (size_t)std::max<int64_t>(bytes, 1), cudaHostAllocDefault));
+    return ZS_OK;
+}
+
+int zs_host_free(zs_ctx *ctx, void *p) {
+    if (!ctx) return ZS_E_ARG;
+    if (p) CK(cudaFreeHost(p));
+    return ZS_OK;
+}
+
 int64_t zs_compress_bound(int64_t n) { return 2 * n + 64; }
 
 int64_t zs_decompress_bound(zs_ctx *ctx, int64_t n) {

@@ -58,10 +58,11 @@ def _read_all(src) -> bytes:
     return b"".join(parts)
 
 
-def run_buffer(buf, d, direction="compress", *, preprocess=False, lenient=False, device=None):
+def run_buffer(buf, d, direction="compress", *, preprocess=False, lenient=False, device=None, out=None):
     """One newline-framed buffer through the GPU.  Returns (output bytes,
     zs_result).  `buf` may be bytes or a uint8 numpy array (pinned memory
-    gives full PCIe rate)."""
+    gives full PCIe rate); `out`, if given, is a uint8 array used as the
+    output buffer when it is large enough (the result is a view of it)."""
     if direction not in ("compress", "decompress"):
         raise ValueError(f"bad direction {direction!r}")
     arr = buf if isinstance(buf, np.ndarray) else np.frombuffer(buf, np.uint8)
@@ -77,8 +78,12 @@ def run_buffer(buf, d, direction="compress", *, preprocess=False, lenient=False,
         else:
             cap = max(4 * n + 64, 1024)
             fn = ctx.lib.zs_decompress_host
+        given = out
         for _ in range(3):
-            out = np.empty(cap, np.uint8)
+            if given is not None and given.size >= cap:
+                out, cap = given, given.size
+            else:
+                out = np.empty(cap, np.uint8)
             rc = fn(ctx.h, _lib.ptr(arr), n, _lib.ptr(out), cap, flags, res)
             if rc == _lib.ZS_E_CAPACITY:
                 cap = res.out_bytes + 64
@@ -91,27 +96,69 @@ def run_buffer(buf, d, direction="compress", *, preprocess=False, lenient=False,
 SEGMENT_BYTES = 256 << 20
 
 
-def _read_seg(src, n):
-    parts, got = [], 0
+def _host_buffer(slot, nbytes, device):
+    """Page-locked staging for run_stream (cached per context and slot)."""
+    return _lib.context(device).pinned(slot, nbytes)
+
+
+def _read_into(src, buf, at, n):
+    """Read up to n bytes of src into buf[at:at + n]; returns the count."""
+    readinto = getattr(src, "readinto", None)
+    got = 0
+    mv = memoryview(buf)
     while got < n:
-        chunk = src.read(n - got)
-        if not chunk:
-            break
-        parts.append(chunk)
-        got += len(chunk)
-    return b"".join(parts)
+        if readinto is not None:
+            k = readinto(mv[at + got:at + n])
+            if not k:
+                break
+        else:
+            chunk = src.read(n - got)
+            if not chunk:
+                break
+            k = len(chunk)
+            buf[at + got:at + got + k] = np.frombuffer(chunk, np.uint8)
+        got += k
+    return got
+
+
+def _last_nl(arr, lo, hi):
+    """Index of the last '\\n' in arr[lo:hi], or -1 (scans back in blocks)."""
+    end = hi
+    while end > lo:
+        beg = max(lo, end - (1 << 20))
+        nz = np.flatnonzero(arr[beg:end] == 10)
+        if nz.size:
+            return beg + int(nz[-1])
+        end = beg
+    return -1
+
+
+def _cut_keeping_last(arr, n, m):
+    """Offset in arr[:n] ('\\n'-terminated records) after which exactly the
+    last m records remain (0 if there are only m)."""
+    need, end = m + 1, n
+    while end > 0:
+        beg = max(0, end - (1 << 20))
+        nz = np.flatnonzero(arr[beg:end] == 10)
+        if nz.size >= need:
+            return beg + int(nz[nz.size - need]) + 1
+        need -= nz.size
+        end = beg
+    return 0
 
 
 def run_stream(src, dst, d, direction="compress", *, preprocess=False, lenient=False, workers=1,
                batch_lines=BATCH_LINES, device=None, segment_bytes=SEGMENT_BYTES) -> CorpusStats:
     """Stream src to dst through the GPU codec; returns exact corpus totals.
 
-    The input is read in `segment_bytes` pieces cut at newlines, so files
-    larger than host or device memory stream through (each segment is one
-    zs_*_host call, itself pipelined in 32 MB chunks).  Output bytes equal the
-    reference's `b"\n".join(kept records) + ("\n" if kept and trailing)`
-    (pipeline.py:148-166) for any segment size: a segment's final '\n' is held
-    back until the next kept record or the end of the input.
+    The input is read (``readinto``, no intermediate copies) into page-locked
+    staging in `segment_bytes` pieces cut at newlines, so files larger than
+    host or device memory stream through at PCIe rate (each segment is one
+    zs_*_host call, itself pipelined in chunks on three streams); output is
+    written from page-locked staging without copies.  Output bytes equal the
+    reference's `b"\\n".join(kept records) + ("\\n" if kept and trailing)`
+    (pipeline.py:148-166) for any segment size: a segment's final '\\n' is
+    held back until the next kept record or the end of the input.
 
     Strict mode raises LineError (1-based) for the first bad line, after
     writing every complete `batch_lines` batch before it like the reference
@@ -124,37 +171,48 @@ def run_stream(src, dst, d, direction="compress", *, preprocess=False, lenient=F
     st = CorpusStats()
     line_base = 0        # input lines before the current segment (strict mode: = output records)
     written = 0          # strict mode: output records written (a multiple of batch_lines)
-    pend = bytearray()   # strict mode: records of lines [written, line_base), '\n'-terminated
-    held_nl = False      # the written output's last '\n', held back until more output follows
+    pend = bytearray()   # strict mode: records of lines [written, line_base), '\\n'-terminated
+    held_nl = False      # the written output's last '\\n', held back until more output follows
 
-    def emit(body):
+    def emit(*parts):
         nonlocal held_nl
         if held_nl:
             dst.write(b"\n")
             st.output_bytes += 1
-        dst.write(bytes(body))
-        st.output_bytes += len(body)
+        for body in parts:
+            if len(body):
+                dst.write(body)
+                st.output_bytes += len(body)
         held_nl = False
-    carry = b""
+
+    seg_bytes = max(1, segment_bytes)
+    inbuf = _host_buffer("stream_in", seg_bytes + 4096, device)
+    carry = 0            # bytes of a partial last line at the front of inbuf
     last_byte = None
     while True:
-        chunk = _read_seg(src, max(1, segment_bytes))
-        if chunk:
-            last_byte = chunk[-1]
-            buf = carry + chunk
-            cut = buf.rfind(b"\n") + 1
-            if cut == 0:
-                carry = buf
+        if inbuf.size < carry + seg_bytes:  # a line longer than the staging: grow, keep the carry
+            keep = inbuf[:carry].copy()
+            inbuf = _host_buffer("stream_in", 2 * (carry + seg_bytes), device)
+            inbuf[:carry] = keep
+        got = _read_into(src, inbuf, carry, seg_bytes)
+        total = carry + got
+        final = got == 0
+        if not final:
+            last_byte = int(inbuf[total - 1])
+            nl = _last_nl(inbuf, carry, total)
+            if nl < 0:
+                carry = total
                 continue
-            seg, carry = buf[:cut], buf[cut:]
+            cut = nl + 1
         else:
-            seg, carry = carry, b""
-            if not seg:
+            cut = total
+            if cut == 0:
                 break
-        final = not chunk
-        st.input_bytes += len(seg)
-        out, res = run_buffer(seg, d, direction, preprocess=preprocess, lenient=lenient,
-                              device=device)
+        seg = inbuf[:cut]
+        st.input_bytes += cut
+        cap = (2 * cut + 64) if direction == "compress" else max(4 * cut + 64, 1024)
+        out, res = run_buffer(seg, d, direction, preprocess=preprocess, lenient=lenient, device=device,
+                              out=_host_buffer("stream_out", cap, device))
         if res.err_line:
             gl = line_base + int(res.err_line)
             cause = from_kind(res.err_kind, res.err_offset, tuple(res.err_ids), res.err_code)
@@ -163,15 +221,13 @@ def run_stream(src, dst, d, direction="compress", *, preprocess=False, lenient=F
             if keep > written:
                 nrec = min(keep, line_base) - written
                 if nrec > 0:
-                    pos = 0
-                    for _ in range(nrec):
-                        pos = pend.index(10, pos) + 1
+                    pos = _cut_keeping_last(np.frombuffer(pend, np.uint8), len(pend),
+                                            (line_base - written) - nrec)
                     blob += pend[:pos]
                 if keep > line_base:
-                    arr = np.frombuffer(seg, np.uint8)
-                    nl = np.flatnonzero(arr == 0x0A)
-                    end = int(nl[keep - line_base - 1]) + 1
-                    part, _ = run_buffer(arr[:end], d, direction, preprocess=preprocess,
+                    nls = np.flatnonzero(seg == 0x0A)
+                    end = int(nls[keep - line_base - 1]) + 1
+                    part, _ = run_buffer(seg[:end].copy(), d, direction, preprocess=preprocess,
                                          lenient=lenient, device=device)
                     blob += part.tobytes()
             if blob.endswith(b"\n"):
@@ -183,26 +239,32 @@ def run_stream(src, dst, d, direction="compress", *, preprocess=False, lenient=F
         st.escapes += res.escapes
         st.skipped += res.skipped
         st.flagged += res.flagged
-        ob = out.tobytes()
+        ob = int(res.out_bytes)
+        outv = memoryview(out)[:ob]
         if lenient:
             if ob:
-                nl_end = ob.endswith(b"\n")
-                emit(ob[:-1] if nl_end else ob)
-                held_nl = nl_end
+                nl_end = out[ob - 1] == 10
+                emit(outv[:ob - 1] if nl_end else outv)
+                held_nl = bool(nl_end)
         else:
             line_base += int(res.lines)
-            pend += ob
-            if not final or last_byte == 10:
+            flush_to = (line_base // bl) * bl
+            if (not final or last_byte == 10) and flush_to > written:
                 # whole batches leave; the rest waits for the next segment
-                flush_to = (line_base // bl) * bl
-                if flush_to > written:
-                    pos = 0
-                    for _ in range(flush_to - written):
-                        pos = pend.index(10, pos) + 1
-                    emit(pend[:pos - 1])
-                    held_nl = True
-                    del pend[:pos]
-                    written = flush_to
+                c = _cut_keeping_last(out, ob, line_base - flush_to)
+                if c > 0:
+                    emit(pend, outv[:c - 1])
+                else:  # (cannot happen: a new batch ends inside this segment)
+                    emit(pend[:-1])
+                held_nl = True
+                pend = bytearray(outv[c:])
+                written = flush_to
+            else:
+                pend += outv
+        rem = total - cut
+        if rem:
+            inbuf[:rem] = inbuf[cut:total].copy()
+        carry = rem
         if final:
             break
     tail = bytes(pend)  # strict mode: the records after the last whole batch

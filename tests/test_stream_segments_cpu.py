@@ -30,7 +30,7 @@ class _Res:
         self.err_ids = ids
 
 
-def _oracle_run_buffer(buf, d, direction="compress", *, preprocess=False, lenient=False, device=None):
+def _oracle_run_buffer(buf, d, direction="compress", *, preprocess=False, lenient=False, device=None, out=None):
     t = oracle.Tables(d.learned, bytes(sorted(d.identity)))
     data = bytes(buf) if not isinstance(buf, (bytes, bytearray)) else bytes(buf)
     out, st = oracle.run_stream(t, data, direction, preprocess, lenient, 1)
@@ -41,6 +41,8 @@ def _oracle_run_buffer(buf, d, direction="compress", *, preprocess=False, lenien
 def _cpu_codec(monkeypatch):
     oracle.build()
     monkeypatch.setattr(pipeline, "run_buffer", _oracle_run_buffer)
+    # host staging without a GPU (page-locked memory needs the CUDA runtime)
+    monkeypatch.setattr(pipeline, "_host_buffer", lambda slot, n, device: np.empty(max(int(n), 1), np.uint8))
 
 
 def _dict(dj):
