@@ -49,13 +49,15 @@ class RecordIndex:
     def __len__(self):
         return self._n
 
-    def decode(self, indices):
-        """Decoded bytes of records `indices` (any order, repeats allowed)."""
+    def decode_packed(self, indices):
+        """Records `indices` decoded into one buffer: (data uint8[total],
+        offsets int64[k + 1]); record j is data[offsets[j]:offsets[j + 1]].
+        The bulk form of ``decode`` (no per-record Python objects)."""
         import torch
-        idx = np.asarray(list(indices) if not isinstance(indices, np.ndarray) else indices, np.int64)
+        idx = np.ascontiguousarray(indices if isinstance(indices, np.ndarray) else list(indices), np.int64)
         k = idx.size
         if k == 0:
-            return []
+            return np.zeros(0, np.uint8), np.zeros(1, np.int64)
         if idx.min() < 0 or idx.max() >= self._n:
             raise IndexError("record index out of range")
         d_idx = torch.from_numpy(idx).to(self._dev)
@@ -63,7 +65,7 @@ class RecordIndex:
         d_st = torch.empty(k, dtype=torch.int8, device=self._dev)
         d_ep = torch.empty(k, dtype=torch.int64, device=self._dev)
         total = ctypes.c_int64(0)
-        cap = max(64, 8 * k)
+        cap = max(64, 96 * k)  # ~2x the mean record (45 B); a second call sizes it exactly
         with self._ctx.lock:
             self._ctx.set_dictionary(self._d)
             for _ in range(2):
@@ -77,18 +79,21 @@ class RecordIndex:
                     continue
                 self._ctx.check(rc, "zs_decode_records")
                 break
-        out = d_out[:total.value].cpu().numpy().tobytes()
-        off = d_off.cpu().numpy()
         st = d_st.cpu().numpy()
-        ep = d_ep.cpu().numpy()
-        res = []
-        for j in range(k):
+        bad = np.flatnonzero(st)
+        if bad.size:  # the first bad record in request order, as decompress_line would raise
+            j = int(bad[0])
+            ep = int(d_ep[j].item())
             if st[j] == 1:
-                raise UnknownCode(int(ep[j] >> 40), int(ep[j] & ((1 << 40) - 1)))
-            if st[j] == 2:
-                raise TruncatedEscape(int(ep[j]))
-            res.append(out[off[j]:off[j + 1]])
-        return res
+                raise UnknownCode(ep >> 40, ep & ((1 << 40) - 1))
+            raise TruncatedEscape(ep)
+        return d_out[:total.value].cpu().numpy(), d_off.cpu().numpy()
+
+    def decode(self, indices):
+        """Decoded bytes of records `indices` (any order, repeats allowed)."""
+        data, off = self.decode_packed(indices)
+        raw = data.tobytes()
+        return [raw[a:b] for a, b in zip(off[:-1].tolist(), off[1:].tolist())]
 
     def __getitem__(self, i):
         return self.decode([i])[0]
