@@ -85,7 +85,9 @@ constexpr int CX_O_LB = CX_O_LA + CX_NT * 4;
 constexpr int CX_O_LC = CX_O_LB + CX_NT * 4;
 constexpr int CX_O_JOBS = CX_O_LC + CX_NT * 4;
 constexpr int CX_O_NJOBS = CX_O_JOBS + CX_NW * CX_JOBS * 16;
-constexpr int CX_O_DFA = (CX_O_NJOBS + CX_NW * 4 + 15) & ~15;
+constexpr int CX_O_CODES = (CX_O_NJOBS + CX_NW * 4 + 15) & ~15;  // code slots, when they fit here
+constexpr int CX_CODES_CAP = 256 * 16;                              // (transducer DFAs: <= 256 states)
+constexpr int CX_O_DFA = CX_O_CODES + CX_CODES_CAP;
 static_assert(CX_O_JOBS % 16 == 0, "int4 job slots");
 
 struct CxLayout {
@@ -95,8 +97,10 @@ struct CxLayout {
 __host__ __device__ inline CxLayout cx_layout(int ns, int nw, int nc) {
     CxLayout L;
     L.o_t2 = CX_O_DFA + cx_align16(ns * nc * 2);
-    L.o_codes = L.o_t2 + cx_align16(nw * T2_MASKS * 2);
-    L.bytes = L.o_codes + cx_align16(ns * CX_CODES);
+    const int end_t2 = L.o_t2 + cx_align16(nw * T2_MASKS * 2);
+    const bool fixed = ns * CX_CODES <= CX_CODES_CAP;  // compile-time offset in the parse loop
+    L.o_codes = fixed ? CX_O_CODES : end_t2;
+    L.bytes = fixed ? end_t2 : end_t2 + cx_align16(ns * CX_CODES);
     return L;
 }
 
@@ -913,7 +917,8 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         {
             const uint16_t *__restrict__ dfa = S.dfa;
             const uint16_t *__restrict__ t2 = S.t2;
-            const uint8_t *__restrict__ codes = S.codes;
+            // transducer DFAs keep their code slots at a compile-time offset
+            const uint8_t *__restrict__ codes = ct.kw ? S.codes : smem + CX_O_CODES;
             const int nc = ct.nc;
             uint8_t *win = S.win;
             unsigned st = 0, wi = 0;
