@@ -118,7 +118,7 @@ struct zs_ctx {
     int no_t2 = 0;  // debug: force the key-window DP
     int no_ip = 0;  // debug: force the decision-array kernel
     int dec_variant = 1;  // 1: per-thread slices (default), 0: warp-cooperative
-    // per-slot (double-buffered) work buffers
+    // per-slot work buffers (NSLOT-deep host pipeline)
     DevBuf ctl[NSLOT], ts[NSLOT], terr[NSLOT], in[NSLOT], out[NSLOT], arena[NSLOT];  // arena: per slot
     DevBuf fxs[NSLOT];  // streaming-decode scratch per slot
     DevBuf ixs;     // record-index scratch
@@ -132,7 +132,7 @@ struct zs_ctx {
     } tr;
     // shim scratch
     DevBuf s_flat, s_starts, s_out, s_lens, s_dec, s_stat, s_errpos, s_tot, s_ids, s_outst;
-    Ctl *h_ctl = nullptr;  // pinned, 2 slots
+    Ctl *h_ctl = nullptr;  // pinned, NSLOT slots
     float last_ms = 0.f;
     int timing = 0;
 };
@@ -803,7 +803,7 @@ int run_device(zs_ctx *ctx, bool compress, const uint8_t *d_in, int64_t n, uint8
     return ZS_E_NOMEM;
 }
 
-// Host-buffer pipeline: newline-aligned chunks, two slots on two streams so
+// Host-buffer pipeline: newline-aligned chunks, NSLOT slots on NSLOT streams so
 // chunk k+1's H2D and kernel overlap chunk k's D2H.
 int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t *h_out,
              int64_t out_cap, int flags, zs_result *res) {

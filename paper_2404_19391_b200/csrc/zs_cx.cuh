@@ -75,10 +75,14 @@ __host__ __device__ inline int cx_align16(int x) { return (x + 15) & ~15; }
 // the host passes the table offsets as kernel parameters).  Constant offsets
 // keep the compiler from rebuilding buffer addresses inside the hot loops.
 constexpr int CX_O_WIN = 0;
-constexpr int CX_O_RB = CX_O_WIN + ((CX_WIN + 32 + 15) & ~15);
+constexpr int CX_O_FB = CX_O_WIN + ((CX_WIN + 32 + 15) & ~15);
+// rbits / ebits are dead once P4 starts: P6 stages its output from their
+// start on (CX_STAGE bytes), so dictionaries with a ratio up to ~0.8 still
+// emit through shared memory
+constexpr int CX_O_RB = CX_O_FB + CX_WORDS * 4;
 constexpr int CX_O_EB = CX_O_RB + CX_WORDS * 4;
-constexpr int CX_O_FB = CX_O_EB + CX_WORDS * 4;
-constexpr int CX_O_OUT = CX_O_FB + CX_WORDS * 4;
+constexpr int CX_O_OUT = CX_O_EB + CX_WORDS * 4;
+constexpr int CX_STAGE = CX_O_OUT + CX_OUTCAP - CX_O_RB;
 constexpr int CX_O_RARE = CX_O_OUT + CX_OUTCAP;
 constexpr int CX_O_LA = CX_O_RARE + CX_RARE * (int)sizeof(CxRare);
 constexpr int CX_O_LB = CX_O_LA + CX_NT * 4;
@@ -146,7 +150,7 @@ __device__ inline CxSmem cx_carve(uint8_t *p, int o_t2, int o_codes) {
     S.rbits = reinterpret_cast<unsigned *>(p + CX_O_RB);
     S.ebits = reinterpret_cast<unsigned *>(p + CX_O_EB);
     S.fbits = reinterpret_cast<unsigned *>(p + CX_O_FB);
-    S.out = p + CX_O_OUT;
+    S.out = p + CX_O_RB;  // P6 staging: rbits + ebits + the out buffer (CX_STAGE bytes)
     S.rare = reinterpret_cast<CxRare *>(p + CX_O_RARE);
     S.lane_a = reinterpret_cast<int *>(p + CX_O_LA);
     S.lane_b = reinterpret_cast<int *>(p + CX_O_LB);
@@ -1152,7 +1156,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         const unsigned tile_lines = (unsigned)(tot & 0xffffffu);
         S.lane_c[tid] = (int)(ex & 0xffffffu);  // lane line bases (strict error ordinals)
         if (tid == 0) lookback_publish(job.ts, t, tile_out, (unsigned long long)tile_lines);
-        const bool staged = tile_out <= (unsigned long long)CX_OUTCAP;
+        const bool staged = tile_out <= (unsigned long long)CX_STAGE;
         pc.mark(job, 5);  // output scan
         // ---- P6: emit (to staging now, or to HBM after the look-back) ----
         // Long-line tiles emit byte-exact slices: a slice starts at the first
