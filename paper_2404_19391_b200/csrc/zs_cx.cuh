@@ -28,9 +28,9 @@
 //       staging buffer, then aligned 16-byte stores at the resolved offset.
 //
 // Escape decisions are the byte 0x20 (never a code); the emit re-reads the
-// literal from the input in HBM.  `rbits` marks newlines and ring tokens for
-// P3, `ebits` carries P2's per-line error flags to P3, `fbits` marks filler
-// and arena-marker positions for P6.
+// literal from the input in HBM.  `rbits` marks the newlines (P1), `gbits`
+// the ring-token starts P2 found (P3 walks them), `fbits` filler and
+// arena-marker positions (P6).
 #pragma once
 #include "zs_kernels.cuh"
 
@@ -76,7 +76,7 @@ __host__ __device__ inline int cx_align16(int x) { return (x + 15) & ~15; }
 // keep the compiler from rebuilding buffer addresses inside the hot loops.
 constexpr int CX_O_WIN = 0;
 constexpr int CX_O_FB = CX_O_WIN + ((CX_WIN + 32 + 15) & ~15);
-// rbits / ebits are dead once P4 starts: P6 stages its output from their
+// rbits / gbits are dead once P4 starts: P6 stages its output from their
 // start on (CX_STAGE bytes), so dictionaries with a ratio up to ~0.8 still
 // emit through shared memory
 constexpr int CX_O_RB = CX_O_FB + CX_WORDS * 4;
@@ -136,7 +136,7 @@ struct CxSmem {
     uint8_t *explen;
     uint8_t *lut;
     uint8_t *win;
-    unsigned *rbits, *ebits, *fbits;
+    unsigned *rbits, *gbits, *fbits;  // newlines (P1), ring-token starts (P2), filler (P6)
     uint8_t *out;
     CxRare *rare;
     int *lane_a, *lane_b, *lane_c;
@@ -148,9 +148,9 @@ __device__ inline CxSmem cx_carve(uint8_t *p, int o_t2, int o_codes) {
     CxSmem S;
     S.win = p + CX_O_WIN;
     S.rbits = reinterpret_cast<unsigned *>(p + CX_O_RB);
-    S.ebits = reinterpret_cast<unsigned *>(p + CX_O_EB);
+    S.gbits = reinterpret_cast<unsigned *>(p + CX_O_EB);
     S.fbits = reinterpret_cast<unsigned *>(p + CX_O_FB);
-    S.out = p + CX_O_RB;  // P6 staging: rbits + ebits + the out buffer (CX_STAGE bytes)
+    S.out = p + CX_O_RB;  // P6 staging: rbits + gbits + the out buffer (CX_STAGE bytes)
     S.rare = reinterpret_cast<CxRare *>(p + CX_O_RARE);
     S.lane_a = reinterpret_cast<int *>(p + CX_O_LA);
     S.lane_b = reinterpret_cast<int *>(p + CX_O_LB);
@@ -361,22 +361,23 @@ __device__ __forceinline__ void cx_rare(const CxSmem &S, int *n, int ls, int le,
     }
 }
 
-// clear the ring-token bits of window positions [a, b] (newline bits stay)
-__device__ __forceinline__ void cx_clear_ring_bits(const CxSmem &S, int a, int b) {
+// clear the bits of window positions [a, b]
+__device__ __forceinline__ void cx_clear_bits(unsigned *bm, int a, int b) {
     for (int w = a >> 5; a <= b && w <= (b >> 5); ++w) {
         unsigned m = 0xffffffffu;
         if (w == (a >> 5)) m &= 0xffffffffu << (a & 31);
         if (w == (b >> 5) && (b & 31) != 31) m &= (2u << (b & 31)) - 1u;
-        unsigned nl = 0;
-        const unsigned *w4 = reinterpret_cast<const unsigned *>(S.win + w * 32);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const unsigned x = w4[k] ^ 0x0a0a0a0au;
-            const unsigned z = ~(((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x | 0x7f7f7f7fu);
-            nl |= (((z >> 7) & 1u) | ((z >> 14) & 2u) | ((z >> 21) & 4u) | ((z >> 28) & 8u)) << (4 * k);
-        }
-        atomicAnd(&S.rbits[w], ~(m & ~nl));
+        atomicAnd(&bm[w], ~m);
     }
+}
+
+// last newline before position q (rbits: newlines only), or lo - 1 if none at or after lo
+__device__ __forceinline__ int cx_prev_nl(const unsigned *rb, int q, int lo) {
+    int w = q >> 5;
+    unsigned m = rb[w] & ((1u << (q & 31)) - 1u);
+    while (!m && w > (lo >> 5)) m = rb[--w];
+    const int p = m ? (w << 5) + 31 - __clz(m) : lo - 1;
+    return p < lo ? lo - 1 : p;
 }
 
 __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb, CxTables ct) {
@@ -440,7 +441,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         const long long ws = T0 - CX_HEAD;
         const int tile_end = (int)(T1 - ws);
         cx_load_window(job.in, job.n, ws, cx_align16(tile_end), S.win);
-        for (int k = tid; k < CX_WORDS; k += CX_NT) S.ebits[k] = S.fbits[k] = 0u;
+        for (int k = tid; k < CX_WORDS; k += CX_NT) S.gbits[k] = S.fbits[k] = 0u;
         S.lane_b[tid] = 0;  // lane output adjustments (compaction gaps, arena lines)
         if (lane == 0) S.njobs[tid >> 5] = 0;
         __syncthreads();
@@ -581,14 +582,16 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 if (nl && ((e & 0x60u) | (crs & TK_CR))) {
                     const int k = (crs & TK_CR) ? E_CR : (e & 0x40u) ? E_PERCENT : E_BRACKET;
                     if (k == E_CR || !job.lenient) {
-                        // dropped (lenient CR) or a strict error: filler (P3 fills when it gets there)
+                        // dropped (lenient CR) or a strict error: filler
                         cx_rare(S, &s_nrare, ls, p, job.lenient ? RK_DROP : RK_STRICT, tid, nlines, k, 0);
-                        if (job.preprocess) cx_set(S.ebits, p);  // P3: fill
-                        else filler(ls, p);
+                        filler(ls, p);
                     } else {
                         atomicAdd(&s_flag, 1u);  // lenient: the raw line is compressed
                     }
-                    if (job.preprocess) cx_set(S.ebits, ls);  // P3: not renumbered
+                    if (job.preprocess) {  // P3 does not renumber it: drop its ring-token bits
+                        cx_clear_bits(S.gbits, ls, p);
+                        rmask &= ls > (p & ~31) ? (1u << (ls & 31)) - 1u : 0u;  // this word's, not flushed yet
+                    }
                 }
                 nlines += nl;
                 ls = nl ? p + 1 : ls;
@@ -596,7 +599,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 st = e & 7u;
             };
             auto flush = [&](int p) {  // ring bits of the bitmap word holding p
-                if (rmask && job.preprocess) atomicOr(&S.rbits[p >> 5], rmask);
+                if (rmask && job.preprocess) atomicOr(&S.gbits[p >> 5], rmask);
                 rmask = 0;
             };
             auto walk = [&](auto &&stepfn) {
@@ -701,7 +704,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                     }
                     if (!__syncthreads_or(need)) break;
                     if (need) {
-                        cx_clear_ring_bits(S, s0, e0);
+                        cx_clear_bits(S.gbits, s0, e0);
                         st = truth;
                         flags = 0;
                         walk_fast_range(s0, e0);
@@ -742,110 +745,98 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         // (5+ open rings, colour >= 4, a colour digit that is not an identity
         // code) go to the general routine.
         if (job.preprocess) {
+            // Ring-token events only (gbits); a line's bounds come from the
+            // newline bitmap when its first event arrives, and lines without
+            // events cost nothing.  P2 already turned its error lines into
+            // filler or raw lines and dropped their ring bits.
             const uint8_t *win = S.win;
-            int ls = first, pos = first - 1, local = glob ? 1 : 0;
-            int n_ev = 0, n_cmp = 0;
+            int ls = -1, le = -1;  // the line being renumbered: [ls, le], le its '\n'
             unsigned oid = 0xffffffffu;  // 4 slots: open ring id per byte, 0xff = free
             int op0 = 0, op1 = 0, op2 = 0, op3 = 0;
             int lc0 = -1, lc1 = -1, lc2 = -1, lc3 = -1;
             unsigned n_pct = 0;
-            bool skip = ls <= end && cx_bit(S.ebits, ls), fail = false;
-            // event iterator: the current bitmap word stays in a register
-            // (events come in position order; the range ends with a '\n' event)
-            int ew = (pos + 1) >> 5;
-            unsigned em = pos < end ? S.rbits[ew] & (0xffffffffu << ((pos + 1) & 31)) : 0u;
-            while (pos < end) {
-                while (!em) em = S.rbits[++ew];
-                const int q = (ew << 5) + __ffs(em) - 1;
-                em &= em - 1u;
-                pos = q;
-                ++n_ev;
-                const unsigned c = win[q];
-                if (c == '\n') {
-                    n_cmp += n_pct != 0;
-                    if ((skip | fail | (oid != 0xffffffffu) | (n_pct != 0)) && job.timing < 3) {
-                        if (skip) {
-                            // a P2 error line: dropped / strict lines become filler
-                            cx_clr(S.ebits, ls);
-                            if (cx_bit(S.ebits, q)) {
-                                cx_clr(S.ebits, q);
-                                filler(ls, q);
-                            }
-                        } else if (fail) {
-                            cx_rare(S, &s_nrare, ls, q, RK_ARENA, tid, local, 0, 0);
-                            filler(ls, q);
-                        } else if (oid != 0xffffffffu) {
-                            // ring ids left open (smiles.py:151-159)
-                            if (job.lenient) {
-                                for (int j = ls; j < q; ++j) S.win[j] = job.in[ws + j];
-                                atomicAdd(&s_flag, 1u);
-                            } else {
-                                cx_rare(S, &s_nrare, ls, q, RK_STRICT, tid, local, E_UNPAIRED, 0);
-                                filler(ls, q);
-                            }
-                        } else {
-                            // '%nn' ring tokens: compacted below by the whole warp
-                            const int jn = atomicAdd(&S.njobs[tid >> 5], 1);
-                            if (jn < CX_JOBS) {
-                                S.jobs[(tid >> 5) * CX_JOBS + jn] = make_int4(ls, q, tid, local);
-                            } else {
-                                cx_rare(S, &s_nrare, ls, q, RK_ARENA, tid, local, 0, 0);
-                                filler(ls, q);
-                            }
+            bool fail = false;
+            auto finish = [&]() {  // special handling at the line's end (smiles.py:151-159, 196-202)
+                if (!((fail | (oid != 0xffffffffu) | (n_pct != 0)) && job.timing < 3)) return;
+                const int q = le;
+                const int local = (glob ? 1 : 0) + (ls > first ? cx_popc_range(S.rbits, first, ls - 1) : 0);
+                if (fail) {
+                    cx_rare(S, &s_nrare, ls, q, RK_ARENA, tid, local, 0, 0);
+                    filler(ls, q);
+                } else if (oid != 0xffffffffu) {
+                    // ring ids left open (smiles.py:151-159)
+                    if (job.lenient) {
+                        for (int j = ls; j < q; ++j) S.win[j] = job.in[ws + j];
+                        atomicAdd(&s_flag, 1u);
+                    } else {
+                        cx_rare(S, &s_nrare, ls, q, RK_STRICT, tid, local, E_UNPAIRED, 0);
+                        filler(ls, q);
+                    }
+                } else {
+                    // '%nn' ring tokens: compacted below by the whole warp
+                    const int jn = atomicAdd(&S.njobs[tid >> 5], 1);
+                    if (jn < CX_JOBS) {
+                        S.jobs[(tid >> 5) * CX_JOBS + jn] = make_int4(ls, q, tid, local);
+                    } else {
+                        cx_rare(S, &s_nrare, ls, q, RK_ARENA, tid, local, 0, 0);
+                        filler(ls, q);
+                    }
+                }
+            };
+            if (first <= end && job.timing != 4) {
+                int ew = first >> 5;
+                const int ew_last = end >> 5;
+                unsigned em = S.gbits[ew] & (0xffffffffu << (first & 31));
+                for (;;) {
+                    while (!em && ew < ew_last) em = S.gbits[++ew];
+                    if (!em) break;
+                    const int q = (ew << 5) + __ffs(em) - 1;
+                    if (q > end) break;
+                    em &= em - 1u;
+                    if (q > le) {  // the first event of a new line
+                        if (le >= 0) finish();
+                        le = cx_next(S.rbits, q);
+                        ls = cx_prev_nl(S.rbits, q, first) + 1;
+                        oid = 0xffffffffu;
+                        lc0 = lc1 = lc2 = lc3 = -1;
+                        n_pct = 0;
+                        fail = false;
+                    }
+                    const unsigned c = win[q];
+                    const bool pct = c == '%';
+                    const unsigned rid = pct ? (win[q + 1] - '0') * 10u + (win[q + 2] - '0') : c - '0';
+                    n_pct += pct;
+                    const unsigned v0 = oid & 0xffu, v1 = (oid >> 8) & 0xffu, v2 = (oid >> 16) & 0xffu,
+                                   v3 = oid >> 24;
+                    const int slot = v0 == rid ? 0 : v1 == rid ? 1 : v2 == rid ? 2 : v3 == rid ? 3 : -1;
+                    if (slot < 0) {
+                        // opens a ring in the first free slot
+                        const int fs = v0 == 0xffu ? 0 : v1 == 0xffu ? 1 : v2 == 0xffu ? 2 : v3 == 0xffu ? 3 : -1;
+                        fail |= fs < 0;
+                        op0 = fs == 0 ? q : op0;
+                        op1 = fs == 1 ? q : op1;
+                        op2 = fs == 2 ? q : op2;
+                        op3 = fs == 3 ? q : op3;
+                        oid = fs < 0 ? oid : (oid & ~(0xffu << (8 * fs))) | (rid << (8 * fs));
+                    } else {
+                        // closes the ring opened at o: the smallest colour not
+                        // closed inside (o, q)
+                        const int o = slot == 0 ? op0 : slot == 1 ? op1 : slot == 2 ? op2 : op3;
+                        oid |= 0xffu << (8 * slot);
+                        const int col = lc0 <= o ? 0 : lc1 <= o ? 1 : lc2 <= o ? 2 : lc3 <= o ? 3 : 4;
+                        const bool ok = col < 4 && S.explen['0' + col] != 0;
+                        fail |= !ok;
+                        if (ok && !fail) {
+                            lc0 = col == 0 ? q : lc0;
+                            lc1 = col == 1 ? q : lc1;
+                            lc2 = col == 2 ? q : lc2;
+                            lc3 = col == 3 ? q : lc3;
+                            S.win[o + (win[o] == '%')] = (uint8_t)('0' + col);
+                            S.win[q + pct] = (uint8_t)('0' + col);
                         }
                     }
-                    ls = q + 1;
-                    ++local;
-                    oid = 0xffffffffu;
-                    lc0 = lc1 = lc2 = lc3 = -1;
-                    n_pct = 0;
-                    fail = false;
-                    skip = ls <= end && cx_bit(S.ebits, ls);
-                    continue;
                 }
-                if (job.timing == 4) continue;
-                const bool pct = c == '%';
-                const unsigned rid = pct ? (win[q + 1] - '0') * 10u + (win[q + 2] - '0') : c - '0';
-                n_pct += pct;
-                const unsigned v0 = oid & 0xffu, v1 = (oid >> 8) & 0xffu, v2 = (oid >> 16) & 0xffu,
-                               v3 = oid >> 24;
-                const int slot = v0 == rid ? 0 : v1 == rid ? 1 : v2 == rid ? 2 : v3 == rid ? 3 : -1;
-                if (slot < 0) {
-                    // opens a ring in the first free slot
-                    const int fs = v0 == 0xffu ? 0 : v1 == 0xffu ? 1 : v2 == 0xffu ? 2 : v3 == 0xffu ? 3 : -1;
-                    fail |= fs < 0;
-                    op0 = fs == 0 ? q : op0;
-                    op1 = fs == 1 ? q : op1;
-                    op2 = fs == 2 ? q : op2;
-                    op3 = fs == 3 ? q : op3;
-                    oid = fs < 0 ? oid : (oid & ~(0xffu << (8 * fs))) | (rid << (8 * fs));
-                } else {
-                    // closes the ring opened at o: the smallest colour not
-                    // closed inside (o, q)
-                    const int o = slot == 0 ? op0 : slot == 1 ? op1 : slot == 2 ? op2 : op3;
-                    oid |= 0xffu << (8 * slot);
-                    const int col = lc0 <= o ? 0 : lc1 <= o ? 1 : lc2 <= o ? 2 : lc3 <= o ? 3 : 4;
-                    const bool ok = col < 4 && S.explen['0' + col] != 0;
-                    fail |= !ok;
-                    if (ok && !fail && !skip) {
-                        lc0 = col == 0 ? q : lc0;
-                        lc1 = col == 1 ? q : lc1;
-                        lc2 = col == 2 ? q : lc2;
-                        lc3 = col == 3 ? q : lc3;
-                        S.win[o + (win[o] == '%')] = (uint8_t)('0' + col);
-                        S.win[q + pct] = (uint8_t)('0' + col);
-                    }
-                }
-            }
-            if (job.timing == 2) {  // debug: event statistics
-                const int wmax = __reduce_max_sync(0xffffffffu, n_ev);
-                const int wsum = __reduce_add_sync(0xffffffffu, n_ev);
-                const int wc = __reduce_add_sync(0xffffffffu, n_cmp);
-                if (lane == 0) {
-                    atomicAdd(&job.ctl->phase[3], (unsigned long long)wmax);
-                    atomicAdd(&job.ctl->phase[4], (unsigned long long)wsum);
-                    atomicAdd(&job.ctl->phase[5], (unsigned long long)wc);
-                }
+                if (le >= 0) finish();
             }
             // ---- '%nn' compaction, the whole warp per line: a ring '%nn'
             // token keeps only its colour digit (at '%' + 1); the line's bytes
@@ -865,7 +856,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                     const int r = c0b + lane;
                     const bool valid = r < jq;
                     const unsigned b = valid ? S.win[r] : 0u;
-                    const bool isp = valid && b == '%' && cx_bit(S.rbits, r);
+                    const bool isp = valid && b == '%' && cx_bit(S.gbits, r);
                     const unsigned M = __ballot_sync(0xffffffffu, isp);
                     const unsigned M2 = (M << 2) | carry;
                     const bool drop = isp || ((M2 >> lane) & 1u);
