@@ -208,6 +208,12 @@ __device__ long long compress_line_global(const Job &job, const Tables &tb, long
     }
     h->n_pre = n_pre;
     h->bytes_off = line == src ? -1 : (long long)(pre - job.arena);
+    // same decisions from every parse (tests/test_gpu_parity.py); the table
+    // walks are L1/L2-resident, the dense trie walk costs HBM latency per step
+    if (n_pre < (1ll << 30)) {
+        if (tb.t2) return dp_t2(line, (int)n_pre, dec, tb.dfa2, tb.t2, tb.codes);
+        if (tb.fast) return dp_fast<FAST_W>(line, (int)n_pre, dec, tb.dfa, tb.codes);
+    }
     long long ring[128];
     return dp_generic(line, n_pre, dec, tb, ring);
 }
