@@ -430,7 +430,7 @@ bool build_kw(const std::vector<std::pair<std::string, int>> &pats, int max_len,
     ht.kw_cols = nc;
     ht.kw_cmap.assign(cmap.begin(), cmap.end());
     ht.kw_dfa.assign((size_t)S * nc, 0);
-    ht.kw_codes.assign((size_t)S * KW, 0);
+    ht.kw_codes.assign((size_t)S * CX_CODES, 0);
     for (int q = 0; q < S; ++q) {
         for (int b = 0; b < 256; ++b) {
             const int t = go[rep[q]][b];
@@ -438,7 +438,7 @@ bool build_kw(const std::vector<std::pair<std::string, int>> &pats, int max_len,
         }
         for (int L = 2; L <= KW; ++L) {
             const int c = code[rep[q]][L - 1];
-            ht.kw_codes[(size_t)q * KW + L - 1] = (uint8_t)(c < 0 ? 0 : c);
+            ht.kw_codes[(size_t)q * CX_CODES + L - 1] = (uint8_t)(c < 0 ? 0 : c);
         }
     }
     return true;
@@ -540,7 +540,7 @@ bool build_cx(HostTables &ht, int max_len) {
         }
     // transducer entries as u16: next window (9 bits) | L << 9 | (delta + 4) << 13
     if (nw > 512) return false;
-    ht.cx_t2.assign((size_t)nw * T2_MASKS, 0);
+    ht.cx_t2.assign((size_t)nw * CX_T2S, 0);
     for (int w = 0; w < nw; ++w)
         for (int m = 0; m < T2_MASKS; ++m) {
             const uint32_t x = ht.t2[(size_t)w * T2_MASKS + m];
@@ -554,7 +554,7 @@ bool build_cx(HostTables &ht, int max_len) {
                 if (delta < -4 || delta > 3 || (x & 0xfffu) > 511u) return false;
                 e = (x & 0x1ffu) | (((x >> 12) & 15u) << 9) | ((uint32_t)(delta + 4) << 13);
             }
-            ht.cx_t2[(size_t)w * T2_MASKS + m] = (uint16_t)e;
+            ht.cx_t2[(size_t)w * CX_T2S + m] = (uint16_t)e;
         }
     // code slot L: 0 = escape (0x20, never a code), 2..8 = the match of length L,
     // 9 = '\n'; length 1 is the byte itself

@@ -46,7 +46,9 @@ constexpr int CX_WIN = CX_HEAD + CX_TILE;         // multiple of 32 (bitmap word
 constexpr int CX_WORDS = CX_WIN / 32 + 4;         // bitmap words (multiple of 4: keeps the carve 16-aligned)
 constexpr int CX_NCOL = 119;                      // dcol: umin(b - 10, 118); 0 = '\n'
 constexpr int CX_NLMASK = 15;                     // transducer mask slot of '\n'
-constexpr int CX_CODES = 16;                      // code slots per state: 0 escape, 1-8 match, 9 '\n'
+constexpr int CX_CODES = 20;                      // code-slot row stride (0 escape, 1-8 match, 9 '\n'; 5 words:
+                                                  // rows of random states spread over the 32 banks)
+constexpr int CX_T2S = 18;                        // transducer row stride in u16 (9 words, same reason)
 constexpr int CX_OUTCAP = 17408;                  // staging (tile output up to ratio ~0.55)
 constexpr int CX_RARE = 64;                       // rare lines per tile
 constexpr int CX_JOBS = 16;                       // '%nn' compactions per warp and tile
@@ -90,7 +92,7 @@ constexpr int CX_O_LC = CX_O_LB + CX_NT * 4;
 constexpr int CX_O_JOBS = CX_O_LC + CX_NT * 4;
 constexpr int CX_O_NJOBS = CX_O_JOBS + CX_NW * CX_JOBS * 16;
 constexpr int CX_O_CODES = (CX_O_NJOBS + CX_NW * 4 + 15) & ~15;  // code slots, when they fit here
-constexpr int CX_CODES_CAP = 256 * 16;                              // (transducer DFAs: <= 256 states)
+constexpr int CX_CODES_CAP = 256 * CX_CODES;                        // (transducer DFAs: <= 256 states)
 constexpr int CX_O_DFA = CX_O_CODES + CX_CODES_CAP;
 static_assert(CX_O_JOBS % 16 == 0, "int4 job slots");
 
@@ -101,7 +103,7 @@ struct CxLayout {
 __host__ __device__ inline CxLayout cx_layout(int ns, int nw, int nc) {
     CxLayout L;
     L.o_t2 = CX_O_DFA + cx_align16(ns * nc * 2);
-    const int end_t2 = L.o_t2 + cx_align16(nw * T2_MASKS * 2);
+    const int end_t2 = L.o_t2 + cx_align16(nw * CX_T2S * 2);
     const bool fixed = ns * CX_CODES <= CX_CODES_CAP;  // compile-time offset in the parse loop
     L.o_codes = fixed ? CX_O_CODES : end_t2;
     L.bytes = fixed ? end_t2 : end_t2 + cx_align16(ns * CX_CODES);
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         const uint4 *src = reinterpret_cast<const uint4 *>(ct.dfa);
         uint4 *dst = reinterpret_cast<uint4 *>(S.dfa);
         for (int k = threadIdx.x; k < cx_align16(ct.ns * ct.nc * 2) / 16; k += CX_NT) dst[k] = src[k];
-        for (int k = threadIdx.x; k < ct.nw * T2_MASKS; k += CX_NT) S.t2[k] = ct.t2[k];
+        for (int k = threadIdx.x; k < ct.nw * CX_T2S; k += CX_NT) S.t2[k] = ct.t2[k];
         for (int k = threadIdx.x; k < ct.ns * CX_CODES; k += CX_NT) S.codes[k] = ct.codes[k];
         for (int k = threadIdx.x; k < 256; k += CX_NT) s_cmap[k] = ct.cmap[k];
         for (int k = threadIdx.x; k < 256; k += CX_NT) S.explen[k] = k == '\n' ? 1 : tb.exp_len[k];
@@ -920,7 +922,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
             auto step = [&](unsigned b) -> unsigned {
                 const unsigned e = dfa[st * nc + s_cmap[b]];
                 st = e & 0xffu;
-                const unsigned x = t2[wi * T2_MASKS + (e >> 8)];
+                const unsigned x = t2[wi * CX_T2S + (e >> 8)];
                 wi = x & 0x1ffu;
                 acc += x >> 13;
                 const unsigned L = (x >> 9) & 15u;
