@@ -48,6 +48,7 @@ constexpr int CX_NCOL = 119;                      // dcol: umin(b - 10, 118); 0 
 constexpr int CX_NLMASK = 15;                     // transducer mask slot of '\n'
 constexpr int CX_CODES = 20;                      // code-slot row stride (0 escape, 1-8 match, 9 '\n'; 5 words:
                                                   // rows of random states spread over the 32 banks)
+constexpr int CX_LUTS = 260;                      // tokenizer LUT row stride (65 words)
 constexpr int CX_T2S = 18;                        // transducer row stride in u16 (9 words, same reason)
 constexpr int CX_OUTCAP = 17408;                  // staging (tile output up to ratio ~0.55)
 constexpr int CX_RARE = 64;                       // rare lines per tile
@@ -391,7 +392,9 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
     __shared__ unsigned s_esc, s_skip, s_flag, s_inl;
     __shared__ unsigned long long s_pre_out, s_pre_lines;
 
-    __shared__ __align__(16) uint8_t s_lut[8 * 256];  // tokenizer transducer (static: constant addresses)
+    // tokenizer transducer (static: constant addresses); rows of CX_LUTS bytes so
+    // the same byte in different states falls in different banks
+    __shared__ __align__(16) uint8_t s_lut[8 * CX_LUTS];
     __shared__ __align__(16) uint8_t s_explen[256];
     __shared__ __align__(16) uint8_t s_exp0[256];  // first byte of each code's expansion (P4 re-parse)
     __shared__ __align__(16) uint8_t s_cmap[256];
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 if (job.preprocess && st == TK_IN) e |= 0x20u;
                 if (job.preprocess && (st == TK_ERR || st >= TK_P1R)) e |= 0x40u;
             }
-            S.lut[k] = e;
+            S.lut[st * CX_LUTS + b] = e;
         }
     }
     const int tid = threadIdx.x;
@@ -570,7 +573,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
             unsigned st = TK_OUT0, crs = 0, rmask = 0, flags = 0;
             int ls = first;
             auto step_fast = [&](int p, unsigned b) {
-                const unsigned e = lut[(st << 8) | b];
+                const unsigned e = lut[st * CX_LUTS + b];
                 rmask |= ((e >> 3) & 1u) << (p & 31);
                 flags |= e;
                 nlines += e >> 7;
@@ -578,7 +581,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
             };
             // one tokenizer step at window position p (byte b), per-line errors
             auto step = [&](int p, unsigned b) {
-                const unsigned e = lut[(st << 8) | b];
+                const unsigned e = lut[st * CX_LUTS + b];
                 rmask |= ((e >> 3) & 1u) << (p & 31);
                 const bool nl = e & 128u;
                 if (nl && ((e & 0x60u) | (crs & TK_CR))) {
@@ -640,10 +643,10 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                     unsigned cur = w32[p >> 2];
                     for (; p < w1; p += 4) {
                         const unsigned nxt = w32[(p >> 2) + 1];  // prefetch (the window has slack after it)
-                        const unsigned e0 = lut[(st << 8) | (cur & 0xffu)];
-                        const unsigned e1 = lut[((e0 & 7u) << 8) | ((cur >> 8) & 0xffu)];
-                        const unsigned e2 = lut[((e1 & 7u) << 8) | ((cur >> 16) & 0xffu)];
-                        const unsigned e3 = lut[((e2 & 7u) << 8) | (cur >> 24)];
+                        const unsigned e0 = lut[st * CX_LUTS + (cur & 0xffu)];
+                        const unsigned e1 = lut[(e0 & 7u) * CX_LUTS + ((cur >> 8) & 0xffu)];
+                        const unsigned e2 = lut[(e1 & 7u) * CX_LUTS + ((cur >> 16) & 0xffu)];
+                        const unsigned e3 = lut[(e2 & 7u) * CX_LUTS + (cur >> 24)];
                         st = e3 & 7u;
                         const unsigned ew = e0 | (e1 << 8) | (e2 << 16) | (e3 << 24);
                         flags |= ew;
@@ -690,7 +693,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                         while (p > lim && S.win[p] != '\n') --p;
                         if (S.win[p] == '\n') ++p;
                         else spec = p > R0;  // R0 is a line start
-                        for (; p < s0; ++p) st = lut[(st << 8) | S.win[p]] & 7u;
+                        for (; p < s0; ++p) st = lut[st * CX_LUTS + S.win[p]] & 7u;
                         spec_state = st;
                     }
                     walk_fast_range(s0, e0);
