@@ -107,6 +107,7 @@ def main():
         rng = np.random.default_rng(7)
         sel = rng.integers(0, len(ix), 1_000_000)
         ix.decode(sel[:1000])
+        ix.decode_packed(sel)  # first call at this size allocates its device buffers
         t0 = time.perf_counter()
         data, offs = ix.decode_packed(sel)
         tpk = time.perf_counter() - t0
