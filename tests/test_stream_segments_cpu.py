@@ -96,3 +96,22 @@ def test_framing_edge_cases():
             got = z.run_stream(io.BytesIO(payload), dst, d, "compress", lenient=True, segment_bytes=seg)
             assert dst.getvalue() == (want or b""), (payload, seg)
             assert (got.lines, got.output_bytes, got.skipped) == (st["lines"], st["out_bytes"], st["skipped"])
+
+
+def test_newline_helpers_against_naive():
+    """pipeline._last_nl / _cut_keeping_last (block-wise scans used by the
+    streaming path) against plain Python on random buffers."""
+    rng = np.random.default_rng(5)
+    for n in (0, 1, 5, 100, 3000, (1 << 20) + 777):
+        arr = rng.choice(np.frombuffer(b"ab\n", np.uint8), size=n, p=[0.45, 0.45, 0.10]).astype(np.uint8)
+        raw = arr.tobytes()
+        for lo, hi in ((0, n), (n // 3, n), (0, n // 2)):
+            want = raw.rfind(b"\n", lo, hi)
+            assert pipeline._last_nl(arr, lo, hi) == want
+        if raw.endswith(b"\n"):
+            nls = [i for i, b in enumerate(raw) if b == 10] if n < 5000 else list(np.flatnonzero(arr == 10))
+            for m in (0, 1, 2, len(nls) - 1, len(nls)):
+                if m < 0 or m > len(nls):
+                    continue
+                want = 0 if m >= len(nls) else int(nls[len(nls) - m - 1]) + 1
+                assert pipeline._cut_keeping_last(arr, n, m) == want, (n, m)
