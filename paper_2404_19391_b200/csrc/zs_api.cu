@@ -118,6 +118,8 @@ struct zs_ctx {
     int no_t2 = 0;  // debug: force the key-window DP
     int no_ip = 0;  // debug: force the decision-array kernel
     int dec_variant = 1;  // 1: per-thread slices (default), 0: warp-cooperative
+    int fx_fused_on = 0;  // 1: single-pass fx_fused instead of the three-launch streaming decode
+    int fx_fused_blocks = 0;  // resident fx_fused CTAs per SM
     // per-slot work buffers (NSLOT-deep host pipeline)
     DevBuf ctl[NSLOT], ts[NSLOT], terr[NSLOT], in[NSLOT], out[NSLOT], arena[NSLOT];  // arena: per slot
     DevBuf fxs[NSLOT];  // streaming-decode scratch per slot
@@ -669,10 +671,26 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
                                            : "compress_tiles<0>";
         } else if (fx) {
             const bool al = (reinterpret_cast<uintptr_t>(d_in) & 15) == 0;
+            const bool wide = ctx->tb.max_exp > 7;
+            if (!wide && ctx->fx_fused_on) {
+                auto kf = al ? fx_fused<true> : fx_fused<false>;
+                CK(set_smem(kf, FX_FUSED_SMEM));
+                if (!ctx->fx_fused_blocks)
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->fx_fused_blocks, kf, FX_NT,
+                                                                     FX_FUSED_SMEM));
+                const int g = (int)std::min<long long>(nt, (long long)ctx->n_sm * std::max(1, ctx->fx_fused_blocks));
+                kf<<<g, FX_NT, FX_FUSED_SMEM, st>>>(job, ctx->d_fxe.as<unsigned long long>());
+                CK(cudaGetLastError());
+                if (timed) CK(cudaEventRecord(ctx->ev1, st));
+                ctx->last_kernel = "fx_fused";
+                ctx->nk[slot] = 1;
+                CK(cudaMemcpyAsync(&ctx->h_ctl[slot], ctx->ctl[slot].p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+                CK(cudaEventRecord(ctx->ev_ctl[slot], st));
+                return ZS_OK;
+            }
             if (ctx->fxs[slot].reserve(fx_scratch_bytes(nt)))
                 return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(fx scratch)");
             const FxScratch sc = fx_carve(ctx->fxs[slot].p, nt);
-            const bool wide = ctx->tb.max_exp > 7;
             auto kc = al ? fx_count<true> : fx_count<false>;
             auto ke = wide ? (al ? fx_emit<true, true> : fx_emit<false, true>)
                            : (al ? fx_emit<true, false> : fx_emit<false, false>);
@@ -1186,6 +1204,7 @@ int zs_set_transducer(zs_ctx *ctx, int on) {
     ctx->no_ip = (on & 2) ? 0 : 1;  // bit 1: in-place kernel (needs the transducer)
     ctx->no_cx = (on & 8) ? 1 : 0;  // bit 3: queue-based in-place kernel instead of the lane-chunk one
     ctx->p4_lane = (on & 16) ? 1 : 0;  // bit 4: lane-chunk parse over line-lane ranges (not byte slices)
+    ctx->fx_fused_on = (on & 32) ? 1 : 0;  // bit 5: single-pass fused streaming decode (fx_fused)
     return ZS_OK;
 }
 

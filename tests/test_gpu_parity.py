@@ -370,12 +370,13 @@ def test_device_and_host_api_agree():
     assert (r.lines, r.out_bytes) == (res.lines, res.out_bytes)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 3, 7, 11])
+@pytest.mark.parametrize("mode", [0, 1, 3, 7, 11, 35])
 def test_kernel_variants_bit_exact(corpus_hashes, mode):
     """Every compress kernel variant (0: key-window DP with a decision array,
     1: + cost-window transducer, 3: + in-place decisions -- the lane-chunk
     kernel, the default; 11: the queue-based in-place kernel; bit 2 selects
-    the warp-cooperative decompress instead of the streaming one) gives the
+    the warp-cooperative decompress instead of the streaming one; bit 5 the
+    single-pass fused streaming decode instead of the three launches) gives the
     reference bytes, both directions."""
     ctx = _lib.context()
     try:
@@ -419,10 +420,21 @@ def test_sharded_gpu_codec(world):
     assert blob == want and v.total_lines == st["lines"]
 
 
-def test_streaming_decode_edges():
-    """decompress_fx (byte-local streaming decode): 0x20 runs across thread
-    chunks and tiles, a final record without '\\n', unaligned device input,
-    and bad records that hand the buffer to the record-aware kernel."""
+@pytest.mark.parametrize("mode", [3, 35])
+def test_streaming_decode_edges(mode):
+    """Byte-local streaming decode (mode 3: fx_count / fx_scan / fx_emit,
+    mode 35: fx_fused): 0x20 runs across thread chunks and tiles, a final
+    record without '\\n', unaligned device input, and bad records that hand
+    the buffer to the record-aware kernel."""
+    ctx = _lib.context()
+    try:
+        ctx.lib.zs_set_transducer(ctx.h, mode)
+        _streaming_decode_edges(mode)
+    finally:
+        ctx.lib.zs_set_transducer(ctx.h, 3)
+
+
+def _streaming_decode_edges(mode):
     import torch
     d = z.Dictionary([b"CC", b"c1"], "smiles")
     t = oracle.Tables(d.learned, bytes(sorted(d.identity)))
@@ -455,12 +467,50 @@ def test_streaming_decode_edges():
                 rc = ctx.lib.zs_decompress_device(ctx.h, din.data_ptr() + off, len(comp),
                                                   dout.data_ptr(), dout.numel(), 0, r)
                 ctx.check(rc, "zs_decompress_device")
+                kname = ctx.lib.zs_last_kernel(ctx.h).decode()
+            assert kname == ("fx_fused" if mode == 35 else "fx_count+fx_scan+fx_emit"), kname
             assert dout[:r.out_bytes].cpu().numpy().tobytes() == want, off
     # a dangling escape at EOF, an escaped '\n', unknown codes: record-aware path
     comp = _oracle_check(b"\n".join(lines) + b"\n", d, False, True)
     for bad in (comp + b"C ", comp[:5000] + b" \n" + comp[5000:], comp[:9000] + b"\x99" + comp[9000:]):
         _oracle_check(bad, d, False, True, "decompress")
         _oracle_check(bad, d, False, False, "decompress")
+
+
+@pytest.mark.parametrize("mode", [3, 35])
+def test_decode_capacity(mode):
+    """Streaming decode (3: three launches, 35: fx_fused) with an output
+    buffer too small: ZS_E_CAPACITY with the bytes needed, and nothing
+    written past the caller's capacity."""
+    ctx = _lib.context()
+    try:
+        ctx.lib.zs_set_transducer(ctx.h, mode)
+        _decode_capacity(mode)
+    finally:
+        ctx.lib.zs_set_transducer(ctx.h, 3)
+
+
+def _decode_capacity(mode):
+    import torch
+    d = z.default_dictionary()
+    buf = synth.generate("mixed", 50000, 5)
+    comp, _ = z.run_buffer(buf, d, "compress", preprocess=False)
+    ctx = _lib.context()
+    din = torch.from_numpy(comp).cuda()
+    for cap in (buf.size // 3, buf.size - 100):
+        dout = torch.full((buf.size + 4096,), 0xAB, dtype=torch.uint8, device="cuda")
+        r = _lib.Result()
+        with ctx.lock:
+            ctx.set_dictionary(d)
+            rc = ctx.lib.zs_decompress_device(ctx.h, din.data_ptr(), comp.size, dout.data_ptr(), cap, 0, r)
+            kname = ctx.lib.zs_last_kernel(ctx.h).decode()
+        assert kname == ("fx_fused" if mode == 35 else "fx_count+fx_scan+fx_emit"), kname
+        assert rc == -5 and r.out_bytes == buf.size
+        assert bool((dout[cap:] == 0xAB).all())
+    r = _lib.Result()
+    with ctx.lock:
+        rc = ctx.lib.zs_decompress_device(ctx.h, din.data_ptr(), comp.size, dout.data_ptr(), buf.size, 0, r)
+    assert rc == 0 and dout[:buf.size].cpu().numpy().tobytes() == buf.tobytes()
 
 
 @pytest.mark.parametrize("seg", [5, 97, 4096])
