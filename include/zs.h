@@ -145,7 +145,8 @@ int zs_overlap_batch(zs_ctx *ctx, const int32_t *children, const int16_t *term_l
 /* debug/ablation kernel selection (default 3): bit 0 transducer parse, bit 1
  * in-place decisions (lane-chunk kernel), bit 2 warp-cooperative decompress
  * instead of the streaming one, bit 3 queue-based in-place compress kernel,
- * bit 4 lane-chunk parse over line ranges instead of byte-exact slices */
+ * bit 4 lane-chunk parse over line ranges instead of byte-exact slices,
+ * bit 5 single-pass fused streaming decode (fx_fused) instead of three launches */
 int zs_set_transducer(zs_ctx *ctx, int on);
 
 /* ---- fine-grained parity shim (reference kernel layouts, host memory) ---- */
