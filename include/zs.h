@@ -28,6 +28,10 @@
  * Dictionary tables are passed in the reference's own layouts
  * (Dictionary.encode_trie -> trie.py:22-50; Dictionary.decode_tables ->
  * dictionary.py:112-129); the library derives its device tables from them.
+ *
+ * Measurement and table-inspection hooks (kernel-variant switches, phase
+ * clocks, host-side table builders) are not part of this boundary; they are
+ * declared in zs_debug.h.
  */
 #ifndef ZS_H
 #define ZS_H
@@ -95,15 +99,6 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
 /* DFA window width (2/4/6/8) if the sm_100a fast path (shared-memory DFA)
  * serves the uploaded dictionary, 0 for the generic trie walk */
 int zs_dictionary_fast(zs_ctx *ctx);
-/* Host-only inspection (no GPU needed): derive the fast-path tables from a
- * reference trie.  dfa: uint16[256*97], codes: uint8[256*8].  Returns 1 if
- * the fast path applies, 0 if not, <0 on bad arguments. */
-int zs_build_tables_host(const int32_t *children, const int16_t *term_code, int32_t n_nodes,
-                         uint16_t *dfa, uint8_t *codes, int32_t *n_states, int32_t *max_len);
-/* Host-only inspection of the cost-window transducer: dfa2 uint16[256*97],
- * t2 uint32[1024*16].  Returns 1 if built, 0 if the dictionary does not fit. */
-int zs_build_t2_host(const int32_t *children, const int16_t *term_code, int32_t n_nodes,
-                     uint16_t *dfa2, uint32_t *t2, int32_t *n_windows, int32_t *n_masks);
 /* Random access (pkg/README.md:106-110: "grab line i,
  * decode line i") into a compressed library resident in HBM.
  * zs_index_build: d_offsets[r] = first byte of record r (records framed by
@@ -141,13 +136,6 @@ int zs_train_load(zs_ctx *ctx, const uint8_t *patterns, int32_t width, const int
 int zs_train_select(zs_ctx *ctx, int32_t t, int64_t cap, int64_t *rows_out, int32_t *n_selected);
 int zs_overlap_batch(zs_ctx *ctx, const int32_t *children, const int16_t *term_len, int32_t n_nodes,
                      const uint8_t *pats, int32_t width, const int64_t *lens, int64_t n, int64_t *out);
-
-/* debug/ablation kernel selection (default 3): bit 0 transducer parse, bit 1
- * in-place decisions (lane-chunk kernel), bit 2 warp-cooperative decompress
- * instead of the streaming one, bit 3 queue-based in-place compress kernel,
- * bit 4 lane-chunk parse over line ranges instead of byte-exact slices,
- * bit 5 single-pass fused streaming decode (fx_fused) instead of three launches */
-int zs_set_transducer(zs_ctx *ctx, int on);
 
 /* ---- fine-grained parity shim (reference kernel layouts, host memory) ---- */
 /* out must hold 2*starts[n_lines] bytes; record i lands at out[2*starts[i]] */
@@ -194,11 +182,13 @@ float zs_last_kernel_ms(zs_ctx *ctx);
 const char *zs_last_kernel(zs_ctx *ctx);
 /* the cudaStream_t the device API launches on (for events around whole calls) */
 void *zs_stream(zs_ctx *ctx);
-
-/* profiling aid: per-phase SM cycles of the tile kernels (summed over CTAs,
- * thread 0's view) for the last device-API call; off by default */
-int zs_set_phase_timing(zs_ctx *ctx, int on);
-int zs_last_phase_cycles(zs_ctx *ctx, uint64_t *cycles8);
+/* Stream ordering of the device-pointer calls (zs_*_device, zs_index_build,
+ * zs_decode_records): each call first waits (cudaStreamWaitEvent) for all
+ * work queued so far on `stream` (a cudaStream_t; NULL = the legacy default
+ * stream, the initial setting), so buffers a caller's kernels or copies are
+ * still writing are not read early.  The calls return after their own work
+ * is complete, so their outputs are ready on every stream when they return. */
+int zs_set_stream(zs_ctx *ctx, void *stream);
 
 #ifdef __cplusplus
 }

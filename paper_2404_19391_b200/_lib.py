@@ -13,7 +13,9 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libzs.so")
+# ZS_LIB: an alternative build of the same library (tools load the
+# -DZS_PHASES=1 measurement build, libzs_phases.so, this way)
+LIB_PATH = os.environ.get("ZS_LIB") or os.path.join(_HERE, "libzs.so")
 
 ZS_OK, ZS_E_ARG, ZS_E_CUDA, ZS_E_NOMEM, ZS_E_NODICT, ZS_E_CAPACITY = 0, -1, -2, -3, -4, -5
 F_PREPROCESS, F_LENIENT = 1, 2
@@ -24,11 +26,13 @@ EXPORTS = (
     "zs_dictionary_fast", "zs_compress_batch", "zs_decompress_sizes", "zs_decompress_fill",
     "zs_preprocess_batch", "zs_compress_device", "zs_decompress_device", "zs_compress_host",
     "zs_decompress_host", "zs_compress_bound", "zs_decompress_bound", "zs_last_kernel_ms",
-    "zs_build_tables_host", "zs_set_phase_timing", "zs_last_phase_cycles", "zs_build_t2_host",
-    "zs_set_transducer", "zs_last_kernel", "zs_stream", "zs_index_build", "zs_decode_records",
+    "zs_last_kernel", "zs_stream", "zs_set_stream", "zs_index_build", "zs_decode_records",
     "zs_train_count", "zs_train_rows", "zs_train_load", "zs_train_select", "zs_overlap_batch",
     "zs_host_alloc", "zs_host_free",
 )
+# measurement / inspection hooks (include/zs_debug.h), not part of the boundary
+DEBUG_EXPORTS = ("zs_build_tables_host", "zs_build_t2_host", "zs_set_transducer", "zs_set_phase_timing",
+                 "zs_last_phase_cycles")
 
 
 class Result(ctypes.Structure):
@@ -86,6 +90,7 @@ def load():
             "zs_last_phase_cycles": (ctypes.c_int, [P, P]),
             "zs_last_kernel": (ctypes.c_char_p, [P]),
             "zs_stream": (P, [P]),
+            "zs_set_stream": (ctypes.c_int, [P, P]),
             "zs_index_build": (ctypes.c_int, [P, P, I64, P, I64, ctypes.POINTER(ctypes.c_int64)]),
             "zs_decode_records": (ctypes.c_int, [P, P, P, I64, P, I64, P, I64, P, P, P,
                                                  ctypes.POINTER(ctypes.c_int64)]),
@@ -177,6 +182,14 @@ class Context:
         self.check(rc, "zs_set_dictionary")
         self._dict_key = key
 
+    def follow_torch_stream(self):
+        """Order the next device-pointer calls after the work queued on
+        torch's current stream of this device (zs_set_stream), so tensors
+        torch is still writing are not read early."""
+        import torch
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        self.check(self.lib.zs_set_stream(self.h, s or None), "zs_set_stream")
+
     def fast_width(self) -> int:
         return self.lib.zs_dictionary_fast(self.h)
 
@@ -199,6 +212,8 @@ _ctx_lock = threading.Lock()
 def context(device: int | None = None) -> Context:
     """Process-wide context for `device` (default: the current torch device
     if torch is imported and CUDA-enabled, else 0)."""
+    if isinstance(device, Context):  # an explicit context (e.g. a second one on the same GPU)
+        return device
     if device is None:
         device = int(os.environ.get("ZS_DEVICE", "0"))
     with _ctx_lock:

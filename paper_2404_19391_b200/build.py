@@ -11,8 +11,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "zs_api.cu")
 DEPS = [os.path.join(HERE, "csrc", f) for f in ("zs_api.cu", "zs_kernels.cuh", "zs_device.cuh", "zs_fx.cuh", "zs_cx.cuh", "zs_ix.cuh", "zs_train.cuh")] + \
-       [os.path.join(ROOT, "include", "zs.h")]
+       [os.path.join(ROOT, "include", f) for f in ("zs.h", "zs_debug.h")]
 OUT = os.path.join(HERE, "libzs.so")
+# measurement build: per-phase clocks compiled in (tools/phase_cx.py loads it via ZS_LIB)
+OUT_PHASES = os.path.join(HERE, "libzs_phases.so")
+# debug build: device-side bounds asserts (ZS_CHECKS)
+OUT_CHECKS = os.path.join(HERE, "libzs_checks.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177,550"]
 
@@ -24,15 +28,17 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    stale = not os.path.exists(OUT) or any(os.path.getmtime(d) > os.path.getmtime(OUT) for d in DEPS)
+def build(force: bool = False, verbose: bool = False, phases: bool = False, checks: bool = False) -> str:
+    out = OUT_PHASES if phases else OUT_CHECKS if checks else OUT
+    stale = not os.path.exists(out) or any(os.path.getmtime(d) > os.path.getmtime(out) for d in DEPS)
     if force or stale:
-        cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT, SRC]
+        cmd = [nvcc(), *NVCC_FLAGS, *(["-DZS_PHASES=1"] if phases else []), *(["-DZS_CHECKS=1"] if checks else []), "-o", out, SRC]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, phases="--phases" in sys.argv,
+                checks="--checks" in sys.argv))

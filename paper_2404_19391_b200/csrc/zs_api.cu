@@ -17,7 +17,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/zs.h"
+#include "../../include/zs_debug.h"
 #include "zs_kernels.cuh"
 #include "zs_fx.cuh"
 #include "zs_cx.cuh"
@@ -88,6 +88,12 @@ struct HostTables {
     std::vector<uint16_t> cx_dfa;
     std::vector<uint16_t> cx_t2;
     std::vector<uint8_t> cx_codes;
+    // product automaton of the minimised DFA and the cost-window transducer
+    // (build_pa): one table lookup per byte in compress_cx<true>'s parse
+    bool pa_ok = false;
+    int pa_states = 0, pa_cols = 0;
+    std::vector<uint8_t> pa_cmap4;  // byte -> column * 4
+    std::vector<uint32_t> pa;       // [state][column] entries (PaEntry layout, zs_cx.cuh)
     uint8_t exp_len[256];
     uint16_t exp_off[257];
     std::vector<uint8_t> exp_flat;
@@ -108,8 +114,9 @@ struct zs_ctx {
     HostTables ht;
     Tables tb{};
     int fast_w = 0;
-    DevBuf d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2, d_fxc, d_fxe, d_cxdfa, d_cxt2, d_cxcodes, d_cxcmap;
-    int no_cx = 0;  // debug: force the queue-based compress kernel
+    DevBuf d_pa, d_pacmap, d_dfa, d_codes, d_children, d_term, d_explen, d_expoff, d_expflat, d_dfa2, d_t2, d_fxc, d_fxe, d_cxdfa, d_cxt2, d_cxcodes, d_cxcmap;
+    int no_pa = 0;  // debug: DFA + transducer parse instead of the product automaton
+    int slices = 0;  // compress_cx<true, true>: every phase on byte-exact slices
     int nk[NSLOT] = {};  // kernels the last launch_stream on a slot issued (zs_result.gpu_launches)
     int p4_lane = 0;  // debug: parse per line-lane range instead of byte-exact slices
     bool fx_ok = false;  // streaming decode kernel serves this dictionary (max expansion <= 7)
@@ -117,9 +124,6 @@ struct zs_ctx {
     int fx_wide = -1;           // fx_blocks were sized for this emit variant
     int no_t2 = 0;  // debug: force the key-window DP
     int no_ip = 0;  // debug: force the decision-array kernel
-    int dec_variant = 1;  // 1: per-thread slices (default), 0: warp-cooperative
-    int fx_fused_on = 0;  // 1: single-pass fx_fused instead of the three-launch streaming decode
-    int fx_fused_blocks = 0;  // resident fx_fused CTAs per SM
     // per-slot work buffers (NSLOT-deep host pipeline)
     DevBuf ctl[NSLOT], ts[NSLOT], terr[NSLOT], in[NSLOT], out[NSLOT], arena[NSLOT];  // arena: per slot
     DevBuf fxs[NSLOT];  // streaming-decode scratch per slot
@@ -137,6 +141,8 @@ struct zs_ctx {
     Ctl *h_ctl = nullptr;  // pinned, NSLOT slots
     float last_ms = 0.f;
     int timing = 0;
+    cudaStream_t user_stream = nullptr;  // zs_set_stream: device-pointer calls order after it
+    cudaEvent_t ev_user = nullptr;
 };
 
 namespace {
@@ -151,6 +157,14 @@ int fail(zs_ctx *ctx, cudaError_t e, const char *what) {
         cudaError_t e_ = (call);                         \
         if (e_ != cudaSuccess) return fail(ctx, e_, #call); \
     } while (0)
+
+// device-pointer calls: wait for the work queued on the caller's stream
+// (zs_set_stream) before reading its buffers
+int after_user_stream(zs_ctx *ctx) {
+    CK(cudaEventRecord(ctx->ev_user, ctx->user_stream));
+    CK(cudaStreamWaitEvent(ctx->stream[0], ctx->ev_user, 0));
+    return ZS_OK;
+}
 
 // ---------------------------------------------------------------------------
 // dictionary -> device tables
@@ -455,7 +469,7 @@ int cx_dyn_smem_limit() {
         cudaFuncAttributes fa{};
         if (cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess &&
-            cudaFuncGetAttributes(&fa, compress_cx) == cudaSuccess)
+            cudaFuncGetAttributes(&fa, compress_cx<false, false>) == cudaSuccess)
             lim = optin - (int)fa.sharedSizeBytes;
         else
             lim = 227 * 1024 - 16 * 1024;  // no device: a conservative bound
@@ -574,6 +588,115 @@ bool build_cx(HostTables &ht, int max_len) {
     return true;
 }
 
+// Product automaton for the parse (compress_cx<true>).  The parse state of
+// compress_cx is the pair (minimised DFA state q, cost window w); reading one
+// byte of column c moves it to (dfa(q, c), t2(w, mask(dfa(q, c)))) and emits
+// a decision (code, identity byte, escape or '\n') and a cost delta.  The
+// joint states reachable from the line-end state (0, 0) are enumerated and
+// Moore-minimised over those outputs, and the byte columns are recomputed for
+// the minimised machine: for the default dictionary 164 states x 27 columns,
+// one u32 lookup per byte instead of a DFA, a transducer and a code lookup.
+// Entry: next state's row offset in bytes (bits 0-15) | code << 16 |
+// (cost delta + 4) << 24 | identity << 31 (the decision is the byte itself).
+bool build_pa(HostTables &ht) {
+    ht.pa_ok = false;
+    if (!ht.cx_ok) return false;
+    const int S = ht.cx_states, nc = ht.cx_cols;
+    std::map<std::pair<int, int>, int> id;
+    std::vector<std::pair<int, int>> js{{0, 0}};
+    id[{0, 0}] = 0;
+    std::vector<int> nxt, out;  // [joint][col]: next joint, output (code | d4 << 8 | identity << 11)
+    for (size_t k = 0; k < js.size(); ++k) {
+        const int q = js[k].first, w = js[k].second;
+        for (int c = 0; c < nc; ++c) {
+            const uint16_t e = ht.cx_dfa[(size_t)q * nc + c];
+            const int q2 = e & 0xff, m = e >> 8;
+            const uint16_t x = ht.cx_t2[(size_t)w * CX_T2S + m];
+            const int w2 = x & 0x1ff, L = (x >> 9) & 15, d4 = x >> 13;
+            const int o = L == 1 ? (1 << 11) | (d4 << 8) : (ht.cx_codes[(size_t)q2 * CX_CODES + L] | (d4 << 8));
+            auto it = id.find({q2, w2});
+            int j;
+            if (it == id.end()) {
+                j = (int)js.size();
+                id[{q2, w2}] = j;
+                js.push_back({q2, w2});
+                if (js.size() > 200000) return false;
+            } else {
+                j = it->second;
+            }
+            nxt.push_back(j);
+            out.push_back(o);
+        }
+    }
+    const int N = (int)js.size();
+    // Moore minimisation (partition refinement on (class, outputs, next classes))
+    std::vector<int> cls(N, 0), tmp(N);
+    int ncls = 0;
+    for (int round = 0;; ++round) {
+        std::map<std::vector<int>, int> ids;
+        for (int s = 0; s < N; ++s) {
+            std::vector<int> key;
+            key.reserve(2 * nc + 1);
+            key.push_back(cls[s]);
+            for (int c = 0; c < nc; ++c) {
+                key.push_back(out[(size_t)s * nc + c]);
+                key.push_back(round ? cls[nxt[(size_t)s * nc + c]] : 0);
+            }
+            tmp[s] = ids.emplace(key, (int)ids.size()).first->second;
+        }
+        cls = tmp;
+        if ((int)ids.size() == ncls) break;
+        ncls = (int)ids.size();
+    }
+    // renumber: the line-end state (0, 0) is state 0
+    std::vector<int> ren(ncls, -1), rep;
+    int P = 0;
+    for (int s = 0; s < N; ++s)
+        if (ren[cls[s]] < 0) {
+            ren[cls[s]] = P++;
+            rep.push_back(s);
+        }
+    // byte columns of the minimised machine
+    std::map<std::vector<int>, int> cols;
+    std::vector<int> cmap(256);
+    for (int b = 0; b < 256; ++b) {
+        const int c = ht.cx_cmap[b];
+        std::vector<int> key;
+        for (int p = 0; p < P; ++p) {
+            key.push_back(out[(size_t)rep[p] * nc + c]);
+            key.push_back(ren[cls[nxt[(size_t)rep[p] * nc + c]]]);
+        }
+        cmap[b] = cols.emplace(key, (int)cols.size()).first->second;
+    }
+    const int npc = (int)cols.size();
+    if (npc * 4 > 255 || (long long)P * npc * 4 > 65536) return false;
+    if (CX_O_DFA + cx_align16(P * npc * 4) > cx_dyn_smem_limit()) return false;
+    std::vector<int> col_rep(npc, -1);
+    for (int b = 0; b < 256; ++b)
+        if (col_rep[cmap[b]] < 0) col_rep[cmap[b]] = ht.cx_cmap[b];
+    ht.pa.assign((size_t)P * npc, 0);
+    for (int p = 0; p < P; ++p)
+        for (int k = 0; k < npc; ++k) {
+            const int c = col_rep[k];
+            const int o = out[(size_t)rep[p] * nc + c];
+            const int to = ren[cls[nxt[(size_t)rep[p] * nc + c]]];
+            uint32_t e = (uint32_t)(to * npc * 4);
+            if (o & (1 << 11)) e |= 1u << 31;
+            else e |= (uint32_t)(o & 0xff) << 16;
+            e |= (uint32_t)((o >> 8) & 7) << 24;
+            ht.pa[(size_t)p * npc + k] = e;
+        }
+    ht.pa_states = P;
+    ht.pa_cols = npc;
+    ht.pa_cmap4.resize(256);
+    for (int b = 0; b < 256; ++b) ht.pa_cmap4[b] = (uint8_t)(cmap[b] * 4);
+    ht.pa_ok = true;
+    if (getenv("ZS_VERBOSE"))
+        fprintf(stderr, "zs: parse automaton: %d joint states -> %d states x %d columns (%d B)\n", N, P, npc,
+                P * npc * 4);
+    return true;
+}
+
 template <typename K>
 cudaError_t set_smem(K kernel, int bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -607,11 +730,9 @@ BatchKernel batch_kernel(int w) {
 // one whole-buffer launch (device pointers) on `slot`'s buffers and stream
 int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, long long n,
                   uint8_t *d_out, long long out_cap, int flags, bool timed, bool general = false) {
-    const bool cx = compress && (ctx->ht.cx_ok || ctx->ht.kw_ok) && !general && !ctx->no_cx && !ctx->no_t2 &&
-                    !ctx->no_ip;
-    const bool ip = compress && !cx && ctx->fast_w && ctx->ht.t2_ok && !ctx->no_t2 && !ctx->no_ip;
-    const bool fx = !compress && ctx->fx_ok && !general && ctx->dec_variant == 1;
-    const long long tile = cx ? CX_TILE : ip ? CTILE : fx ? FX_TILE : TILE;
+    const bool cx = compress && (ctx->ht.cx_ok || ctx->ht.kw_ok) && !general && !ctx->no_t2 && !ctx->no_ip;
+    const bool fx = !compress && ctx->fx_ok && !general;
+    const long long tile = cx ? CX_TILE : fx ? FX_TILE : TILE;
     const long long nt = (n + tile - 1) / tile;
     cudaStream_t st = ctx->stream[slot];
     if (ctx->ctl[slot].reserve(sizeof(Ctl)) || ctx->ts[slot].reserve(sizeof(TileState) * (nt + 1)) ||
@@ -643,23 +764,29 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
         if (timed) CK(cudaEventRecord(ctx->ev0, st));
         if (cx) {
             const bool kw = !ctx->ht.cx_ok;
-            const CxLayout L = kw ? cx_layout(ctx->ht.kw_states, 0, 2 * ctx->ht.kw_cols)
-                                  : cx_layout(ctx->ht.cx_states, ctx->ht.n_windows, ctx->ht.cx_cols);
-            const int smem = L.bytes + (kw ? cx_kw_ring_bytes() : 0);
-            CK(set_smem(compress_cx, smem));
-            CxTables ct{ctx->d_cxdfa.as<uint16_t>(), kw ? nullptr : ctx->d_cxt2.as<uint16_t>(),
-                        ctx->d_cxcodes.as<uint8_t>(), ctx->d_cxcmap.as<uint8_t>(),
-                        kw ? ctx->ht.kw_states : ctx->ht.cx_states, kw ? 0 : ctx->ht.n_windows,
-                        kw ? 2 * ctx->ht.kw_cols : ctx->ht.cx_cols, L.o_t2, L.o_codes, ctx->p4_lane ? 0 : 1,
-                        kw ? 1 : 0, L.bytes};
+            const bool pa = ctx->ht.pa_ok && !kw && !ctx->no_pa;
             const int g2 = (int)std::min<long long>(nt, (long long)ctx->n_sm * CX_CTAS);
-            compress_cx<<<g2, CX_NT, smem, st>>>(job, ctx->tb, ct);
-            ctx->last_kernel = kw ? "compress_cx<kw16>" : "compress_cx";
-        } else if (ip) {
-            const int smem = ip_smem_bytes(ctx->tb.n_states, ctx->ht.n_windows);
-            CK(set_smem(compress_tiles_ip, smem));
-            compress_tiles_ip<<<grid, NT, smem, st>>>(job, ctx->tb);
-            ctx->last_kernel = "compress_tiles_ip";
+            if (pa) {
+                const int smem = cx_pa_smem_bytes(ctx->ht.pa_states, ctx->ht.pa_cols);
+                auto k = ctx->slices ? compress_cx<true, true> : compress_cx<true, false>;
+                CK(set_smem(k, smem));
+                CxTables ct{nullptr, nullptr, nullptr, ctx->d_pacmap.as<uint8_t>(), ctx->ht.pa_states, 0,
+                            ctx->ht.pa_cols, 0, 0, ctx->p4_lane ? 0 : 1, 0, smem, ctx->d_pa.as<uint32_t>()};
+                k<<<g2, CX_NT, smem, st>>>(job, ctx->tb, ct);
+                ctx->last_kernel = ctx->slices ? "compress_cx<slices>" : "compress_cx";
+            } else {
+                const CxLayout L = kw ? cx_layout(ctx->ht.kw_states, 0, 2 * ctx->ht.kw_cols)
+                                      : cx_layout(ctx->ht.cx_states, ctx->ht.n_windows, ctx->ht.cx_cols);
+                const int smem = L.bytes + (kw ? cx_kw_ring_bytes() : 0);
+                CK(set_smem(compress_cx<false, false>, smem));
+                CxTables ct{ctx->d_cxdfa.as<uint16_t>(), kw ? nullptr : ctx->d_cxt2.as<uint16_t>(),
+                            ctx->d_cxcodes.as<uint8_t>(), ctx->d_cxcmap.as<uint8_t>(),
+                            kw ? ctx->ht.kw_states : ctx->ht.cx_states, kw ? 0 : ctx->ht.n_windows,
+                            kw ? 2 * ctx->ht.kw_cols : ctx->ht.cx_cols, L.o_t2, L.o_codes, ctx->p4_lane ? 0 : 1,
+                            kw ? 1 : 0, L.bytes, nullptr};
+                compress_cx<false, false><<<g2, CX_NT, smem, st>>>(job, ctx->tb, ct);
+                ctx->last_kernel = kw ? "compress_cx<kw16>" : "compress_cx<t2>";
+            }
         } else if (compress) {
             const bool t2 = ctx->fast_w && ctx->ht.t2_ok && !ctx->no_t2;
             TileKernel k = compress_kernel(ctx->fast_w, t2);
@@ -672,22 +799,6 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
         } else if (fx) {
             const bool al = (reinterpret_cast<uintptr_t>(d_in) & 15) == 0;
             const bool wide = ctx->tb.max_exp > 7;
-            if (!wide && ctx->fx_fused_on) {
-                auto kf = al ? fx_fused<true> : fx_fused<false>;
-                CK(set_smem(kf, FX_FUSED_SMEM));
-                if (!ctx->fx_fused_blocks)
-                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->fx_fused_blocks, kf, FX_NT,
-                                                                     FX_FUSED_SMEM));
-                const int g = (int)std::min<long long>(nt, (long long)ctx->n_sm * std::max(1, ctx->fx_fused_blocks));
-                kf<<<g, FX_NT, FX_FUSED_SMEM, st>>>(job, ctx->d_fxe.as<unsigned long long>());
-                CK(cudaGetLastError());
-                if (timed) CK(cudaEventRecord(ctx->ev1, st));
-                ctx->last_kernel = "fx_fused";
-                ctx->nk[slot] = 1;
-                CK(cudaMemcpyAsync(&ctx->h_ctl[slot], ctx->ctl[slot].p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-                CK(cudaEventRecord(ctx->ev_ctl[slot], st));
-                return ZS_OK;
-            }
             if (ctx->fxs[slot].reserve(fx_scratch_bytes(nt)))
                 return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(fx scratch)");
             const FxScratch sc = fx_carve(ctx->fxs[slot].p, nt);
@@ -710,15 +821,9 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
             ctx->nk[slot] = 3;
         } else {
             const int smem = bp_smem_bytes(ctx->tb.n_flat);
-            if (ctx->dec_variant == 1) {
-                CK(set_smem(decompress_tiles_bp, smem));
-                decompress_tiles_bp<<<grid, NT, smem, st>>>(job, ctx->tb);
-                ctx->last_kernel = "decompress_tiles_bp";
-            } else {
-                CK(set_smem(decompress_tiles_wc, smem));
-                decompress_tiles_wc<<<grid, NT, smem, st>>>(job, ctx->tb);
-                ctx->last_kernel = "decompress_tiles_wc";
-            }
+            CK(set_smem(decompress_tiles_bp, smem));
+            decompress_tiles_bp<<<grid, NT, smem, st>>>(job, ctx->tb);
+            ctx->last_kernel = "decompress_tiles_bp";
         }
         CK(cudaGetLastError());
         if (timed) CK(cudaEventRecord(ctx->ev1, st));
@@ -792,6 +897,7 @@ int run_device(zs_ctx *ctx, bool compress, const uint8_t *d_in, int64_t n, uint8
     if (!ctx->have_dict) return ZS_E_NODICT;
     CK(cudaSetDevice(ctx->dev));
     memset(res, 0, sizeof *res);
+    if (int rc = after_user_stream(ctx)) return rc;
     bool trailing = true;
     if (n > 0) {
         uint8_t last;
@@ -1012,6 +1118,7 @@ int zs_ctx_create(int device, zs_ctx **out) {
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_out[s], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_out[s], ctx->stream[s]);
     }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_user, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_ctl, zs_ctx::NSLOT * sizeof(Ctl));
@@ -1045,6 +1152,7 @@ int zs_ctx_destroy(zs_ctx *ctx) {
         if (ctx->ev_out[s]) cudaEventDestroy(ctx->ev_out[s]);
     }
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev_user) cudaEventDestroy(ctx->ev_user);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
     delete ctx;
@@ -1086,7 +1194,7 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
     for (auto &p : pats) ht.max_len = std::max<int>(ht.max_len, (int)p.first.size());
     ht.fast = build_dfa(pats, ht.max_len, ht);
     ht.cx_ok = ht.kw_ok = false;
-    if (ht.fast && build_t2(ht, std::max(1, ht.max_len))) build_cx(ht, ht.max_len);
+    if (ht.fast && build_t2(ht, std::max(1, ht.max_len)) && build_cx(ht, ht.max_len)) build_pa(ht);
     if (!ht.cx_ok && build_kw(pats, ht.max_len, ht)) {
         const CxLayout L = cx_layout(ht.kw_states, 0, 2 * ht.kw_cols);
         ht.kw_ok = L.bytes + cx_kw_ring_bytes() <= cx_dyn_smem_limit();
@@ -1135,6 +1243,10 @@ int zs_set_dictionary(zs_ctx *ctx, const int32_t *children, const int16_t *term_
         CK(up(ctx->d_cxdfa, ht.cx_dfa.data(), ht.cx_dfa.size() * 2));
         CK(up(ctx->d_cxt2, ht.cx_t2.data(), ht.cx_t2.size() * 2));
         CK(up(ctx->d_cxcodes, ht.cx_codes.data(), ht.cx_codes.size()));
+    }
+    if (ht.pa_ok) {
+        CK(up(ctx->d_pa, ht.pa.data(), ht.pa.size() * 4));
+        CK(up(ctx->d_pacmap, ht.pa_cmap4.data(), 256));
     }
     {
         unsigned fxc[256];
@@ -1197,14 +1309,20 @@ int zs_build_t2_host(const int32_t *children, const int16_t *term_code, int32_t 
     return 1;
 }
 
+int zs_set_stream(zs_ctx *ctx, void *stream) {
+    if (!ctx) return ZS_E_ARG;
+    ctx->user_stream = static_cast<cudaStream_t>(stream);
+    return ZS_OK;
+}
+
 int zs_set_transducer(zs_ctx *ctx, int on) {
     if (!ctx) return ZS_E_ARG;
-    ctx->dec_variant = (on & 4) ? 0 : 1;  // bit 2: warp-cooperative decompress
-    ctx->no_t2 = (on & 1) ? 0 : 1;  // bit 0: transducer parse
-    ctx->no_ip = (on & 2) ? 0 : 1;  // bit 1: in-place kernel (needs the transducer)
-    ctx->no_cx = (on & 8) ? 1 : 0;  // bit 3: queue-based in-place kernel instead of the lane-chunk one
-    ctx->p4_lane = (on & 16) ? 1 : 0;  // bit 4: lane-chunk parse over line-lane ranges (not byte slices)
-    ctx->fx_fused_on = (on & 32) ? 1 : 0;  // bit 5: single-pass fused streaming decode (fx_fused)
+    // measurement / parity switches over the compress kernels (default 3):
+    ctx->no_t2 = (on & 1) ? 0 : 1;   // bit 0 clear: generic key-window / trie-walk kernel (compress_tiles)
+    ctx->no_ip = (on & 2) ? 0 : 1;   // bit 1 clear: likewise (kept for the old mode numbers)
+    ctx->p4_lane = (on & 16) ? 1 : 0;  // bit 4: compress_cx parse over line-lane ranges, not byte slices
+    ctx->no_pa = (on & 64) ? 1 : 0;    // bit 6: DFA + transducer parse instead of the product automaton
+    ctx->slices = (on & 128) ? 1 : 0;  // bit 7: compress_cx on byte-exact slices in every phase
     return ZS_OK;
 }
 
@@ -1231,6 +1349,7 @@ int zs_index_build(zs_ctx *ctx, const uint8_t *d_comp, int64_t n, uint64_t *d_of
     if (!ctx || n < 0 || (n > 0 && !d_comp) || !d_offsets || !n_records) return ZS_E_ARG;
     CK(cudaSetDevice(ctx->dev));
     cudaStream_t st = ctx->stream[0];
+    if (int rc = after_user_stream(ctx)) return rc;
     *n_records = 0;
     if (n == 0) {
         if (cap < 1) return ZS_E_CAPACITY;
@@ -1274,6 +1393,7 @@ int zs_decode_records(zs_ctx *ctx, const uint8_t *d_comp, const uint64_t *d_offs
     if (!ctx->have_dict) return ZS_E_NODICT;
     CK(cudaSetDevice(ctx->dev));
     cudaStream_t st = ctx->stream[0];
+    if (int rc = after_user_stream(ctx)) return rc;
     *total_out = 0;
     if (k == 0) return ZS_OK;
     if (ctx->ixs.reserve((size_t)k * 8 + 64)) return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(index)");

@@ -33,6 +33,12 @@
 // arena-marker positions (P6).
 #pragma once
 #include "zs_kernels.cuh"
+#ifdef ZS_CHECKS
+#include <cassert>
+#define ZS_ASSERT(c) assert(c)
+#else
+#define ZS_ASSERT(c) ((void)0)
+#endif
 
 namespace zs {
 
@@ -55,6 +61,8 @@ constexpr int CX_RARE = 64;                       // rare lines per tile
 constexpr int CX_JOBS = 16;                       // '%nn' compactions per warp and tile
 constexpr int CX_WARM = 32;                       // P4 warm-up bytes right of a slice (speculative entry)
 constexpr int CX_XLONG = 4 * CX_CC;               // P4 uses byte-exact slices when a line-lane range is longer
+constexpr int CX_PWARM = 8;                       // PA: warm-up bytes of a slice's guessed P4 / P6 entry
+static_assert((CX_WIN + CX_NT) / CX_NT + 31 <= 128, "a P3 slice spans at most 4 bitmap words");
 
 // rare-line kinds
 enum : int { RK_DROP = 1, RK_ARENA = 2, RK_STRICT = 3 };
@@ -90,9 +98,14 @@ constexpr int CX_O_RARE = CX_O_OUT + CX_OUTCAP;
 constexpr int CX_O_LA = CX_O_RARE + CX_RARE * (int)sizeof(CxRare);
 constexpr int CX_O_LB = CX_O_LA + CX_NT * 4;
 constexpr int CX_O_LC = CX_O_LB + CX_NT * 4;
-constexpr int CX_O_JOBS = CX_O_LC + CX_NT * 4;
+constexpr int CX_O_LF = CX_O_LC + CX_NT * 4;      // per line-lane: first in-window line byte | glob << 30
+constexpr int CX_O_JOBS = CX_O_LF + CX_NT * 4;
 constexpr int CX_O_NJOBS = CX_O_JOBS + CX_NW * CX_JOBS * 16;
-constexpr int CX_O_CODES = (CX_O_NJOBS + CX_NW * 4 + 15) & ~15;  // code slots, when they fit here
+constexpr int CX_POOL = 1536;                     // P3 (PA): lines with ring events per tile, sorted
+constexpr int CX_HIST = 64;                       // P3 (PA): event-count buckets
+constexpr int CX_O_POOL = (CX_O_NJOBS + CX_NW * 4 + 15) & ~15;
+constexpr int CX_O_HIST = CX_O_POOL + CX_POOL * 4;
+constexpr int CX_O_CODES = (CX_O_HIST + CX_HIST * 4 + 15) & ~15;  // code slots, when they fit here
 constexpr int CX_CODES_CAP = 256 * CX_CODES;                        // (transducer DFAs: <= 256 states)
 constexpr int CX_O_DFA = CX_O_CODES + CX_CODES_CAP;
 static_assert(CX_O_JOBS % 16 == 0, "int4 job slots");
@@ -126,7 +139,11 @@ struct CxTables {
     int p4x;               // 1: byte-exact parse slices (default), 0: parse the lane's line range
     int kw;                // 1: key-window parse (patterns up to 16 bytes; dfa = u32 [states][nc/2])
     int o_ring;            // kw: per-thread key rings (cx_kw_ring_bytes) at this smem offset
+    const uint32_t *pa;    // compress_cx<true>: parse automaton [ns][nc] (build_pa); cmap = column * 4
 };
+
+// shared memory of compress_cx<true>: the fixed buffers, then the parse automaton
+__host__ __device__ inline int cx_pa_smem_bytes(int ns, int nc) { return CX_O_DFA + cx_align16(ns * nc * 4); }
 
 // kw: a 32-entry key ring per thread (stride 33 words: conflict-free banks)
 constexpr int CX_KW_RING = 33;
@@ -142,9 +159,11 @@ struct CxSmem {
     unsigned *rbits, *gbits, *fbits;  // newlines (P1), ring-token starts (P2), filler (P6)
     uint8_t *out;
     CxRare *rare;
-    int *lane_a, *lane_b, *lane_c;
+    int *lane_a, *lane_b, *lane_c, *lane_f;
     int4 *jobs;   // [warp][CX_JOBS] (ls, q, owner lane, local line index)
     int *njobs;   // [warp]
+    uint32_t *pool;  // [CX_POOL] lines with ring events: first event | '\n' << 16 (P3, PA)
+    int *hist;       // [CX_HIST] event-count buckets (P3, PA)
 };
 
 __device__ inline CxSmem cx_carve(uint8_t *p, int o_t2, int o_codes) {
@@ -158,8 +177,11 @@ __device__ inline CxSmem cx_carve(uint8_t *p, int o_t2, int o_codes) {
     S.lane_a = reinterpret_cast<int *>(p + CX_O_LA);
     S.lane_b = reinterpret_cast<int *>(p + CX_O_LB);
     S.lane_c = reinterpret_cast<int *>(p + CX_O_LC);
+    S.lane_f = reinterpret_cast<int *>(p + CX_O_LF);
     S.jobs = reinterpret_cast<int4 *>(p + CX_O_JOBS);
     S.njobs = reinterpret_cast<int *>(p + CX_O_NJOBS);
+    S.pool = reinterpret_cast<uint32_t *>(p + CX_O_POOL);
+    S.hist = reinterpret_cast<int *>(p + CX_O_HIST);
     S.dfa = reinterpret_cast<uint16_t *>(p + CX_O_DFA);
     S.t2 = reinterpret_cast<uint16_t *>(p + o_t2);
     S.codes = p + o_codes;
@@ -383,12 +405,20 @@ __device__ __forceinline__ int cx_prev_nl(const unsigned *rb, int q, int lo) {
     return p < lo ? lo - 1 : p;
 }
 
+// PA: the parse runs the product automaton (one lookup per byte) instead of
+// the DFA + cost-window transducer + code slots.
+// SL: every phase on byte-exact slices (P2 and P4 entered by guess and
+// repaired up to where the guessed and the true walks meet, P3 over lines
+// bucket-sorted by event count, P6 by path entry guess + repair): balanced
+// lanes, but a block barrier between phases (measured slower on C2 than the
+// barrier-free line-lane pipeline; kept as a mode)
+template <bool PA, bool SL>
 __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb, CxTables ct) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int s_tmp[CX_NW];
     __shared__ unsigned long long s_tmp64[CX_NW];
     __shared__ long long s_tile;
-    __shared__ int s_head_nl, s_last_nl, s_nrare, s_err_ord, s_r0, s_r2;
+    __shared__ int s_head_nl, s_last_nl, s_nrare, s_err_ord, s_r0, s_r2, s_nfe;
     __shared__ unsigned s_esc, s_skip, s_flag, s_inl;
     __shared__ unsigned long long s_pre_out, s_pre_lines;
 
@@ -402,11 +432,16 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
     S.lut = s_lut;
     S.explen = s_explen;
     {
-        const uint4 *src = reinterpret_cast<const uint4 *>(ct.dfa);
-        uint4 *dst = reinterpret_cast<uint4 *>(S.dfa);
-        for (int k = threadIdx.x; k < cx_align16(ct.ns * ct.nc * 2) / 16; k += CX_NT) dst[k] = src[k];
-        for (int k = threadIdx.x; k < ct.nw * CX_T2S; k += CX_NT) S.t2[k] = ct.t2[k];
-        for (int k = threadIdx.x; k < ct.ns * CX_CODES; k += CX_NT) S.codes[k] = ct.codes[k];
+        if (PA) {
+            uint32_t *dst = reinterpret_cast<uint32_t *>(S.dfa);
+            for (int k = threadIdx.x; k < ct.ns * ct.nc; k += CX_NT) dst[k] = ct.pa[k];
+        } else {
+            const uint4 *src = reinterpret_cast<const uint4 *>(ct.dfa);
+            uint4 *dst = reinterpret_cast<uint4 *>(S.dfa);
+            for (int k = threadIdx.x; k < cx_align16(ct.ns * ct.nc * 2) / 16; k += CX_NT) dst[k] = src[k];
+            for (int k = threadIdx.x; k < ct.nw * CX_T2S; k += CX_NT) S.t2[k] = ct.t2[k];
+            for (int k = threadIdx.x; k < ct.ns * CX_CODES; k += CX_NT) S.codes[k] = ct.codes[k];
+        }
         for (int k = threadIdx.x; k < 256; k += CX_NT) s_cmap[k] = ct.cmap[k];
         for (int k = threadIdx.x; k < 256; k += CX_NT) S.explen[k] = k == '\n' ? 1 : tb.exp_len[k];
         for (int k = threadIdx.x; k < 256; k += CX_NT)
@@ -448,6 +483,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         cx_load_window(job.in, job.n, ws, cx_align16(tile_end), S.win);
         for (int k = tid; k < CX_WORDS; k += CX_NT) S.gbits[k] = S.fbits[k] = 0u;
         S.lane_b[tid] = 0;  // lane output adjustments (compaction gaps, arena lines)
+        if (PA && tid < CX_HIST) S.hist[tid] = 0;  // P3 buckets
         if (lane == 0) S.njobs[tid >> 5] = 0;
         __syncthreads();
         // the final tile closes a last line without '\n' with a virtual one
@@ -525,7 +561,8 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
             start = gpos;
         }
         const int first = glob ? gpos + 1 : start;  // first byte of the first in-window line
-        if (job.timing == 2) {  // debug: lane range statistics
+        S.lane_f[tid] = first | (glob ? 1 << 30 : 0);
+        if (kPhases && job.timing == 2) {  // debug: lane range statistics
             const int len = max(0, end - start + 1);
             const int wmax = __reduce_max_sync(0xffffffffu, len);
             const int wsum = __reduce_add_sync(0xffffffffu, len);
@@ -561,6 +598,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         // it only when a line-lane range is much longer than a slice).  Every
         // warp derives the same decision from lane_a.
         bool long_ranges = false;
+        bool p2_regular = true;  // P2 ended with the per-line walks (no final block barrier)
         if (ct.p4x) {
             int mx = 0;
             for (int k = lane; k < CX_NT; k += 32)
@@ -664,8 +702,8 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 flush(end);
                 flags |= (flags >> 8) | (flags >> 16) | (flags >> 24);
             };
-            bool regular = true;
-            if (long_ranges) {
+            bool &regular = p2_regular;
+            if (SL || long_ranges) {
                 // ---- P2 on byte-exact slices ----
                 // A slice is entered in the tokenizer state a newline leaves
                 // (found within CX_WARM bytes to its left, or the region start),
@@ -687,7 +725,9 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 flags = 0;
                 st = TK_OUT0;
                 if (sz > 0 && s0 <= e0) {
-                    if (s0 > R0 && S.win[s0 - 1] != '\n') {
+                    if (SL && s0 > R0 && S.win[s0 - 1] != '\n') {
+                        spec = true;  // guess TK_OUT0, repaired below up to where the walks meet
+                    } else if (s0 > R0 && S.win[s0 - 1] != '\n') {
                         const int lim = max(R0, s0 - CX_WARM);
                         int p = s0 - 1;
                         while (p > lim && S.win[p] != '\n') --p;
@@ -708,7 +748,27 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                         need = truth != spec_state;
                     }
                     if (!__syncthreads_or(need)) break;
-                    if (need) {
+                    if (SL && need) {
+                        // walk again from the true entry state next to the guessed
+                        // one until the two states meet; fix the ring bits of the
+                        // bytes where they differ
+                        unsigned so = spec_state, sn = truth;
+                        int p = s0;
+                        for (; p <= e0; ++p) {
+                            const unsigned b = S.win[p];
+                            const unsigned eo = lut[so * CX_LUTS + b], en = lut[sn * CX_LUTS + b];
+                            so = eo & 7u;
+                            sn = en & 7u;
+                            flags |= en;
+                            if (((eo ^ en) & 8u) && job.preprocess) {
+                                if (en & 8u) atomicOr(&S.gbits[p >> 5], 1u << (p & 31));
+                                else atomicAnd(&S.gbits[p >> 5], ~(1u << (p & 31)));
+                            }
+                            if (so == sn) break;
+                        }
+                        spec_state = truth;
+                        if (p > e0) S.lane_c[tid] = (int)sn;
+                    } else if (need) {
                         cx_clear_bits(S.gbits, s0, e0);
                         st = truth;
                         flags = 0;
@@ -762,33 +822,255 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
             unsigned n_pct = 0;
             bool fail = false;
             auto finish = [&]() {  // special handling at the line's end (smiles.py:151-159, 196-202)
-                if (!((fail | (oid != 0xffffffffu) | (n_pct != 0)) && job.timing < 3)) return;
+                if (!((fail | (oid != 0xffffffffu) | (n_pct != 0)) && (!kPhases || job.timing < 3))) return;
                 const int q = le;
-                const int local = (glob ? 1 : 0) + (ls > first ? cx_popc_range(S.rbits, first, ls - 1) : 0);
+                // the line-lane owning the line (P3 slices: not this lane) and the
+                // line's index in it
+                int own = tid, local;
+                if (SL) {
+                    int lo = 0, hi = CX_NT - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (S.lane_a[mid] < ls) lo = mid;
+                        else hi = mid - 1;
+                    }
+                    own = lo;
+                    const int f = S.lane_f[own], f0 = f & ((1 << 30) - 1);
+                    local = (f >> 30) + (ls > f0 ? cx_popc_range(S.rbits, f0, ls - 1) : 0);
+                } else {
+                    local = (glob ? 1 : 0) + (ls > first ? cx_popc_range(S.rbits, first, ls - 1) : 0);
+                }
+                auto fill = [&](int a, int b) {
+                    if (SL) {
+                        for (int j = a; j <= b; ++j) {
+                            S.win[j] = 0x01;
+                            cx_set(S.fbits, j);
+                        }
+                        atomicAdd(&S.lane_b[own], -2 * (b - a + 1));
+                    } else {
+                        filler(a, b);
+                    }
+                };
                 if (fail) {
-                    cx_rare(S, &s_nrare, ls, q, RK_ARENA, tid, local, 0, 0);
-                    filler(ls, q);
+#ifdef ZS_CHECKS
+                    if (t < 4) {
+                        char buf[96];
+                        int k = 0;
+                        for (int j = ls; j <= q && k < 90; ++j) buf[k++] = job.in[ws + j] == '\n' ? '|' : (char)job.in[ws + j];
+                        buf[k] = 0;
+                        printf("tile %lld tid %d fail line [%d,%d] oid %08x: %s\n", t, tid, ls, q, oid, buf);
+                    }
+#endif
+                    cx_rare(S, &s_nrare, ls, q, RK_ARENA, own, local, 0, 0);
+                    fill(ls, q);
                 } else if (oid != 0xffffffffu) {
                     // ring ids left open (smiles.py:151-159)
                     if (job.lenient) {
                         for (int j = ls; j < q; ++j) S.win[j] = job.in[ws + j];
                         atomicAdd(&s_flag, 1u);
                     } else {
-                        cx_rare(S, &s_nrare, ls, q, RK_STRICT, tid, local, E_UNPAIRED, 0);
-                        filler(ls, q);
+                        cx_rare(S, &s_nrare, ls, q, RK_STRICT, own, local, E_UNPAIRED, 0);
+                        fill(ls, q);
                     }
                 } else {
-                    // '%nn' ring tokens: compacted below by the whole warp
-                    const int jn = atomicAdd(&S.njobs[tid >> 5], 1);
-                    if (jn < CX_JOBS) {
-                        S.jobs[(tid >> 5) * CX_JOBS + jn] = make_int4(ls, q, tid, local);
+                    // '%nn' ring tokens: compacted below by a whole warp (PA: one
+                    // job list per CTA, spread over the warps after P3)
+                    const int jn = atomicAdd(&S.njobs[SL ? 0 : tid >> 5], 1);
+                    if (jn < (SL ? CX_NW * CX_JOBS : CX_JOBS)) {
+                        S.jobs[SL ? jn : (tid >> 5) * CX_JOBS + jn] = make_int4(ls, q, own, local);
                     } else {
-                        cx_rare(S, &s_nrare, ls, q, RK_ARENA, tid, local, 0, 0);
-                        filler(ls, q);
+                        cx_rare(S, &s_nrare, ls, q, RK_ARENA, own, local, 0, 0);
+                        fill(ls, q);
                     }
                 }
             };
-            if (first <= end && job.timing != 4) {
+            // PA: byte-exact slices of the tile's lines: a lane renumbers the
+            // lines whose first ring event lies in its slice (to their end), so
+            // every lane walks about the same number of events.  The lines of
+            // other line-lanes must be through P2 (ring bits final) first.
+            int p3a = first, p3b = end, p3lo = first;
+            if (SL) {
+                if (p2_regular) __syncthreads();  // P2's per-line walks of every warp done (else P2 ended on a barrier)
+                const int R0 = s_r2, R1 = s_last_nl;
+                const int sz = R1 >= R0 ? (R1 - R0 + CX_NT) / CX_NT : 0;
+                p3a = R0 + tid * sz;
+                p3b = sz > 0 ? min(R1, p3a + sz - 1) : p3a - 1;
+                p3lo = R0;
+            }
+            // one ring event of the current line (smiles.py:140-180 restated
+            // over 4 open-ring slots and the per-colour last-close positions)
+            auto ring_event = [&](int q) {
+                ZS_ASSERT(q >= 0 && q < le && q < CX_WIN);
+                const unsigned c = win[q];
+                ZS_ASSERT(c == '%' || (c >= '0' && c <= '9'));
+                const bool pct = c == '%';
+                const unsigned rid = pct ? (win[q + 1] - '0') * 10u + (win[q + 2] - '0') : c - '0';
+                n_pct += pct;
+                const unsigned v0 = oid & 0xffu, v1 = (oid >> 8) & 0xffu, v2 = (oid >> 16) & 0xffu, v3 = oid >> 24;
+                const int slot = v0 == rid ? 0 : v1 == rid ? 1 : v2 == rid ? 2 : v3 == rid ? 3 : -1;
+                if (slot < 0) {
+                    const int fs = v0 == 0xffu ? 0 : v1 == 0xffu ? 1 : v2 == 0xffu ? 2 : v3 == 0xffu ? 3 : -1;
+                    fail |= fs < 0;
+                    op0 = fs == 0 ? q : op0;
+                    op1 = fs == 1 ? q : op1;
+                    op2 = fs == 2 ? q : op2;
+                    op3 = fs == 3 ? q : op3;
+                    oid = fs < 0 ? oid : (oid & ~(0xffu << (8 * fs))) | (rid << (8 * fs));
+                } else {
+                    const int o = slot == 0 ? op0 : slot == 1 ? op1 : slot == 2 ? op2 : op3;
+                    oid |= 0xffu << (8 * slot);
+                    const int col = lc0 <= o ? 0 : lc1 <= o ? 1 : lc2 <= o ? 2 : lc3 <= o ? 3 : 4;
+                    const bool ok = col < 4 && S.explen['0' + col] != 0;
+                    fail |= !ok;
+                    if (ok && !fail) {
+                        lc0 = col == 0 ? q : lc0;
+                        lc1 = col == 1 ? q : lc1;
+                        lc2 = col == 2 ? q : lc2;
+                        lc3 = col == 3 ? q : lc3;
+                        S.win[o + (win[o] == '%')] = (uint8_t)('0' + col);
+                        S.win[q + pct] = (uint8_t)('0' + col);
+                    }
+                }
+            };
+            if (SL && (!kPhases || job.timing != 4)) {
+                // Line-first ring events of the slice (an event whose previous
+                // newline-or-event mark is a newline): with X = newlines |
+                // events, ~X + (newlines << 1) carries each newline's bit up to
+                // the next mark; the marks it reaches that are events start a
+                // line.  Each line is renumbered by one lane, event by event;
+                // a tile has ~1.7 such lines per lane and their event counts
+                // vary, so the lines are bucket-sorted by event count
+                // (descending) and lane t takes sorted lines t, t + CX_NT, ...:
+                // the lanes of a warp walk lines of about the same length.
+                unsigned nfe = 0;
+                const int w0 = p3a >> 5, w1 = p3b >> 5;
+                unsigned cin = 1;  // the last mark before word w0 is a newline (or the region start)
+                if (p3a <= p3b) {
+                    for (int v = w0 - 1; v >= (p3lo >> 5); --v) {
+                        unsigned xm = S.rbits[v] | S.gbits[v];
+                        if (v == (p3lo >> 5)) xm &= 0xffffffffu << (p3lo & 31);
+                        if (xm) {
+                            cin = (S.rbits[v] >> (31 - __clz(xm))) & 1u;
+                            break;
+                        }
+                    }
+                }
+                unsigned fe_w[4];  // line-first event bits of the slice's words (<= 4 words)
+                #pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    fe_w[k] = 0;
+                    const int w = w0 + k;
+                    if (p3a <= p3b && w <= w1) {
+                        const unsigned N = S.rbits[w], E = S.gbits[w], X = N | E;
+                        const unsigned fe = ((~X) + (N << 1) + cin) & E;
+                        unsigned m = 0xffffffffu;
+                        if (w == w0) m &= 0xffffffffu << (p3a & 31);
+                        if (w == w1 && (p3b & 31) != 31) m &= (2u << (p3b & 31)) - 1u;
+                        fe_w[k] = fe & m;
+                        nfe += __popc(fe_w[k]);
+                        cin = X ? (N >> (31 - __clz(X))) & 1u : cin;
+                    }
+                }
+                // bucket-sort the lines by (about) their event count,
+                // descending: the events between a line-first event and the
+                // next one in the slice (the slice's last line: to the slice
+                // end) -- only the order depends on it
+                auto keys = [&](auto &&fn) {
+                    int prev = -1;
+                    #pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        unsigned m = fe_w[k];
+                        while (m) {
+                            const int q0 = ((w0 + k) << 5) + __ffs(m) - 1;
+                            m &= m - 1u;
+                            if (prev >= 0) fn(prev, cx_popc_range(S.gbits, prev, q0 - 1));
+                            prev = q0;
+                        }
+                    }
+                    if (prev >= 0) fn(prev, cx_popc_range(S.gbits, prev, p3b));
+                };
+                int nfe_all;
+                {
+                    keys([&](int, int ne) { atomicAdd(&S.hist[CX_HIST - 1 - min(ne, CX_HIST - 1)], 1); });
+                    __syncthreads();
+                    if (tid < 32) {  // exclusive scan of the 64 buckets
+                        const int h0 = S.hist[2 * lane], h1 = S.hist[2 * lane + 1];
+                        int x = h0 + h1;
+                        #pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int y = __shfl_up_sync(0xffffffffu, x, o);
+                            if (lane >= o) x += y;
+                        }
+                        S.hist[2 * lane] = x - h0 - h1;
+                        S.hist[2 * lane + 1] = x - h1;
+                        if (lane == 31) s_nfe = x;
+                    }
+                    __syncthreads();
+                    nfe_all = s_nfe;
+                }
+                const bool pooled = nfe_all <= CX_POOL;
+                if (pooled)
+                    keys([&](int q0, int ne) {
+                        const int at = atomicAdd(&S.hist[CX_HIST - 1 - min(ne, CX_HIST - 1)], 1);
+                        ZS_ASSERT(at >= 0 && at < nfe_all);
+                        S.pool[at] = (uint32_t)q0;
+                    });
+                __syncthreads();
+                if (pooled) {
+                    for (int i = tid; i < nfe_all; i += CX_NT) {
+                        const int q0 = (int)S.pool[i];
+                        le = cx_next(S.rbits, q0);
+                        ZS_ASSERT(q0 >= p3lo && q0 < le && le <= s_last_nl && S.win[le] == '\n');
+                        ls = cx_prev_nl(S.rbits, q0, p3lo) + 1;
+                        oid = 0xffffffffu;
+                        lc0 = lc1 = lc2 = lc3 = -1;
+                        n_pct = 0;
+                        fail = false;
+                        int ew = q0 >> 5;
+                        const int ew_last = le >> 5;
+                        unsigned em = S.gbits[ew] & (0xffffffffu << (q0 & 31));
+                        for (;;) {
+                            while (!em && ew < ew_last) em = S.gbits[++ew];
+                            const int q = em ? (ew << 5) + __ffs(em) - 1 : 0x7fffffff;
+                            if (q > le) break;
+                            em &= em - 1u;
+                            ring_event(q);
+                        }
+                        finish();
+                    }
+                    le = -1;
+                } else if (p3a <= p3b) {
+                    // (more line-first events than the queue holds: this lane
+                    // walks the lines that start in its slice itself)
+                    #pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        unsigned m = fe_w[k];
+                        while (m) {
+                            const int q0 = ((w0 + k) << 5) + __ffs(m) - 1;
+                            m &= m - 1u;
+                            le = cx_next(S.rbits, q0);
+                            ls = cx_prev_nl(S.rbits, q0, p3lo) + 1;
+                            oid = 0xffffffffu;
+                            lc0 = lc1 = lc2 = lc3 = -1;
+                            n_pct = 0;
+                            fail = false;
+                            int ew = q0 >> 5;
+                            unsigned em = S.gbits[ew] & (0xffffffffu << (q0 & 31));
+                            for (;;) {
+                                while (!em && ew < (le >> 5)) em = S.gbits[++ew];
+                                if (!em) break;
+                                const int qq = (ew << 5) + __ffs(em) - 1;
+                                if (qq > le) break;
+                                em &= em - 1u;
+                                ring_event(qq);
+                            }
+                            finish();
+                        }
+                    }
+                    le = -1;
+                }
+            }
+            if (!SL && first <= end && (!kPhases || job.timing != 4)) {
                 int ew = first >> 5;
                 const int ew_last = end >> 5;
                 unsigned em = S.gbits[ew] & (0xffffffffu << (first & 31));
@@ -849,10 +1131,11 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
             // filler.  A byte that could be escaped in a shifted line (its
             // literal is re-read from HBM by position) sends the line to the
             // general routine instead.
-            __syncwarp();
-            const int nj = min(S.njobs[tid >> 5], CX_JOBS);
-            for (int j = 0; j < nj; ++j) {
-                const int4 J = S.jobs[(tid >> 5) * CX_JOBS + j];
+            if (SL) __syncthreads();
+            else __syncwarp();
+            const int nj = SL ? min(S.njobs[0], CX_NW * CX_JOBS) : min(S.njobs[tid >> 5], CX_JOBS);
+            for (int j = SL ? tid >> 5 : 0; j < nj; j += SL ? CX_NW : 1) {
+                const int4 J = S.jobs[SL ? j : (tid >> 5) * CX_JOBS + j];
                 const int jls = J.x, jq = J.y;
                 int kept = 0;
                 unsigned carry = 0;  // ring-'%' flags of the previous chunk's last two bytes
@@ -922,7 +1205,14 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
             const int nc = ct.nc;
             uint8_t *win = S.win;
             unsigned st = 0, wi = 0;
+            const unsigned pa_base = (unsigned)__cvta_generic_to_shared(S.dfa);
             auto step = [&](unsigned b) -> unsigned {
+                if (PA) {  // st: the state's row offset in bytes (SL: no costs, P6 counts the output)
+                    const unsigned e = cx_lw(pa_base + st + s_cmap[b]);
+                    st = e & 0xffffu;
+                    if (!SL) acc += (e >> 24) & 7u;
+                    return ((e >> 16) & 0xffu) | (b & (unsigned)((int)e >> 31));
+                }
                 const unsigned e = dfa[st * nc + s_cmap[b]];
                 st = e & 0xffu;
                 const unsigned x = t2[wi * CX_T2S + (e >> 8)];
@@ -954,8 +1244,10 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 }
                 for (; i >= lo; --i) win[i] = (uint8_t)step(win[i]);
             };
-            p4_exact = long_ranges && !ct.kw;
-            if (ct.kw) {
+            // the product-automaton parse always runs byte-exact slices (no
+            // warm-up, so they pay on short lines too)
+            p4_exact = SL || (long_ranges && (PA || !ct.kw));
+            if (!PA && ct.kw) {
                 // Key-window parse (dp_fast restated for W = 16): key(j) =
                 // cost[j] * 16 - j, kept in a 32-entry ring per thread; the
                 // cheapest candidate, longer on ties (numba_impl.py:50), wins.
@@ -1004,10 +1296,59 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 }
                 if (end >= start) tot += (unsigned)(((k1 + start) >> 4) + (virt ? 0 : 1));
                 acc = (unsigned)(tot + 4ull * (unsigned)(end >= start ? end - start + 1 : 0));
+            } else if (SL) {
+                // One byte-exact slice per lane, parsed right to left in one
+                // range.  A slice whose last byte is not a '\n' is entered in
+                // the line-end state (a guess); after the pass the guess is
+                // checked against the right neighbour's exit state and, where
+                // it differs, the slice is parsed again from the true state
+                // next to the guessed one until the two meet (a '\n' resets
+                // both).  Costs are not kept: P6 counts the output.
+                if (!long_ranges && start <= end) atomicMin(&s_r0, start);
+                __syncthreads();  // P2 / P3 of every warp done (slices cross line-lanes)
+                const int R0 = s_r0, R1 = s_last_nl;
+                const int sz = R1 >= R0 ? (R1 - R0 + CX_NT) / CX_NT : 0;
+                const int s0 = R0 + tid * sz, e0 = min(R1, s0 + sz - 1);
+                const bool any = sz > 0 && s0 <= e0;
+                const bool spec = any && win[e0] != '\n';
+                // the guess: the state after a short warm-up over the next slice's
+                // first bytes from a virtual line end (the right neighbour
+                // rewrites those bytes last; a stale read only changes the guess)
+                if (spec)
+                    for (int p = min(e0 + CX_PWARM, R1); p > e0; --p) step(win[p]);
+                const unsigned guess = st;
+                if (any) parse_range(s0, e0);
+                S.lane_c[tid] = (int)st;  // exit state (read by the left neighbour)
+                __syncthreads();
+                unsigned assumed = guess;  // the entry state the slice's decisions were made from
+                for (;;) {
+                    const unsigned truth = spec ? (unsigned)S.lane_c[tid + 1] : 0u;
+                    const bool need = spec && truth != assumed;
+                    if (!__syncthreads_or(need)) break;  // (also: every lane has read)
+                    if (need) {
+                        unsigned so = assumed, sn = truth;
+                        int p = e0;
+                        for (; p >= s0; --p) {
+                            const unsigned c = win[p];
+                            const unsigned b = c == 0x20u ? (cx_bit(S.fbits, p) ? 0x01u : job.in[ws + p]) : s_exp0[c];
+                            const unsigned col = s_cmap[b];
+                            const unsigned eo = cx_lw(pa_base + so + col);
+                            const unsigned en = cx_lw(pa_base + sn + col);
+                            so = eo & 0xffffu;
+                            sn = en & 0xffffu;
+                            win[p] = (uint8_t)(((en >> 16) & 0xffu) | (b & (unsigned)((int)en >> 31)));
+                            if (sn == so) break;
+                        }
+                        assumed = truth;
+                        if (p < s0) S.lane_c[tid] = (int)sn;  // never met: the exit state changed
+                    }
+                    __syncthreads();
+                }
             } else if (!p4_exact) {
                 parse_range(start, end);
             } else {
-                __syncthreads();  // P2 / P3 of every warp done (slices cross line-lanes); R0 set in P2
+                if (SL && !long_ranges && start <= end) atomicMin(&s_r0, start);
+                __syncthreads();  // P2 / P3 of every warp done (slices cross line-lanes); R0 set
                 const int R0 = s_r0, R1 = s_last_nl;
                 const int sz = R1 >= R0 ? (R1 - R0 + CX_NT) / CX_NT : 0;
                 const int s0 = R0 + tid * sz, e0 = min(R1, s0 + sz - 1);
@@ -1016,7 +1357,13 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                 int rlo = s0, rj = 0;
                 if (sz > 0 && s0 <= e0) {
                     // entry state at e0
-                    if (win[e0] != '\n') {
+                    if (PA && win[e0] != '\n') {
+                        // no warm-up: enter in the line-end state; a wrong guess
+                        // is repaired below from the right neighbour's exit
+                        // state, only up to where the two parses converge
+                        spec = true;
+                        spec_state = 0;
+                    } else if (win[e0] != '\n') {
                         // every such entry is checked below, also when a newline was
                         // found (the check does not depend on when the right
                         // neighbour rewrites these bytes; it rewrites them last)
@@ -1069,7 +1416,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                         truth = (unsigned)S.lane_c[tid + 1];
                         need = truth != spec_state;
                     }
-                    if (job.timing == 6 && round == 0) {  // debug: entries and first-round mismatches by warm-up kind
+                    if (kPhases && job.timing == 6 && round == 0) {  // debug: entries and first-round mismatches by warm-up kind
                         const unsigned F = 0xffffffffu;
                         if (lane == 0) {
                             atomicAdd(&job.ctl->phase[0], (unsigned long long)__popc(__ballot_sync(F, spec && found)));
@@ -1084,7 +1431,30 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
                         }
                     }
                     if (!__syncthreads_or(need)) break;
-                    if (need) {
+                    if (PA && need) {
+                        // Re-run the first piece from the true entry state next to
+                        // the speculative run (both over the bytes rebuilt from the
+                        // decisions) until the two states meet; from there on every
+                        // decision and cost is the same.  A '\n' resets both, so
+                        // the repair stays inside the piece.
+                        unsigned so = spec_state, sn = truth;
+                        int d = 0, p = e0;
+                        for (; p >= rlo; --p) {
+                            const unsigned c = win[p];
+                            const unsigned b = c == 0x20u ? (cx_bit(S.fbits, p) ? 0x01u : job.in[ws + p]) : s_exp0[c];
+                            const unsigned col = s_cmap[b];
+                            const unsigned eo = cx_lw(pa_base + so + col);
+                            const unsigned en = cx_lw(pa_base + sn + col);
+                            so = eo & 0xffffu;
+                            sn = en & 0xffffu;
+                            d += (int)((en >> 24) & 7u) - (int)((eo >> 24) & 7u);
+                            win[p] = (uint8_t)(((en >> 16) & 0xffu) | (b & (unsigned)((int)en >> 31)));
+                            if (sn == so) break;
+                        }
+                        atomicAdd(&S.lane_b[rj], d);
+                        spec_state = truth;
+                        if (p < rlo && rlo == s0) S.lane_c[tid] = (int)sn;
+                    } else if (need) {
                         // rebuild the piece's bytes from its decisions, parse it again
                         for (int p = rlo; p <= e0; ++p) {
                             const unsigned d = win[p];
@@ -1144,93 +1514,186 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         __syncthreads();
         const int nbytes = (!p4_exact && end >= start) ? end - start + 1 : 0;  // exact slices: costs are in lane_b
         const long long my_out = (long long)acc - 4ll * nbytes - sub + S.lane_b[tid];
-        // ---- P5: tile output bytes and lines (one scan); publish ----
-        unsigned long long tot;
-        const unsigned long long ex = block_exscan_n<unsigned long long, CX_NT>(
-            ((unsigned long long)my_out << 24) | (unsigned long long)nlines, s_tmp64, tot);
-        const unsigned long long my_off = ex >> 24, tile_out = tot >> 24;
-        const unsigned tile_lines = (unsigned)(tot & 0xffffffu);
-        S.lane_c[tid] = (int)(ex & 0xffffffu);  // lane line bases (strict error ordinals)
-        if (tid == 0) lookback_publish(job.ts, t, tile_out, (unsigned long long)tile_lines);
-        const bool staged = tile_out <= (unsigned long long)CX_STAGE;
-        pc.mark(job, 5);  // output scan
-        // ---- P6: emit (to staging now, or to HBM after the look-back) ----
-        // Long-line tiles emit byte-exact slices: a slice starts at the first
-        // decision at or after its first byte on the path the reference's
-        // forward walk takes (numba_impl.py:57-69) -- found from a line start
-        // within CX_WARM bytes to its left, or guessed from a walk started
-        // CX_WARM bytes left and checked against the left neighbour's exit --
-        // then counts its output bytes (one scan gives the slice offsets) and
-        // emits them.
         int p6a = start, p6b = end;
-        unsigned long long p6off = my_off;
-        if (long_ranges) {
+        unsigned long long p6off, tile_out;
+        unsigned tile_lines;
+        if (SL) {
+            // ---- P6a: output bytes per byte-exact slice ----
+            // A slice's output starts at the first decision at or after its
+            // first byte on the path the reference's forward walk takes
+            // (numba_impl.py:57-69).  Guess: the slice's first byte; after the
+            // count, the left neighbour's exit (its first path position past
+            // its slice) is the truth, and a wrong guess is walked again next
+            // to the guessed path until the two paths meet.
             const uint8_t *win = S.win;
             const int R0 = s_r0, R1 = s_last_nl;
             const int sz = R1 >= R0 ? (R1 - R0 + CX_NT) / CX_NT : 0;
             const int s0 = R0 + tid * sz, e0 = min(R1, s0 + sz - 1);
+            const bool any = sz > 0 && s0 <= e0;
             auto marker_out = [&](int p) {
                 int o = 0;
                 for (int r = 0; r < n_rare; ++r)
                     if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p) o += S.rare[r].out;
                 return o;
             };
-            auto count = [&](int p, unsigned &cnt) {  // walk [p, e0]; returns the exit position
-                cnt = 0;
-                while (p <= e0) {
-                    const unsigned d = win[p];
-                    if (d == 0x20u) {
-                        cnt += cx_bit(S.fbits, p) ? (unsigned)marker_out(p) : 2u;
-                        ++p;
-                    } else {
-                        ++cnt;
-                        p += S.explen[d];
-                    }
+            // output bytes of the decision at p; L = positions it covers
+            auto out_at = [&](int p, int &L) -> unsigned {
+                const unsigned d = win[p];
+                if (d == 0x20u) {
+                    L = 1;
+                    return cx_bit(S.fbits, p) ? (unsigned)marker_out(p) : 2u;
                 }
-                return p;
+                L = S.explen[d];
+                return 1u;
             };
             int c = s0, x = s0;
-            bool spec = false;
             unsigned cnt = 0;
-            if (sz > 0 && s0 <= e0) {
-                if (s0 > R0 && win[s0 - 1] != '\n') {
-                    const int w = max(R0, s0 - CX_WARM);
-                    int p = s0 - 1;
-                    while (p > w && win[p] != '\n') --p;
-                    if (win[p] == '\n') {
-                        c = p + 1;
-                    } else {
-                        c = w;
-                        spec = w > R0;  // R0 starts the path
-                    }
-                    while (c < s0) c += win[c] == 0x20u ? 1 : S.explen[win[c]];
+            const bool spec = any && s0 > R0 && win[s0 - 1] != '\n';
+            if (spec) {
+                // guess: the path through a decision up to CX_PWARM bytes left
+                // (exact when a line starts there)
+                const int w = max(R0, s0 - CX_PWARM);
+                int p = s0 - 1;
+                while (p > w && win[p] != '\n') --p;
+                c = win[p] == '\n' ? p + 1 : w;
+                while (c < s0) c += win[c] == 0x20u ? 1 : S.explen[win[c]];
+            }
+            if (any) {
+                int p = c;
+                while (p <= e0) {
+                    int L;
+                    cnt += out_at(p, L);
+                    p += L;
                 }
-                x = count(c, cnt);
+                x = p;
             }
             __syncthreads();  // lane_a (the cuts) is free from here on
             S.lane_a[tid] = x;  // exit: first path position of the right neighbour's slice
             __syncthreads();
             for (;;) {
-                bool need = false;
-                int truth = 0;
-                if (spec) {
-                    truth = S.lane_a[tid - 1];
-                    need = truth != c;
-                }
+                const int truth = spec ? S.lane_a[tid - 1] : 0;
+                const bool need = spec && truth != c;
                 if (!__syncthreads_or(need)) break;
                 if (need) {
+                    int a = truth, b = c;
+                    while (a != b && (a <= e0 || b <= e0)) {
+                        int L;
+                        if (a < b) {
+                            cnt += out_at(a, L);
+                            a += L;
+                        } else {
+                            cnt -= out_at(b, L);
+                            b += L;
+                        }
+                    }
                     c = truth;
-                    x = count(c, cnt);
-                    S.lane_a[tid] = x;
+                    if (a != b) {  // the paths never met in the slice: new exit
+                        x = a;
+                        S.lane_a[tid] = x;
+                    }
                 }
                 __syncthreads();
             }
-            unsigned long long stot;
-            p6off = block_exscan_n<unsigned long long, CX_NT>((unsigned long long)cnt, s_tmp64, stot);
+            // ---- P5: tile output bytes and lines (one scan); publish ----
+            unsigned long long tot;
+            const unsigned long long ex = block_exscan_n<unsigned long long, CX_NT>(
+                ((unsigned long long)cnt << 24) | (unsigned long long)nlines, s_tmp64, tot);
+            p6off = ex >> 24;
+            tile_out = tot >> 24;
+            tile_lines = (unsigned)(tot & 0xffffffu);
+            S.lane_c[tid] = (int)(ex & 0xffffffu);  // line-lane line bases (strict error ordinals)
+            if (tid == 0) lookback_publish(job.ts, t, tile_out, (unsigned long long)tile_lines);
             p6a = c;
-            p6b = e0;
-            if (!(sz > 0 && s0 <= e0)) p6b = p6a - 1;  // empty slice
+            p6b = any ? e0 : c - 1;
+        } else {
+            // ---- P5: tile output bytes and lines (one scan); publish ----
+            unsigned long long tot;
+            const unsigned long long ex = block_exscan_n<unsigned long long, CX_NT>(
+                ((unsigned long long)my_out << 24) | (unsigned long long)nlines, s_tmp64, tot);
+            const unsigned long long my_off = ex >> 24;
+            tile_out = tot >> 24;
+            tile_lines = (unsigned)(tot & 0xffffffu);
+            S.lane_c[tid] = (int)(ex & 0xffffffu);  // lane line bases (strict error ordinals)
+            if (tid == 0) lookback_publish(job.ts, t, tile_out, (unsigned long long)tile_lines);
+            // ---- P6: emit (to staging now, or to HBM after the look-back) ----
+            // Long-line tiles emit byte-exact slices: a slice starts at the first
+            // decision at or after its first byte on the path the reference's
+            // forward walk takes (numba_impl.py:57-69) -- found from a line start
+            // within CX_WARM bytes to its left, or guessed from a walk started
+            // CX_WARM bytes left and checked against the left neighbour's exit --
+            // then counts its output bytes (one scan gives the slice offsets) and
+            // emits them.
+            p6off = my_off;
+            if (long_ranges) {
+                const uint8_t *win = S.win;
+                const int R0 = s_r0, R1 = s_last_nl;
+                const int sz = R1 >= R0 ? (R1 - R0 + CX_NT) / CX_NT : 0;
+                const int s0 = R0 + tid * sz, e0 = min(R1, s0 + sz - 1);
+                auto marker_out = [&](int p) {
+                    int o = 0;
+                    for (int r = 0; r < n_rare; ++r)
+                        if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p) o += S.rare[r].out;
+                    return o;
+                };
+                auto count = [&](int p, unsigned &cnt) {  // walk [p, e0]; returns the exit position
+                    cnt = 0;
+                    while (p <= e0) {
+                        const unsigned d = win[p];
+                        if (d == 0x20u) {
+                            cnt += cx_bit(S.fbits, p) ? (unsigned)marker_out(p) : 2u;
+                            ++p;
+                        } else {
+                            ++cnt;
+                            p += S.explen[d];
+                        }
+                    }
+                    return p;
+                };
+                int c = s0, x = s0;
+                bool spec = false;
+                unsigned cnt = 0;
+                if (sz > 0 && s0 <= e0) {
+                    if (s0 > R0 && win[s0 - 1] != '\n') {
+                        const int w = max(R0, s0 - CX_WARM);
+                        int p = s0 - 1;
+                        while (p > w && win[p] != '\n') --p;
+                        if (win[p] == '\n') {
+                            c = p + 1;
+                        } else {
+                            c = w;
+                            spec = w > R0;  // R0 starts the path
+                        }
+                        while (c < s0) c += win[c] == 0x20u ? 1 : S.explen[win[c]];
+                    }
+                    x = count(c, cnt);
+                }
+                __syncthreads();  // lane_a (the cuts) is free from here on
+                S.lane_a[tid] = x;  // exit: first path position of the right neighbour's slice
+                __syncthreads();
+                for (;;) {
+                    bool need = false;
+                    int truth = 0;
+                    if (spec) {
+                        truth = S.lane_a[tid - 1];
+                        need = truth != c;
+                    }
+                    if (!__syncthreads_or(need)) break;
+                    if (need) {
+                        c = truth;
+                        x = count(c, cnt);
+                        S.lane_a[tid] = x;
+                    }
+                    __syncthreads();
+                }
+                unsigned long long stot;
+                p6off = block_exscan_n<unsigned long long, CX_NT>((unsigned long long)cnt, s_tmp64, stot);
+                p6a = c;
+                p6b = e0;
+                if (!(sz > 0 && s0 <= e0)) p6b = p6a - 1;  // empty slice
+            }
         }
+        const bool staged = tile_out <= (unsigned long long)CX_STAGE;
+        pc.mark(job, 5);  // output scan
         unsigned esc = 0;
         if (staged && p6a <= p6b)
             esc = cx_emit_range<true>(job, S, ws, p6a, p6b, S.out, p6off, n_rare);

@@ -133,12 +133,22 @@ struct Job {
     int timing;  // accumulate per-phase clock64 deltas into Ctl.phase
 };
 
+// Phase clocks and the other measurement hooks are compiled in only with
+// -DZS_PHASES=1 (tools/phase_cx.py builds such a library); the production
+// kernels carry no timing branches.
+#ifndef ZS_PHASES
+#define ZS_PHASES 0
+#endif
+constexpr bool kPhases = ZS_PHASES != 0;
+
 // thread-0 phase clock: PHASE(k) adds the cycles since the last mark to phase k
 struct PhaseClock {
     long long t;
-    __device__ __forceinline__ void start() { t = clock64(); }
+    __device__ __forceinline__ void start() {
+        if (kPhases) t = clock64();
+    }
     __device__ __forceinline__ void mark(const Job &job, int k) {
-        if (job.timing != 2 && job.timing != 6 && job.timing && threadIdx.x == 0) {
+        if (kPhases && job.timing != 2 && job.timing != 6 && job.timing && threadIdx.x == 0) {
             long long now = clock64();
             atomicAdd(&job.ctl->phase[k], (unsigned long long)(now - t));
             t = now;

@@ -505,253 +505,4 @@ __global__ void __launch_bounds__(FX_NT) fx_emit(Job job, const unsigned long lo
     }
 }
 
-// ---------------------------------------------------------------------------
-// fx_fused: a single-pass decode (narrow dictionaries, longest expansion
-// <= 7), opt-in (zs_set_transducer bit 5).  A ticket takes a group of FX_K
-// consecutive 8 KB tiles: pass 1 reads each slice from HBM (double-buffered),
-// counts its output bytes from the emit table (length in bits 59-63; '\n' and
-// 0x20 found with SWAR compares) and keeps the per-thread u16 offsets in
-// shared memory; one decoupled look-back per group gives the group's output
-// offset; pass 2 re-reads the slices (L2) and emits them through the same
-// zeroed staging tile as fx_emit.  Error semantics are those of the three
-// launches: unknown codes and dangling escapes set Ctl.overflow bit 2 and the
-// host re-runs the buffer through decompress_tiles_bp.  The last group writes
-// Ctl.total_out; a group whose output would pass out_cap writes nothing and
-// sets overflow bit 0.
-//
-// Measured (tools/cmp_decode.py, C2 177 MB in): 0.50 ms against 0.37 ms for
-// fx_count -> fx_scan -> fx_emit.  The decode is issue-bound, not HBM-bound
-// (fx_emit: 69 % issue slots busy, 27 % of DRAM bandwidth), so saving the
-// 177 MB re-read buys nothing while the fused kernel runs both passes at the
-// emit kernel's occupancy (3 CTAs/SM) with 64-bit count lookups.  One
-// look-back per 8 KB tile (no groups) measured 0.60 ms: ~1.5 us of work per
-// tile against a walk past hundreds of aggregate-only tiles.
-// ---------------------------------------------------------------------------
-constexpr int FX_FUSED_SMEM = FX_ETAB + FX_STAGE;
-constexpr int FX_K = 8;  // 8 KB tiles per ticket (one look-back per group)
-
-__device__ __forceinline__ unsigned fx_swar_count(const uint4 &va, const uint4 &vb, int cnt, unsigned pat) {
-    unsigned n = 0;
-#pragma unroll
-    for (int w = 0; w < FX_B / 4; ++w) {
-        unsigned m = __vcmpeq4(fx_word(va, vb, w), pat);
-        const int valid = cnt - 4 * w;  // bytes of this word inside the slice
-        if (valid < 4) m &= valid <= 0 ? 0u : (0xffffffffu >> (8 * (4 - valid)));
-        n += __popc(m);
-    }
-    return n >> 3;
-}
-
-template <bool ALIGNED>
-__global__ void __launch_bounds__(FX_NT) fx_fused(Job job, const unsigned long long *etab) {
-    extern __shared__ __align__(16) uint8_t fsm[];  // emit table, then the staging tile
-    auto s_tab = reinterpret_cast<unsigned long long (*)[16]>(fsm);
-    uint8_t *stage = fsm + FX_ETAB;
-    __shared__ unsigned long long s_tmp64[FX_NT / 32];
-    __shared__ uint8_t s_explen[256];
-    __shared__ uint8_t s_flg[FX_K];
-    __shared__ unsigned s_tsum[FX_K];
-    __shared__ uint16_t s_off[FX_K][FX_NT];
-    __shared__ long long s_tile;
-    __shared__ unsigned long long s_base;
-    for (int k = threadIdx.x; k < 256 * 16; k += FX_NT) s_tab[k >> 4][k & 15] = etab[k >> 4];
-    for (int k = threadIdx.x; k < 256; k += FX_NT)
-        s_explen[k] = (uint8_t)(k == '\n' ? 1u : (unsigned)(etab[k] >> 59));
-    const int tid = threadIdx.x, lane = tid & 31;
-    const unsigned a_stage = sa(stage);
-    const bool ends_nl = job.n > 0 && job.in[job.n - 1] == '\n';
-    unsigned long long my_nl = 0, my_esc = 0;
-    unsigned any_bad = 0, any_ovf = 0;
-    const long long n_groups = (job.n_tiles + FX_K - 1) / FX_K;
-    for (;;) {
-        __syncthreads();  // previous group's copy-out and s_* reads are done
-        if (tid == 0) s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
-        if (tid < FX_K) s_flg[tid] = 0;
-        __syncthreads();
-        const long long g = s_tile;
-        if (g >= n_groups) break;
-        const int nk = (int)min((long long)FX_K, job.n_tiles - g * FX_K);
-        // ---- pass 1: count every tile of the group (the input's one HBM read) ----
-        unsigned long long gtot = 0;
-        // slices are double-buffered: tile j + 1's loads are in flight while j is worked
-        auto load_tile = [&](int j, uint4 &a, uint4 &b) {
-            const long long c = (g * FX_K + j) * (long long)FX_TILE + (long long)tid * FX_B;
-            fx_load<ALIGNED>(job.in, c, (int)max(0ll, min((long long)FX_B, job.n - c)), a, b);
-        };
-        uint4 na, nb4;
-        load_tile(0, na, nb4);
-        for (int j = 0; j < nk; ++j) {
-            const long long t = g * FX_K + j;
-            const long long c0 = t * (long long)FX_TILE + (long long)tid * FX_B;
-            const int cnt = (int)max(0ll, min((long long)FX_B, job.n - c0));
-            const uint4 va = na, vb = nb4;
-            if (j + 1 < nk) load_tile(j + 1, na, nb4);
-            // ---- count: output bytes of the slice ----
-            unsigned sum = 0, zero = 0;
-    #pragma unroll
-            for (int k = 0; k < FX_B; ++k) {
-                const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
-                const unsigned long long e = fx_etab(s_tab, lane, b);
-                if (k < cnt) {
-                    sum += (unsigned)(e >> 59);
-                    zero |= e == 0ull;  // 0x20 mark or unknown code
-                }
-            }
-            unsigned nl = fx_swar_count(va, vb, cnt, 0x0a0a0a0au), nesc = 0, bad = 0;
-            const unsigned marks = zero ? fx_swar_count(va, vb, cnt, 0x20202020u) : 0u;
-            bad = zero && !marks;
-            const unsigned prev = __shfl_up_sync(0xffffffffu, vb.w >> 24, 1);
-            unsigned esc0 = 0;
-            if (cnt > 0 && c0 > 0) {
-                const unsigned pb = lane ? prev : job.in[c0 - 1];
-                if (pb == 0x20) esc0 = fx_escaped(job.in, c0);
-            }
-            if (marks | esc0) {
-                unsigned esc_out;
-                fx_walk_esc(va, vb, cnt, esc0, s_explen, sum, nl, nesc, bad, esc_out);
-                if (cnt > 0 && c0 + cnt == job.n && esc_out) bad = 1;  // dangling escape at EOF
-                s_flg[j] = 1;
-            }
-            const bool eof_nl = cnt > 0 && c0 + cnt == job.n && !ends_nl;
-            if (eof_nl) {  // virtual '\n' closing the last record
-                sum += 1;
-                nl += 1;
-            }
-            any_bad |= bad;
-            my_nl += nl;
-            my_esc += nesc;
-            unsigned long long tot;
-            const unsigned my_off = (unsigned)block_exscan_n<unsigned long long, FX_NT>(sum, s_tmp64, tot);
-            s_off[j][tid] = (uint16_t)my_off;
-            if (tid == 0) s_tsum[j] = (unsigned)tot;
-            gtot += tot;
-        }
-        load_tile(0, na, nb4);  // pass 2's first slice (L2) behind the look-back
-        // ---- one look-back per group ----
-        if (tid < 32) {
-            if (tid == 0) lookback_publish(job.ts, g, gtot, 0ull);
-            __syncwarp();
-            unsigned long long po, pl;
-            lookback_resolve(job.ts, g, gtot, 0ull, po, pl);
-            if (tid == 0) {
-                s_base = po;
-                if (g == n_groups - 1) job.ctl->total_out = po + gtot;
-            }
-        }
-        __syncthreads();
-        unsigned long long tbase = s_base;
-        if (tbase + gtot > (unsigned long long)job.out_cap) {
-            any_ovf = 1;
-            continue;
-        }
-        // ---- pass 2: emit each tile (its slice re-read from L2) ----
-        for (int j = 0; j < nk; ++j, tbase += s_tsum[j - 1]) {
-            const uint4 va = na, vb = nb4;
-            if (j + 1 < nk) load_tile(j + 1, na, nb4);
-            const unsigned tsum = s_tsum[j];
-            if (tsum == 0) continue;
-            const long long t = g * FX_K + j;
-            const long long c0 = t * (long long)FX_TILE + (long long)tid * FX_B;
-            const int cnt = (int)max(0ll, min((long long)FX_B, job.n - c0));
-            const unsigned flag = s_flg[j];
-            const unsigned my_off = s_off[j][tid];
-            const bool eof_nl = cnt > 0 && c0 + cnt == job.n && !ends_nl;
-            const bool staged = tsum + 16 <= (unsigned)FX_STAGE;
-            if (staged) {
-                __syncthreads();  // previous tile's copy-out is done
-                const int words = ((int)tsum + 16 + 15) >> 4;
-                for (int k = tid; k < words; k += FX_NT)
-                    asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(a_stage + 16u * k), "r"(0u)
-                                 : "memory");
-                __syncthreads();
-            }
-            const int shift = (int)(tbase & 15);  // stage[shift + j] <-> out[tbase + j]
-            if (cnt > 0) {
-                unsigned esc = 0;
-                if (flag) {
-                    const unsigned pb = c0 > 0 ? job.in[c0 - 1] : 0u;
-                    if (pb == 0x20) esc = fx_escaped(job.in, c0);
-                }
-                if (staged) {
-                    const unsigned o = (unsigned)shift + my_off;
-                    FxAcc acc{0ull, 8u * (o & 7u), a_stage + (o & ~7u), true};
-                    if (!flag) {
-                        if (cnt == FX_B) fx_emit_clean<true>(acc, s_tab, lane, va, vb, cnt);
-                        else fx_emit_clean<false>(acc, s_tab, lane, va, vb, cnt);
-                    } else {
-                        for (int k = 0; k < cnt; ++k) {
-                            const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
-                            const unsigned long long e = fx_etab(s_tab, lane, b);
-                            if (esc) {
-                                acc.put<true>(b, 8u);
-                                esc = 0;
-                            } else if (b == 0x20) {
-                                esc = 1;
-                            } else {
-                                acc.put<true>(e & FX_BYTES, (unsigned)(e >> 56));
-                            }
-                        }
-                    }
-                    if (eof_nl) acc.put<true>('\n', 8u);
-                    acc.finish();
-                } else {
-                    uint8_t *o = job.out + tbase + my_off;
-                    for (int k = 0; k < cnt; ++k) {
-                        const unsigned b = (fx_word(va, vb, k >> 2) >> (8 * (k & 3))) & 0xffu;
-                        const unsigned long long e = fx_etab(s_tab, lane, b);
-                        if (esc) {
-                            *o++ = (uint8_t)b;
-                            esc = 0;
-                        } else if (b == 0x20) {
-                            esc = 1;
-                        } else {
-                            const unsigned L = (unsigned)(e >> 56) >> 3;
-                            for (unsigned j = 0; j < L; ++j) o[j] = (uint8_t)(e >> (8 * j));
-                            o += L;
-                        }
-                    }
-                    if (eof_nl) *o++ = '\n';
-                }
-            }
-            if (staged) {
-                __syncthreads();
-                const unsigned long long lo = tbase, hi = tbase + tsum;
-                const unsigned long long g0 = (lo + 15) & ~15ull, g1 = hi & ~15ull;
-                const uint4 *s4 = reinterpret_cast<const uint4 *>(stage);
-                if (g0 < g1) {
-                    const int n16 = (int)((g1 - g0) >> 4);
-                    const int s0 = (int)((g0 - (lo & ~15ull)) >> 4);
-                    uint4 *d4 = reinterpret_cast<uint4 *>(job.out + g0);
-                    for (int k = tid; k < n16; k += FX_NT) __stcs(d4 + k, s4[s0 + k]);
-                    if (tid < 32) {
-                        for (unsigned long long g = lo + tid; g < g0; g += 32) job.out[g] = stage[shift + (g - lo)];
-                    } else if (tid < 64) {
-                        for (unsigned long long g = g1 + (tid - 32); g < hi; g += 32)
-                            job.out[g] = stage[shift + (g - lo)];
-                    }
-                } else if (tid < 32) {
-                    for (unsigned long long g = lo + tid; g < hi; g += 32) job.out[g] = stage[shift + (g - lo)];
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        my_nl += __shfl_xor_sync(0xffffffffu, my_nl, o);
-        my_esc += __shfl_xor_sync(0xffffffffu, my_esc, o);
-    }
-    any_bad = __any_sync(0xffffffffu, any_bad != 0);
-    any_ovf = __any_sync(0xffffffffu, any_ovf != 0);
-    if (lane == 0) {
-        if (my_nl) {
-            atomicAdd(&job.ctl->lines, my_nl);
-            atomicAdd(&job.ctl->in_lines, my_nl);
-        }
-        if (my_esc) atomicAdd(&job.ctl->escapes, my_esc);
-        if (any_bad) atomicOr(&job.ctl->overflow, 4ull);
-        if (any_ovf) atomicOr(&job.ctl->overflow, 1ull);
-    }
-}
-
-
 }  // namespace zs

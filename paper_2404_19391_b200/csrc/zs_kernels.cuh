@@ -67,34 +67,6 @@ __device__ __forceinline__ void store_out(uint8_t *dst, const uint8_t *src, int 
     for (int k = head + (nvec << 4) + threadIdx.x; k < len; k += NT) dst[k] = src[k];
 }
 
-struct DSmem {
-    uint8_t *expflat;
-    uint16_t *expoff;
-    uint8_t *explen;
-    uint8_t *win;
-    uint8_t *out;
-    uint16_t *queue;
-    unsigned *chunk;
-    uint8_t *stat;  // one status byte per line ordinal of the tile
-};
-
-__host__ __device__ inline int decompress_smem_bytes(int n_flat) {
-    return align16(n_flat + 16) + align16(257 * 2) + 256 + align16(WIN + 16) + align16(DOUTCAP) +
-           QCAP * 2 + NT * 4 + TILE;
-}
-
-__device__ inline DSmem carve_dsmem(uint8_t *p, int n_flat) {
-    DSmem S;
-    S.expflat = p; p += align16(n_flat + 16);
-    S.expoff = reinterpret_cast<uint16_t *>(p); p += align16(257 * 2);
-    S.explen = p; p += 256;
-    S.win = p; p += align16(WIN + 16);
-    S.out = p; p += align16(DOUTCAP);
-    S.queue = reinterpret_cast<uint16_t *>(p); p += QCAP * 2;
-    S.chunk = reinterpret_cast<unsigned *>(p); p += NT * 4;
-    S.stat = p;
-    return S;
-}
 
 // Stage window bytes [ws, ws+len) of `in` into smem `win` (positions before
 // the buffer start read as '\n' so offset 0 is a line start).
@@ -480,7 +452,7 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                 const long long tr0 = clock64();
                 rn_k = renumber_fast(s, rn ? n_l : 0, s_lut, d, &rn_len, &rn_off, rn_ids);
                 __syncwarp();
-                if (job.timing && (tid & 31) == 0) atomicAdd(&s_trn, (unsigned long long)(clock64() - tr0));
+                if (kPhases && job.timing && (tid & 31) == 0) atomicAdd(&s_trn, (unsigned long long)(clock64() - tr0));
                 if (do_dp) {
                     if (job.preprocess) {
                         int eoff = rn_off;
@@ -537,7 +509,7 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                     }
                 }
                 __syncwarp();
-                if (job.timing && (tid & 31) == 0) atomicAdd(&s_tdp, (unsigned long long)(clock64() - td0));
+                if (kPhases && job.timing && (tid & 31) == 0) atomicAdd(&s_tdp, (unsigned long long)(clock64() - td0));
                 if (global_line) {
                     // line in HBM: find its end, process in the arena
                     const long long gs = ws + p;
@@ -571,7 +543,7 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
                 }
                 __syncwarp();
             }
-            if (job.timing && (tid & 31) == 0) {
+            if (kPhases && job.timing && (tid & 31) == 0) {
                 const unsigned long long dt = (unsigned long long)(clock64() - wt0);
                 atomicMax(&s_wmax, dt);
                 atomicMin(&s_wmin, dt);
@@ -581,7 +553,7 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
             pc.mark(job, 6);  // thread 0's own parse work
             __syncthreads();
             pc.mark(job, 2);  // waiting for the slowest warp
-            if (job.timing && tid == 0) {
+            if (kPhases && job.timing && tid == 0) {
                 atomicAdd(&job.ctl->phase[3], s_wmax);  // slot 3: max warp parse time
                 atomicAdd(&job.ctl->phase[4], s_wmin);  // slot 4: min warp parse time
                 atomicAdd(&job.ctl->phase[0], s_wsum / NWARP);  // slot 0: avg warp parse
@@ -695,432 +667,6 @@ __global__ void __launch_bounds__(NT, 1) compress_tiles(Job job, Tables tb) {
     }
 }
 
-// ============================================================================
-// In-place compress kernel (transducer dictionaries): decisions overwrite the
-// line bytes in the staged window, so a CTA stages ~67 KB tiles (~1500 lines,
-// ~46 warp groups) instead of ~34 KB; escape literals stay in place with
-// their bit set in `ebits`; ring-token starts are marked in `rbits`.
-// In-band line encoding after the parse (position p = line start):
-//   ebits[p] && win[p] == '\n'  -> line dropped (lenient CR / strict error)
-//   ebits[p] && win[p] == 0x0d  -> line parsed in the HBM arena (offset/16 in
-//                                   win[p+1..p+4])
-//   otherwise decisions from p: code (advance by its length) or, with the
-//   ebits bit, an escaped literal; '\n' ends the line.
-// ============================================================================
-constexpr int CCHUNK = 116;                 // 29 words: odd stride across lanes
-constexpr int CTILE = CCHUNK * NT;          // 59392 bytes of line starts per tile
-constexpr int CWIN = HEAD + CTILE + EXTRA;  // 63504 (multiple of 16; window offsets fit u16)
-static_assert(CWIN + 16 < 65536, "line queue stores u16 window offsets");
-constexpr int CWORDS = CWIN / 32 + 2;       // bitmap words
-constexpr int COUTCAP = 30720;
-constexpr int CQCAP = 2048;
-
-struct IpSmem {
-    uint16_t *dfa;
-    uint32_t *t2;
-    uint8_t *codes;
-    uint8_t *explen;
-    uint8_t *win;
-    unsigned *rbits;
-    unsigned *ebits;
-    uint8_t *out;
-    uint16_t *queue, *qlen, *qsort;
-    unsigned *qoff;
-    unsigned *chunk;
-};
-
-__host__ __device__ inline int ip_smem_bytes(int n_states, int n_windows) {
-    return align16(n_states * NCOL * 2) + n_windows * T2_MASKS * 4 + align16(n_states * FAST_W) +
-           256 + align16(CWIN + 16) + 2 * CWORDS * 4 + align16(COUTCAP) + 3 * CQCAP * 2 +
-           CQCAP * 4 + NT * 4;
-}
-
-__device__ inline IpSmem carve_ip(uint8_t *p, int ns, int nw) {
-    IpSmem S;
-    S.dfa = reinterpret_cast<uint16_t *>(p); p += align16(ns * NCOL * 2);
-    S.t2 = reinterpret_cast<uint32_t *>(p); p += nw * T2_MASKS * 4;
-    S.codes = p; p += align16(ns * FAST_W);
-    S.explen = p; p += 256;
-    S.win = p; p += align16(CWIN + 16);
-    S.rbits = reinterpret_cast<unsigned *>(p); p += CWORDS * 4;
-    S.ebits = reinterpret_cast<unsigned *>(p); p += CWORDS * 4;
-    S.out = p; p += align16(COUTCAP);
-    S.queue = reinterpret_cast<uint16_t *>(p); p += CQCAP * 2;
-    S.qlen = reinterpret_cast<uint16_t *>(p); p += CQCAP * 2;
-    S.qsort = reinterpret_cast<uint16_t *>(p); p += CQCAP * 2;
-    S.qoff = reinterpret_cast<unsigned *>(p); p += CQCAP * 4;
-    S.chunk = reinterpret_cast<unsigned *>(p);
-    return S;
-}
-
-__device__ __forceinline__ bool bm_get(const unsigned *bm, int pos) {
-    return (bm[pos >> 5] >> (pos & 31)) & 1u;
-}
-
-// Emit one line from the in-place encoding at o[w...] (w advanced); returns
-// the escapes emitted.
-__device__ __forceinline__ unsigned ip_emit_line(const Job &job, const IpSmem &S, long long ws, int p,
-                                                 uint8_t *o, unsigned long long &w) {
-    unsigned esc = 0;
-    const uint8_t *win = S.win;
-    if (bm_get(S.ebits, p) && win[p] == '\n') return 0;  // dropped
-    if (bm_get(S.ebits, p) && win[p] == 0x0d) {           // parsed in the arena
-        const unsigned aoff = win[p + 1] | (win[p + 2] << 8) | (win[p + 3] << 16) |
-                              ((unsigned)win[p + 4] << 24);
-        const uint8_t *blk = job.arena + ((long long)aoff << 4);
-        const ArenaHdr *h = reinterpret_cast<const ArenaHdr *>(blk);
-        const uint8_t *bytes = h->bytes_off < 0 ? job.in + ws + p : job.arena + h->bytes_off;
-        const uint8_t *dec = job.arena + h->dec_off;
-        for (long long i = 0; i < h->n_pre;) {
-            const uint8_t c = dec[i];
-            if (c == D_ESC) {
-                o[w++] = 0x20;
-                o[w++] = bytes[i];
-                ++esc;
-                ++i;
-            } else {
-                o[w++] = c;
-                i += S.explen[c];
-            }
-        }
-        o[w++] = '\n';
-        return esc;
-    }
-    for (int i = p;;) {
-        const uint8_t c = win[i];
-        if (c == '\n') break;
-        if (bm_get(S.ebits, i)) {
-            o[w++] = 0x20;
-            o[w++] = c;
-            ++esc;
-            ++i;
-        } else {
-            o[w++] = c;
-            i += S.explen[c];
-        }
-    }
-    o[w++] = '\n';
-    return esc;
-}
-
-__global__ void __launch_bounds__(NT, 1) compress_tiles_ip(Job job, Tables tb) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ unsigned long long s_tmp64[NWARP];
-    __shared__ int s_tmp32[NWARP];
-    __shared__ unsigned s_hist[256];
-    __shared__ __align__(16) uint8_t s_lut[8 * 256];  // tokenizer transducer
-    __shared__ long long s_tile;
-    __shared__ int s_err_ord, s_global, s_grp;
-    __shared__ unsigned long long s_pre_out, s_pre_lines;
-    __shared__ unsigned s_kept, s_esc, s_skip, s_flag;
-
-    const IpSmem S = carve_ip(smem, tb.n_states, tb.n_windows);
-    {
-        const uint4 *src = reinterpret_cast<const uint4 *>(tb.dfa2);
-        uint4 *dst = reinterpret_cast<uint4 *>(S.dfa);
-        for (int k = threadIdx.x; k < align16(tb.n_states * NCOL * 2) / 16; k += NT) dst[k] = src[k];
-        for (int k = threadIdx.x; k < tb.n_windows * T2_MASKS; k += NT) S.t2[k] = tb.t2[k];
-        for (int k = threadIdx.x; k < tb.n_states * FAST_W; k += NT) S.codes[k] = tb.codes[k];
-        for (int k = threadIdx.x; k < 256; k += NT) S.explen[k] = tb.exp_len[k];
-        for (int k = threadIdx.x; k < 8 * 256; k += NT) s_lut[k] = tk_entry(k >> 8, k & 255);
-    }
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-
-    for (;;) {
-        __syncthreads();
-        if (tid == 0) {
-            s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
-            s_err_ord = 0x7fffffff;
-            s_global = 0;
-            s_kept = s_esc = s_skip = s_flag = 0;
-        }
-        __syncthreads();
-        const long long t = s_tile;
-        if (t >= job.n_tiles) break;
-        const long long T0 = t * (long long)CTILE;
-        const int tile_len = (int)min((long long)CTILE, job.n - T0);
-        const long long ws = T0 - HEAD;
-        const long long we = min(job.n, T0 + CTILE + EXTRA);
-        const int win_len = (int)(we - ws);
-        const bool hits_eof = we == job.n;
-        load_window(job.in, job.n, ws, align16(win_len), S.win);
-        for (int k = tid; k < CWORDS; k += NT) S.rbits[k] = S.ebits[k] = 0u;
-        S.chunk[tid] = 0;
-        __syncthreads();
-        if (tid == 0 && hits_eof) S.win[win_len] = '\n';  // end of a final partial line
-
-        const int my_cnt = scan_starts<CCHUNK>(S.win, tile_len, 0, nullptr, 0, 0);
-        int tile_lines;
-        const int my_off = block_exscan<int>(my_cnt, s_tmp32, tile_lines);
-
-        for (int q0 = 0; q0 < tile_lines; q0 += CQCAP) {
-            const int nq = min(CQCAP, tile_lines - q0);
-            if (my_cnt) scan_starts<CCHUNK>(S.win, tile_len, my_off, S.queue, q0, q0 + nq);
-            for (int k = tid; k < 256; k += NT) s_hist[k] = 0;
-            __syncthreads();
-            for (int q = tid; q < nq; q += NT) {
-                const int p = S.queue[q];
-                const int end = (q + 1 < nq) ? S.queue[q + 1] - 1 : find_end(S.win, p, win_len, hits_eof);
-                const int len = end < 0 ? 0xffff : end - p;
-                S.qlen[q] = (uint16_t)len;
-                atomicAdd(&s_hist[255 - min(len, 255)], 1u);
-            }
-            __syncthreads();
-            {
-                unsigned h = tid < 256 ? s_hist[tid] : 0u;
-                unsigned tot;
-                const unsigned ex = block_exscan<unsigned>(h, reinterpret_cast<unsigned *>(s_tmp32), tot);
-                if (tid < 256) s_hist[tid] = ex;
-            }
-            __syncthreads();
-            for (int q = tid; q < nq; q += NT) {
-                const unsigned r = atomicAdd(&s_hist[255 - min((int)S.qlen[q], 255)], 1u);
-                S.qsort[r] = (uint16_t)q;
-            }
-            if (tid == 0) s_grp = 0;
-            __syncthreads();
-            // warps pull groups of 32 lines, longest first (LPT)
-            for (;;) {
-                int g = 0;
-                if (lane == 0) g = atomicAdd(&s_grp, 1);
-                g = __shfl_sync(0xffffffffu, g, 0);
-                if (g * 32 >= nq) break;
-                const int r = g * 32 + lane;
-                const bool valid = r < nq;
-                int q = 0, p = HEAD, qlen = 0;
-                if (valid) {
-                    q = S.qsort[r];
-                    p = S.queue[q];
-                    qlen = S.qlen[q];
-                }
-                const int ord = q0 + q;
-                int kind = E_NONE;
-                long long size = 0;
-                bool global_line = valid && qlen == 0xffff;
-                bool do_dp = valid && !global_line;
-                uint8_t *s = S.win + p;
-                int n_l = qlen;
-                // ---- CR policy + ring renumbering (all lanes call) ----
-                int rn_len = 0, rn_off = -1;
-                unsigned long long rn_ids[2] = {0, 0};
-                const bool rn = do_dp && job.preprocess;
-                int k = renumber_bm(s, rn ? n_l : 0, s_lut, S.rbits, p, &rn_len, &rn_off, rn_ids);
-                if (do_dp) {
-                    if (job.preprocess) {
-                        if (k == E_NONE) {
-                            if (rn_len < n_l) s[rn_len] = '\n';  // end of the shrunk line
-                            n_l = rn_len;
-                        } else if (k == RN_FALLBACK) {
-                            // pristine bytes, then the general routine (marks in the arena)
-                            const uint8_t *g8 = job.in + ws + p;
-                            for (int j = 0; j < n_l; ++j) s[j] = g8[j];
-                            const unsigned long long need = ((unsigned long long)n_l + 31) & ~15ull;
-                            const unsigned long long a = atomicAdd(&job.ctl->arena_used, need);
-                            if (a + need <= (unsigned long long)job.arena_cap) {
-                                int nl2 = n_l;
-                                k = preprocess_line(s, n_l, job.arena + a, s, &nl2, &rn_off, rn_ids);
-                                if (k == E_NONE) {
-                                    if (nl2 < n_l) s[nl2] = '\n';
-                                    n_l = nl2;
-                                }
-                            } else {
-                                atomicOr(&job.ctl->overflow, 2ull);
-                                k = E_NONE;
-                            }
-                        }
-                        if (k == -1) {
-                            global_line = true;
-                            do_dp = false;
-                        } else if (k != E_NONE) {
-                            if (k == E_CR) {
-                                kind = E_CR;
-                            } else if (job.lenient) {
-                                // keep the raw line (pipeline.py:108-115)
-                                const uint8_t *g8 = job.in + ws + p;
-                                for (int j = 0; j < n_l; ++j) s[j] = g8[j];
-                                atomicAdd(&s_flag, 1u);
-                            } else {
-                                kind = k;
-                            }
-                        }
-                    } else {
-                        for (int j = 0; j < n_l; ++j)
-                            if (s[j] == '\r') { kind = E_CR; break; }
-                    }
-                    if (do_dp && kind != E_NONE) {
-                        do_dp = false;
-                        s[0] = '\n';
-                        bm_set(S.ebits, p);
-                        if (job.lenient) atomicAdd(&s_skip, 1u);
-                        else atomicMin(&s_err_ord, ord);
-                    }
-                }
-                __syncwarp();
-                // ---- min-cost parse, decisions in place (converged) ----
-                if (do_dp) size = dp_t2_inplace(s, n_l, S.dfa, S.t2, S.codes, S.ebits, p) + 1;
-                __syncwarp();
-                if (global_line) {
-                    const long long gs = ws + p;
-                    long long ge = gs;
-                    while (ge < job.n && job.in[ge] != '\n') ++ge;
-                    unsigned aoff = 0;
-                    int eoff = -1;
-                    unsigned long long ids[2] = {0, 0};
-                    long long cost = compress_line_global(job, tb, gs, ge - gs, &aoff, &kind, &eoff, ids);
-                    s_global = 1;
-                    if (kind == -2) {
-                        kind = E_NONE;  // arena exhausted; host re-runs
-                        s[0] = '\n';
-                        bm_set(S.ebits, p);
-                    } else if (kind == E_CR || (kind > 0 && !job.lenient)) {
-                        s[0] = '\n';
-                        bm_set(S.ebits, p);
-                        if (job.lenient) atomicAdd(&s_skip, 1u);
-                        else atomicMin(&s_err_ord, ord);
-                    } else {
-                        if (kind == -3) atomicAdd(&s_flag, 1u);
-                        kind = E_NONE;
-                        s[0] = 0x0d;
-                        s[1] = aoff & 0xff; s[2] = (aoff >> 8) & 0xff;
-                        s[3] = (aoff >> 16) & 0xff; s[4] = (aoff >> 24) & 0xff;
-                        bm_set(S.ebits, p);
-                        size = cost + 1;
-                    }
-                }
-                if (valid) S.qoff[q] = (unsigned)size;
-                if (size) {
-                    atomicAdd(&S.chunk[(p - HEAD) / CCHUNK], (unsigned)size);
-                    atomicAdd(&s_kept, 1u);
-                }
-                __syncwarp();
-            }
-            __syncthreads();
-        }
-
-        // ---- tile output size; publish; emit to smem; look-back ----
-        unsigned long long tile_out;
-        const unsigned long long my_out = S.chunk[tid];
-        const unsigned long long my_out_off = block_exscan<unsigned long long>(my_out, s_tmp64, tile_out);
-        const bool one_round = tile_lines <= CQCAP;
-        if (one_round) {
-            const int per = (tile_lines + NT - 1) / NT;
-            const int l0 = min(tid * per, tile_lines), l1 = min(l0 + per, tile_lines);
-            unsigned sum = 0;
-            for (int l = l0; l < l1; ++l) sum += S.qoff[l];
-            unsigned tot;
-            unsigned run = block_exscan<unsigned>(sum, reinterpret_cast<unsigned *>(s_tmp32), tot);
-            for (int l = l0; l < l1; ++l) {
-                const unsigned v = S.qoff[l];
-                S.qoff[l] = run;
-                run += v;
-            }
-            if (tid == 0) s_grp = 0;
-            __syncthreads();
-        }
-        if (tid == 0) lookback_publish(job.ts, t, tile_out, (unsigned long long)tile_lines);
-        const bool staged = !s_global && one_round && tile_out <= (unsigned long long)COUTCAP;
-        if (staged) {
-            unsigned esc = 0;
-            for (;;) {
-                int g = 0;
-                if (lane == 0) g = atomicAdd(&s_grp, 1);
-                g = __shfl_sync(0xffffffffu, g, 0);
-                if (g * 32 >= tile_lines) break;
-                const int r = g * 32 + lane;
-                __syncwarp();
-                if (r < tile_lines) {
-                    const int q = S.qsort[r];
-                    unsigned long long w = S.qoff[q];
-                    esc += ip_emit_line(job, S, ws, S.queue[q], S.out, w);
-                }
-                __syncwarp();
-            }
-            if (esc) atomicAdd(&s_esc, esc);
-        }
-        if (tid < 32) {
-            unsigned long long po, pl;
-            lookback_resolve(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
-            if (tid == 0) {
-                s_pre_out = po;
-                s_pre_lines = pl;
-            }
-        }
-        __syncthreads();
-        const unsigned long long pre_out = s_pre_out;
-        const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
-        if (tid == 0) {
-            atomicAdd(&job.ctl->total_out, tile_out);
-            atomicAdd(&job.ctl->lines, (unsigned long long)s_kept);
-            atomicAdd(&job.ctl->in_lines, (unsigned long long)tile_lines);
-            if (s_skip) atomicAdd(&job.ctl->skipped, (unsigned long long)s_skip);
-            if (s_flag) atomicAdd(&job.ctl->flagged, (unsigned long long)s_flag);
-            if (!fits) atomicOr(&job.ctl->overflow, 1ull);
-        }
-        // ---- strict error: re-derive details of the first bad line ----
-        if (tid == 0 && s_err_ord != 0x7fffffff) {
-            int ord = s_err_ord, seen = 0;
-            long long gp = -1;
-            for (long long x = T0; x < T0 + tile_len && gp < 0; ++x)
-                if (x == 0 || job.in[x - 1] == '\n') {
-                    if (seen == ord) gp = x;
-                    ++seen;
-                }
-            long long gs = gp, ge = gs;
-            while (ge < job.n && job.in[ge] != '\n') ++ge;
-            TileErr e = {E_CR, 0, -1, {0, 0}};
-            bool cr = false;
-            for (long long k = gs; k < ge; ++k) cr |= job.in[k] == '\r';
-            if (!cr && job.preprocess) {
-                int nl2, eoff = -1;
-                unsigned long long ids[2] = {0, 0};
-                const long long n_l = ge - gs;
-                const unsigned long long need = (4 * (unsigned long long)n_l + 19) & ~15ull;
-                unsigned long long a = atomicAdd(&job.ctl->arena_used, need);
-                uint8_t *tmp = a + need <= (unsigned long long)job.arena_cap ? job.arena + a : nullptr;
-                if (!tmp) atomicOr(&job.ctl->overflow, 2ull);
-                int k = tmp ? preprocess_line(job.in + gs, (int)n_l, tmp, tmp + n_l + 1, &nl2, &eoff, ids)
-                            : E_NONE;
-                e.kind = k;
-                e.offset = eoff;
-                e.ids[0] = ids[0];
-                e.ids[1] = ids[1];
-            }
-            job.terr[t] = e;
-            __threadfence();
-            atomicMin(&job.ctl->err_key, ((s_pre_lines + (unsigned long long)ord) << 24) |
-                                             (unsigned long long)(t & 0xffffff));
-        }
-        if (!fits) continue;
-
-        if (staged) {
-            store_out(job.out + pre_out, S.out, (int)tile_out);
-        } else {
-            // direct emit: per line in queue order (single round) or, for
-            // tiles with more than CQCAP lines, by chunk with the line starts
-            // re-derived from the pristine input in HBM (rare paths)
-            unsigned esc = 0;
-            if (one_round) {
-                for (int q = tid; q < tile_lines; q += NT) {
-                    unsigned long long w = pre_out + S.qoff[q];
-                    esc += ip_emit_line(job, S, ws, S.queue[q], job.out, w);
-                }
-            } else {
-                unsigned long long w = pre_out + my_out_off;
-                const int c0 = tid * CCHUNK, c1 = min(c0 + CCHUNK, tile_len);
-                for (int x = c0; x < c1; ++x) {
-                    const long long gx = T0 + x;
-                    if (gx == 0 || job.in[gx - 1] == '\n')
-                        esc += ip_emit_line(job, S, ws, HEAD + x, job.out, w);
-                }
-            }
-            if (esc) atomicAdd(&s_esc, esc);
-        }
-        __syncthreads();
-        if (tid == 0 && s_esc) atomicAdd(&job.ctl->escapes, (unsigned long long)s_esc);
-    }
-}
-
 // ----------------------------------------------------------------------------
 // decompress: same skeleton; size/validate pass then table expansion.
 // ----------------------------------------------------------------------------
@@ -1164,210 +710,6 @@ __device__ __forceinline__ long long decode_fill(const uint8_t *r, long long n, 
         }
     }
     return w;
-}
-
-// Decompress emit: one flat walk over the positions of the thread's chunk
-// (records that start in it are finished past its end).  ST_LONG marks a
-// good record that runs past the staged window; it is expanded from HBM
-// (tiles holding one are never staged).
-constexpr uint8_t ST_LONG = 0xfe;
-
-template <bool STAGED>
-__device__ __forceinline__ void dec_emit_chunk(const Job &job, const DSmem &S, long long ws,
-                                               int tile_len, int ord, unsigned long long w,
-                                               uint8_t *o) {
-    const int c0 = threadIdx.x * CHUNK;
-    const int c1 = min(c0 + CHUNK, tile_len);
-    bool in = false, esc_next = false;
-    for (int x = c0; __any_sync(0xffffffffu, x < c1 || in); ++x) {
-        const int p = HEAD + x;
-        if (x < c1 && S.win[p - 1] == '\n') {
-            const uint8_t st = S.stat[ord++];
-            in = st == E_NONE;
-            esc_next = false;
-            if (st == ST_LONG) {
-                const long long gs = ws + p;
-                long long ge = gs;
-                while (ge < job.n && job.in[ge] != '\n') ++ge;
-                w += decode_fill(job.in + gs, ge - gs, S.explen, S.expoff, S.expflat, job.out + w);
-                job.out[w++] = '\n';
-            }
-        }
-        if (!in) continue;
-        const unsigned b = S.win[p];
-        if (esc_next) {
-            o[w++] = (uint8_t)b;
-            esc_next = false;
-        } else if (b == '\n') {
-            o[w++] = '\n';
-            in = false;
-        } else if (b == 0x20) {
-            esc_next = true;
-        } else {
-            const unsigned L = S.explen[b];
-            const uint8_t *e = S.expflat + S.expoff[b];
-            for (unsigned k = 0; k < L; ++k) o[w + k] = e[k];
-            w += L;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(NT, 1) decompress_tiles(Job job, Tables tb) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ unsigned long long s_tmp64[NWARP];
-    __shared__ int s_tmp32[NWARP];
-    __shared__ long long s_tile;
-    __shared__ int s_qhead, s_err_ord, s_global;
-    __shared__ unsigned long long s_pre_out, s_pre_lines;
-    __shared__ unsigned s_kept, s_esc, s_skip;
-
-    const DSmem S = carve_dsmem(smem, tb.n_flat);
-    uint8_t *expflat = S.expflat;
-    uint16_t *expoff = S.expoff;
-    uint8_t *explen = S.explen;
-    uint8_t *win = S.win;
-    uint8_t *obuf = S.out;
-    uint16_t *queue = S.queue;
-    unsigned *chunk = S.chunk;
-    uint8_t *stat = S.stat;
-    for (int k = threadIdx.x; k < tb.n_flat; k += NT) expflat[k] = tb.exp_flat[k];
-    for (int k = threadIdx.x; k < 257; k += NT) expoff[k] = tb.exp_off[k];
-    for (int k = threadIdx.x; k < 256; k += NT) explen[k] = tb.exp_len[k];
-    const int tid = threadIdx.x;
-
-    for (;;) {
-        __syncthreads();
-        if (tid == 0) {
-            s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
-            s_err_ord = 0x7fffffff;
-            s_global = 0;
-            s_kept = s_esc = s_skip = 0;
-        }
-        __syncthreads();
-        const long long t = s_tile;
-        if (t >= job.n_tiles) break;
-        const long long T0 = t * (long long)TILE;
-        const int tile_len = (int)min((long long)TILE, job.n - T0);
-        const long long ws = T0 - HEAD;
-        const long long we = min(job.n, T0 + TILE + EXTRA);
-        const int win_len = (int)(we - ws);
-        const bool hits_eof = we == job.n;
-        load_window(job.in, job.n, ws, align16(win_len), win);
-        chunk[tid] = 0;
-        __syncthreads();
-        if (tid == 0 && hits_eof) win[win_len] = '\n';  // virtual newline after a final partial record
-        __syncthreads();
-
-        const int my_cnt = scan_starts(win, tile_len, 0, nullptr, 0, 0);
-        int tile_lines;
-        const int my_off = block_exscan<int>(my_cnt, s_tmp32, tile_lines);
-
-        for (int q0 = 0; q0 < tile_lines; q0 += QCAP) {
-            const int q1 = min(q0 + QCAP, tile_lines);
-            if (my_cnt) scan_starts(win, tile_len, my_off, queue, q0, q1);
-            if (tid == 0) s_qhead = 0;
-            __syncthreads();
-            // warps take 32 consecutive records at a time; lanes reconverge
-            // (__syncwarp) before the per-record size/validate walk
-            for (;;) {
-                int g = 0;
-                if ((tid & 31) == 0) g = atomicAdd(&s_qhead, 1);
-                g = __shfl_sync(0xffffffffu, g, 0);
-                if (g * 32 >= q1 - q0) break;
-                const int q = g * 32 + (tid & 31);
-                if (q >= q1 - q0) {
-                    __syncwarp();
-                    continue;
-                }
-                const int ord = q0 + q;
-                const int p = queue[q];
-                int end = (q + 1 < q1 - q0) ? queue[q + 1] - 1 : find_end(win, p, win_len, hits_eof);
-                const uint8_t *r;
-                long long n_r;
-                if (end >= 0) {
-                    r = win + p;
-                    n_r = end - p;
-                } else {
-                    long long gs = ws + p, ge = gs;
-                    while (ge < job.n && job.in[ge] != '\n') ++ge;
-                    r = job.in + gs;
-                    n_r = ge - gs;
-                    s_global = 1;
-                }
-                __syncwarp();
-                long long m = 0, ep = -1;
-                int code = 0;
-                unsigned esc = 0;
-                int st = decode_size(r, n_r, explen, &m, &ep, &code, &esc);
-                stat[ord] = (uint8_t)(st == E_NONE && end < 0 ? ST_LONG : st);
-                if (esc) atomicAdd(&s_esc, esc);
-                if (st == E_NONE) {
-                    atomicAdd(&chunk[(p - HEAD) / CHUNK], (unsigned)(m + 1));
-                    atomicAdd(&s_kept, 1u);
-                } else if (job.lenient) {
-                    atomicAdd(&s_skip, 1u);
-                } else {
-                    atomicMin(&s_err_ord, ord);
-                }
-            }
-            __syncthreads();
-        }
-
-        unsigned long long tile_out;
-        const unsigned long long my_out_off = block_exscan<unsigned long long>(
-            (unsigned long long)chunk[tid], s_tmp64, tile_out);
-        if (tid < 32) {
-            unsigned long long po, pl;
-            lookback(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
-            if (tid == 0) {
-                s_pre_out = po;
-                s_pre_lines = pl;
-            }
-        }
-        if (tid == 0) {
-            atomicAdd(&job.ctl->total_out, tile_out);
-            atomicAdd(&job.ctl->lines, (unsigned long long)s_kept);
-            atomicAdd(&job.ctl->in_lines, (unsigned long long)tile_lines);
-            if (s_skip) atomicAdd(&job.ctl->skipped, (unsigned long long)s_skip);
-            if (s_esc) atomicAdd(&job.ctl->escapes, (unsigned long long)s_esc);
-            if (s_pre_out + tile_out > (unsigned long long)job.out_cap)
-                atomicOr(&job.ctl->overflow, 1ull);
-        }
-        __syncthreads();
-        const unsigned long long pre_out = s_pre_out;
-        const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
-        const bool staged = fits && !s_global && tile_out <= (unsigned long long)DOUTCAP;
-
-        if (tid == 0 && s_err_ord != 0x7fffffff) {
-            int ord = s_err_ord, seen = 0, p = -1;
-            for (int x = 0; x < tile_len && p < 0; ++x)
-                if (win[HEAD + x - 1] == '\n') {
-                    if (seen == ord) p = HEAD + x;
-                    ++seen;
-                }
-            long long gs = ws + p, ge = gs;
-            while (ge < job.n && job.in[ge] != '\n') ++ge;
-            long long m = 0, ep = -1;
-            int code = 0;
-            unsigned esc = 0;
-            TileErr e;
-            e.kind = decode_size(job.in + gs, ge - gs, explen, &m, &ep, &code, &esc);
-            e.code = code;
-            e.offset = ep;
-            e.ids[0] = e.ids[1] = 0;
-            job.terr[t] = e;
-            __threadfence();
-            atomicMin(&job.ctl->err_key, ((s_pre_lines + (unsigned long long)ord) << 24) |
-                                             (unsigned long long)(t & 0xffffff));
-        }
-        if (!fits) continue;
-
-        __syncthreads();
-        if (staged) dec_emit_chunk<true>(job, S, ws, tile_len, my_off, my_out_off, obuf);
-        else dec_emit_chunk<false>(job, S, ws, tile_len, my_off, pre_out + my_out_off, job.out);
-        __syncthreads();
-        if (staged) store_out(job.out + pre_out, obuf, (int)tile_out);
-    }
 }
 
 // ============================================================================
@@ -1675,320 +1017,6 @@ __global__ void __launch_bounds__(NT, 1) decompress_tiles_bp(Job job, Tables tb)
         else if (resident) bp_walk<2, true>(W, S, B, S.bad, dummy, dummy, job.out, pre_out + my_base);
         else bp_walk<2, false>(W, S, B, S.bad, dummy, dummy, job.out, pre_out + my_base);
         pc.mark(job, 6);  // store
-    }
-}
-
-// ============================================================================
-// Warp-cooperative decompress.  A warp owns a contiguous range of the tile's
-// compressed bytes and processes it in 32-byte blocks, one byte per lane
-// (conflict-free smem reads).  Byte roles come from ballot masks:
-//   SP = 0x20 bytes, NL = '\n' bytes.  Inside a maximal 0x20 run the bytes at
-//   even offsets from the run start are escape markers, odd offsets are
-//   literals; the byte after a run that ends on a marker is a literal
-//   (numba_impl.py:93-101 read sequentially).  Per block, with A = even bit
-//   positions, Rodd = runs whose start offset is odd (a run continuing from
-//   the previous block takes the carried parity):
-//     D_odd = SP & ~(SP + Rodd)        (carry fills each odd-start run)
-//     M     = SP & (A ^ D_odd)         markers
-//     LIT   = (SP & ~M) | (((M & runend) << 1) & ~SP) | carry-in literal
-//   A marker right before '\n' is a dangling escape (record error).
-// Record ordinals are popcounts of NL; output offsets are warp scans.
-// ============================================================================
-struct WcRoles {
-    unsigned nl, mark, lit, code, e_out;
-};
-
-__device__ __forceinline__ WcRoles wc_roles(unsigned b, bool valid, unsigned e_in) {
-    const unsigned lane = threadIdx.x & 31;
-    const unsigned NL = __ballot_sync(0xffffffffu, valid && b == '\n');
-    const unsigned SP = __ballot_sync(0xffffffffu, valid && b == 0x20);
-    const unsigned VA = __ballot_sync(0xffffffffu, valid);
-    constexpr unsigned A = 0x55555555u;
-    const unsigned rstart = SP & ~(SP << 1);
-    const unsigned rodd = (rstart & ~A & ~1u) | (SP & e_in & 1u);
-    const unsigned d_odd = SP & ~(SP + rodd);
-    const unsigned M = SP & (A ^ d_odd);
-    const unsigned runend = SP & ~(SP >> 1);
-    const unsigned litc = (SP & ~M) | (((M & runend) << 1) & ~SP) | ((e_in & ~SP) & 1u);
-    WcRoles r;
-    r.nl = NL;
-    r.mark = M;
-    r.lit = litc & ~NL & VA;
-    r.code = VA & ~SP & ~NL & ~r.lit;
-    // error: a marker directly before '\n' (litc candidate on a NL byte)
-    r.e_out = (M >> 31) & 1u;
-    (void)lane;
-    return r;
-}
-
-__global__ void __launch_bounds__(NT, 1) decompress_tiles_wc(Job job, Tables tb) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ unsigned long long s_tmp64[NWARP];
-    __shared__ int s_tmp32[NWARP];
-    __shared__ long long s_tile;
-    __shared__ int s_last_end, s_first_start, s_nbad;
-    __shared__ unsigned long long s_pre_out, s_pre_lines;
-    __shared__ unsigned s_esc;
-
-    const BpSmem S = carve_bp(smem, tb.n_flat);
-    for (int k = threadIdx.x; k < tb.n_flat; k += NT) S.expflat[k] = tb.exp_flat[k];
-    for (int k = threadIdx.x; k < 257; k += NT) S.expoff[k] = tb.exp_off[k];
-    for (int k = threadIdx.x; k < 256; k += NT) S.explen[k] = tb.exp_len[k];
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, wid = tid >> 5;
-    const unsigned a_win = sa(S.win), a_len = sa(S.explen), a_bad = sa(S.bad);
-    const unsigned a_off = sa(S.expoff), a_flat = sa(S.expflat), a_out = sa(S.out);
-    const bool short_exp = tb.max_exp <= 8;
-
-    for (;;) {
-        __syncthreads();
-        if (tid == 0) {
-            s_tile = (long long)atomicAdd(&job.ctl->ticket, 1ull);
-            s_nbad = 0;
-            s_esc = 0;
-            s_last_end = -1;
-            s_first_start = 0x7fffffff;
-        }
-        __syncthreads();
-        const long long t = s_tile;
-        if (t >= job.n_tiles) break;
-        const long long T0 = t * (long long)TILE;
-        const int tile_len = (int)min((long long)TILE, job.n - T0);
-        const long long ws = T0 - HEAD;
-        const long long we = min(job.n, T0 + TILE + EXTRA);
-        const int win_len = (int)(we - ws);
-        const bool hits_eof = we == job.n;
-        load_window(job.in, job.n, ws, align16(win_len), S.win);
-        for (int k = tid; k < BP_BADW; k += NT) S.bad[k] = 0u;
-        __syncthreads();
-        if (tid == 0 && hits_eof) S.win[win_len] = '\n';
-        // owned range: [first owned start, end of the last owned record]
-        const int my_cnt = scan_starts(S.win, tile_len, 0, nullptr, 0, 0);
-        int tile_lines;
-        (void)block_exscan<int>(my_cnt, s_tmp32, tile_lines);
-        {
-            const int c0 = tid * CHUNK, c1 = min(c0 + CHUNK, tile_len);
-            for (int x = c0; x < c1; ++x)
-                if (S.win[HEAD + x - 1] == '\n') {
-                    atomicMin(&s_first_start, HEAD + x);
-                    break;
-                }
-            if (tid == 0 && tile_lines > 0) {
-                int e;
-                if (S.win[HEAD + tile_len - 1] == '\n') {
-                    e = HEAD + tile_len - 1;
-                } else {
-                    e = HEAD + tile_len;
-                    while (e < win_len && S.win[e] != '\n') ++e;
-                    if (e >= win_len && !hits_eof) {
-                        long long g = ws + e;
-                        while (g < job.n && job.in[g] != '\n') ++g;
-                        e = (int)(g - ws);
-                    }
-                }
-                s_last_end = e;
-            }
-        }
-        __syncthreads();
-        const int first = s_first_start, last_end = s_last_end;
-        const int lim = hits_eof ? win_len + 1 : win_len;  // resident bytes [0, lim)
-        const BpBytes B{S.win, job.in, ws, lim};
-        const bool resident = last_end < lim;
-        // warp ranges over [first, last_end], whole 32-byte blocks
-        int r0 = 0, r1 = 0;
-        if (tile_lines > 0) {
-            const int nblk = (last_end + 1 - first + 31) / 32;
-            r0 = first + 32 * (int)((long long)nblk * wid / NWARP);
-            r1 = first + 32 * (int)((long long)nblk * (wid + 1) / NWARP);
-            r1 = min(r1, last_end + 1);
-            r0 = min(r0, r1);
-        }
-        // pass 0: newlines per warp range -> ordinal base; escape carry-in
-        int nl_cnt = 0;
-        for (int q0 = r0; q0 < r1; q0 += 32) {
-            const int q = q0 + lane;
-            const bool valid = q < r1;
-            const unsigned b = valid ? (resident ? ldsb(a_win + q) : B(q)) : 0u;
-            nl_cnt += __popc(__ballot_sync(0xffffffffu, valid && b == '\n'));
-        }
-        int n_before;
-        {
-            int tot;
-            const int v = lane == 0 ? nl_cnt : 0;
-            n_before = block_exscan<int>(v, s_tmp32, tot);
-            n_before = __shfl_sync(0xffffffffu, n_before, 0);
-        }
-        unsigned e_in0 = 0;
-        if (lane == 0 && r0 < r1 && r0 > first) {
-            int rr = 0;
-            while (r0 - 1 - rr >= first && B(r0 - 1 - rr) == 0x20) ++rr;
-            // the run before r0 (within the record) ends in a marker iff its length is odd
-            e_in0 = rr & 1;
-        }
-        e_in0 = __shfl_sync(0xffffffffu, e_in0, 0);
-        // pass 1: validate
-        {
-            int ord = n_before;
-            unsigned e_in = e_in0;
-            for (int q0 = r0; q0 < r1; q0 += 32) {
-                const int q = q0 + lane;
-                const bool valid = q < r1;
-                const unsigned b = valid ? (resident ? ldsb(a_win + q) : B(q)) : 0u;
-                const WcRoles R = wc_roles(b, valid, e_in);
-                const unsigned me = 1u << lane;
-                const int my_ord = ord + __popc(R.nl & (me - 1));
-                const unsigned L = ldsb(a_len + b);
-                // dangling escape: the byte before this '\n' is a marker
-                const unsigned prev_mark = lane ? (R.mark >> (lane - 1)) & 1u : e_in;
-                const bool err = ((R.code & me) && L == 0) || ((R.nl & me) && prev_mark);
-                if (err) atomicOr(&S.bad[my_ord >> 5], 1u << (my_ord & 31));
-                ord += __popc(R.nl);
-                e_in = R.e_out;
-            }
-        }
-        __syncthreads();
-        // pass 2: output bytes of good records
-        unsigned long long wsum = 0;
-        unsigned wesc = 0;
-        {
-            int ord = n_before;
-            unsigned e_in = e_in0;
-            for (int q0 = r0; q0 < r1; q0 += 32) {
-                const int q = q0 + lane;
-                const bool valid = q < r1;
-                const unsigned b = valid ? (resident ? ldsb(a_win + q) : B(q)) : 0u;
-                const WcRoles R = wc_roles(b, valid, e_in);
-                const unsigned me = 1u << lane;
-                const int my_ord = ord + __popc(R.nl & (me - 1));
-                const bool good = valid && !((ldsw(a_bad + 4 * (my_ord >> 5)) >> (my_ord & 31)) & 1u);
-                const unsigned L = ldsb(a_len + b);
-                const unsigned add = (R.code & me) ? L : ((R.lit | R.nl) & me ? 1u : 0u);
-                unsigned v = good ? add : 0u;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                wsum += v;
-                wesc += __popc(__ballot_sync(0xffffffffu, good && (R.mark & me)));
-                ord += __popc(R.nl);
-                e_in = R.e_out;
-            }
-        }
-        unsigned long long tile_out;
-        const unsigned long long wbase = block_exscan<unsigned long long>(lane == 0 ? wsum : 0ull, s_tmp64, tile_out);
-        const unsigned long long my_wbase = __shfl_sync(0xffffffffu, wbase, 0);
-        if (lane == 0 && wesc) atomicAdd(&s_esc, wesc);
-        if (tid == 0) lookback_publish(job.ts, t, tile_out, (unsigned long long)tile_lines);
-        const bool staged = resident && tile_out <= (unsigned long long)DOUTCAP;
-        // pass 3: expand (smem when staged, else HBM after the look-back)
-        auto expand = [&](uint8_t *o_glob, unsigned long long base) {
-            int ord = n_before;
-            unsigned e_in = e_in0;
-            unsigned long long run = base;
-            for (int q0 = r0; q0 < r1; q0 += 32) {
-                const int q = q0 + lane;
-                const bool valid = q < r1;
-                const unsigned b = valid ? (resident ? ldsb(a_win + q) : B(q)) : 0u;
-                const WcRoles R = wc_roles(b, valid, e_in);
-                const unsigned me = 1u << lane;
-                const int my_ord = ord + __popc(R.nl & (me - 1));
-                const bool good = valid && !((ldsw(a_bad + 4 * (my_ord >> 5)) >> (my_ord & 31)) & 1u);
-                const bool is_code = R.code & me;
-                const unsigned L = ldsb(a_len + b);
-                const unsigned add = good ? (is_code ? L : ((R.lit | R.nl) & me ? 1u : 0u)) : 0u;
-                unsigned inc = add;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc += y;
-                }
-                const unsigned long long w = run + inc - add;
-                if (add) {
-                    if (o_glob == nullptr) {
-                        const unsigned ow = a_out + (unsigned)w;
-                        if (!is_code) {
-                            stsb(ow, b);
-                        } else {
-                            const unsigned e = a_flat + ldsh(a_off + 2 * b);
-                            if (short_exp) {
-#pragma unroll
-                                for (unsigned k = 0; k < 8; ++k)
-                                    if (k < L) stsb(ow + k, ldsb(e + k));
-                            } else {
-                                for (unsigned k = 0; k < L; ++k) stsb(ow + k, ldsb(e + k));
-                            }
-                        }
-                    } else {
-                        if (!is_code) {
-                            o_glob[w] = (uint8_t)b;
-                        } else {
-                            const uint8_t *e = S.expflat + S.expoff[b];
-                            for (unsigned k = 0; k < L; ++k) o_glob[w + k] = e[k];
-                        }
-                    }
-                }
-                run += __shfl_sync(0xffffffffu, inc, 31);
-                ord += __popc(R.nl);
-                e_in = R.e_out;
-            }
-        };
-        if (staged) expand(nullptr, my_wbase);
-        if (tid < 32) {
-            unsigned long long po, pl;
-            lookback_resolve(job.ts, t, tile_out, (unsigned long long)tile_lines, po, pl);
-            if (tid == 0) {
-                s_pre_out = po;
-                s_pre_lines = pl;
-            }
-        }
-        {
-            unsigned nb = 0;
-            for (int k = tid; k < (tile_lines + 31) / 32; k += NT) nb += __popc(S.bad[k]);
-            if (nb) atomicAdd(&s_nbad, (int)nb);
-        }
-        __syncthreads();
-        const unsigned long long pre_out = s_pre_out;
-        const bool fits = pre_out + tile_out <= (unsigned long long)job.out_cap;
-        if (tid == 0) {
-            const int nbad = s_nbad;
-            atomicAdd(&job.ctl->total_out, tile_out);
-            atomicAdd(&job.ctl->lines, (unsigned long long)(tile_lines - nbad));
-            atomicAdd(&job.ctl->in_lines, (unsigned long long)tile_lines);
-            if (!fits) atomicOr(&job.ctl->overflow, 1ull);
-            unsigned long long esc_bad = 0;
-            if (nbad) {
-                if (job.lenient) atomicAdd(&job.ctl->skipped, (unsigned long long)nbad);
-                int ord = -1, first_bad = -1;
-                for (long long x = T0; x < T0 + tile_len; ++x) {
-                    if (!(x == 0 || job.in[x - 1] == '\n')) continue;
-                    ++ord;
-                    if (!((S.bad[ord >> 5] >> (ord & 31)) & 1u)) continue;
-                    long long ge = x;
-                    while (ge < job.n && job.in[ge] != '\n') ++ge;
-                    long long m = 0, ep = -1;
-                    int code = 0;
-                    unsigned e2 = 0;
-                    const int kind = decode_size(job.in + x, ge - x, S.explen, &m, &ep, &code, &e2);
-                    esc_bad += e2;
-                    if (first_bad < 0) {
-                        first_bad = ord;
-                        if (!job.lenient) {
-                            TileErr e;
-                            e.kind = kind;
-                            e.code = code;
-                            e.offset = ep;
-                            e.ids[0] = e.ids[1] = 0;
-                            job.terr[t] = e;
-                            __threadfence();
-                            atomicMin(&job.ctl->err_key, ((s_pre_lines + (unsigned long long)ord) << 24) |
-                                                             (unsigned long long)(t & 0xffffff));
-                        }
-                    }
-                }
-            }
-            if (s_esc + esc_bad) atomicAdd(&job.ctl->escapes, (unsigned long long)s_esc + esc_bad);
-        }
-        if (!fits) continue;
-        if (staged) store_out(job.out + pre_out, S.out, (int)tile_out);
-        else expand(job.out, pre_out + my_wbase);
     }
 }
 

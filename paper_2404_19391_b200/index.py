@@ -35,6 +35,7 @@ class RecordIndex:
         nrec = ctypes.c_int64(0)
         cap = n // 2 + 2
         with self._ctx.lock:
+            self._ctx.follow_torch_stream()
             for _ in range(2):
                 self._off = torch.empty(cap, dtype=torch.int64, device=self._dev)
                 rc = self._ctx.lib.zs_index_build(self._ctx.h, self._comp.data_ptr() if n else None, n,
@@ -44,6 +45,8 @@ class RecordIndex:
                     continue
                 self._ctx.check(rc, "zs_index_build")
                 break
+            else:
+                raise _lib.ZsCudaError(f"zs_index_build: offsets still too small ({nrec.value} records)")
         self._n = int(nrec.value)
 
     def __len__(self):
@@ -68,6 +71,7 @@ class RecordIndex:
         cap = max(64, 96 * k)  # ~2x the mean record (45 B); a second call sizes it exactly
         with self._ctx.lock:
             self._ctx.set_dictionary(self._d)
+            self._ctx.follow_torch_stream()
             for _ in range(2):
                 d_out = torch.empty(cap, dtype=torch.uint8, device=self._dev)
                 rc = self._ctx.lib.zs_decode_records(self._ctx.h, self._comp.data_ptr(), self._off.data_ptr(),
@@ -79,6 +83,8 @@ class RecordIndex:
                     continue
                 self._ctx.check(rc, "zs_decode_records")
                 break
+            else:
+                raise _lib.ZsCudaError(f"zs_decode_records: output still too small ({total.value} bytes)")
         st = d_st.cpu().numpy()
         bad = np.flatnonzero(st)
         if bad.size:  # the first bad record in request order, as decompress_line would raise

@@ -48,16 +48,6 @@ def compute_ratio(stats: CorpusStats) -> float:
     return stats.ratio
 
 
-def _read_all(src) -> bytes:
-    parts = []
-    while True:
-        chunk = src.read(64 << 20)
-        if not chunk:
-            break
-        parts.append(chunk)
-    return b"".join(parts)
-
-
 def run_buffer(buf, d, direction="compress", *, preprocess=False, lenient=False, device=None, out=None):
     """One newline-framed buffer through the GPU.  Returns (output bytes,
     zs_result).  `buf` may be bytes or a uint8 numpy array (pinned memory
@@ -90,6 +80,9 @@ def run_buffer(buf, d, direction="compress", *, preprocess=False, lenient=False,
                 continue
             ctx.check(rc, "zs_compress_host" if direction == "compress" else "zs_decompress_host")
             break
+        else:
+            raise _lib.ZsCudaError(f"{direction}: output buffer still too small after 3 attempts "
+                                   f"({res.out_bytes} bytes needed)")
     return out[:res.out_bytes], res
 
 
@@ -163,9 +156,19 @@ def run_stream(src, dst, d, direction="compress", *, preprocess=False, lenient=F
     Strict mode raises LineError (1-based) for the first bad line, after
     writing every complete `batch_lines` batch before it like the reference
     (pipeline.py:154-161); lenient mode drops undecodable / carriage-return
-    lines (``skipped``) and keeps unpreprocessable ones raw (``flagged``)."""
+    lines (``skipped``) and keeps unpreprocessable ones raw (``flagged``).
+
+    The page-locked staging belongs to the device's context, so concurrent
+    run_stream calls on one device run one after the other (the context
+    lock is held for the whole stream); `dst.write` receives bytes."""
     if direction not in ("compress", "decompress"):
         raise ValueError(f"bad direction {direction!r}")
+    # the staging buffers are per context: one stream at a time per device
+    with _lib.context(device).lock:
+        return _run_stream(src, dst, d, direction, preprocess, lenient, batch_lines, device, segment_bytes)
+
+
+def _run_stream(src, dst, d, direction, preprocess, lenient, batch_lines, device, segment_bytes):
     t0 = time.perf_counter()
     bl = max(1, batch_lines)
     st = CorpusStats()
@@ -181,7 +184,7 @@ def run_stream(src, dst, d, direction="compress", *, preprocess=False, lenient=F
             st.output_bytes += 1
         for body in parts:
             if len(body):
-                dst.write(body)
+                dst.write(bytes(body))  # a copy: the staging is reused (the reference writes bytes)
                 st.output_bytes += len(body)
         held_nl = False
 
@@ -278,21 +281,3 @@ def run_stream(src, dst, d, direction="compress", *, preprocess=False, lenient=F
         st.output_bytes += 1
     st.elapsed = time.perf_counter() - t0
     return st
-
-
-def _write_partial(dst, data, d, direction, preprocess, lenient, err_line, batch_lines, device):
-    """Reference behaviour on a strict error: every complete batch before the
-    failing line's batch has already been written (no trailing newline)."""
-    keep = ((err_line - 1) // max(1, batch_lines)) * max(1, batch_lines)
-    if keep <= 0:
-        return
-    arr = np.frombuffer(data, np.uint8)
-    nl = np.flatnonzero(arr == 0x0A)
-    end = int(nl[keep - 1]) + 1
-    out, _ = run_buffer(arr[:end], d, direction, preprocess=preprocess, lenient=lenient,
-                        device=device)
-    blob = out.tobytes()
-    if blob.endswith(b"\n"):
-        blob = blob[:-1]
-    if blob:
-        dst.write(blob)

@@ -140,3 +140,54 @@ def run_sharded(buf, codec_fn, rank: int, world: int, group=None):
     trailing = arr.size == 0 or arr[-1] == 0x0A
     view = combine(results, rank, trailing)
     return bytes(out[:view.out_bytes]), view
+
+
+def run_library(buf, d, direction="compress", *, preprocess=False, lenient=False, devices=None):
+    """One library over several GPUs of this process (the multi-GPU form of
+    ``run_buffer``; the reference spreads batches over a thread pool,
+    pipeline.py:77-94).  The buffer is cut into one newline-aligned shard
+    per device (shard_bounds), the shards run concurrently (one host thread
+    per device; the C-ABI calls release the GIL), and the shard protocol
+    combines the per-shard scalars (combine).  Returns (output uint8 array,
+    GlobalView, per-shard zs_result list); the output equals the
+    single-device stream byte for byte.  Strict-mode errors are reported,
+    not raised: GlobalView.err_line is the global 1-based first bad line
+    (the caller raises, as run_stream does)."""
+    import threading
+
+    from . import _lib
+    from .pipeline import run_buffer
+    arr = buf if isinstance(buf, np.ndarray) else np.frombuffer(buf, np.uint8)
+    if devices is None:
+        devices = list(range(max(1, _lib.device_count())))
+    world = len(devices)
+    cuts = shard_bounds(arr, world)
+    outs, res, errs = [None] * world, [None] * world, []
+
+    def work(r):
+        try:
+            sh = np.ascontiguousarray(arr[cuts[r]:cuts[r + 1]])
+            o, z = run_buffer(sh, d, direction, preprocess=preprocess, lenient=lenient, device=devices[r])
+            outs[r] = o.copy()
+            res[r] = z
+        except BaseException as e:  # re-raised in the caller's thread
+            errs.append(e)
+
+    threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errs:
+        raise errs[0]
+    locals_ = []
+    for r in range(world):
+        sh = arr[cuts[r]:cuts[r + 1]]
+        body, loc = normalise(sh, outs[r].tobytes(), res[r].lines, res[r].err_line)
+        outs[r] = body
+        locals_.append(loc)
+    trailing = arr.size == 0 or arr[-1] == 0x0A
+    views = [combine(locals_, r, trailing) for r in range(world)]
+    blob = b"".join(o[:v.out_bytes] for o, v in zip(outs, views))
+    return np.frombuffer(blob, np.uint8), views[0], res
+

@@ -370,14 +370,14 @@ def test_device_and_host_api_agree():
     assert (r.lines, r.out_bytes) == (res.lines, res.out_bytes)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 3, 7, 11, 35])
+@pytest.mark.parametrize("mode", [0, 1, 3, 19, 67, 83, 131])
 def test_kernel_variants_bit_exact(corpus_hashes, mode):
-    """Every compress kernel variant (0: key-window DP with a decision array,
-    1: + cost-window transducer, 3: + in-place decisions -- the lane-chunk
-    kernel, the default; 11: the queue-based in-place kernel; bit 2 selects
-    the warp-cooperative decompress instead of the streaming one; bit 5 the
-    single-pass fused streaming decode instead of the three launches) gives the
-    reference bytes, both directions."""
+    """Every compress kernel variant gives the reference bytes, both
+    directions (include/zs_debug.h): 0 the generic key-window DP with a
+    decision array, 1 + the cost-window transducer, 3 compress_cx with the
+    product-automaton parse (the default), 19 without the byte-exact slices
+    of long-line tiles, 67 compress_cx with the DFA + transducer parse,
+    83 both, 131 compress_cx with every phase on byte-exact slices."""
     ctx = _lib.context()
     try:
         ctx.lib.zs_set_transducer(ctx.h, mode)
@@ -420,10 +420,37 @@ def test_sharded_gpu_codec(world):
     assert blob == want and v.total_lines == st["lines"]
 
 
-@pytest.mark.parametrize("mode", [3, 35])
+def test_run_library_two_contexts(corpus_hashes):
+    """The single-process multi-GPU API (shard.run_library) with two real
+    contexts on one device (one shard each, run concurrently) reproduces the
+    reference's own C1 output and round trip (golden hashes)."""
+    from paper_2404_19391_b200 import shard
+    e = corpus_hashes["c1_100k"]
+    buf = synth.generate(e["kind"], e["lines"], e["seed"])
+    d = z.deserialize(golden_dict_bytes(e["dict"]))
+    ctxs = [_lib.Context(0), _lib.Context(0)]
+    try:
+        for world in (2, 3):
+            devs = [ctxs[r % 2] for r in range(world)]
+            comp, v, res = shard.run_library(buf, d, "compress", preprocess=True, lenient=True, devices=devs)
+            assert hashlib.sha256(comp.tobytes()).hexdigest() == e["pre_on"]["comp_sha256"]
+            assert v.total_lines == e["lines"] and v.total_out == comp.size and v.err_line == 0
+            back, _, _ = shard.run_library(comp, d, "decompress", devices=devs)
+            assert hashlib.sha256(back.tobytes()).hexdigest() == e["pre_on"]["roundtrip_sha256"]
+        # a strict error in the second shard: global 1-based line number
+        lines = buf.tobytes().split(b"\n")
+        lines[70000] = b"C1CC[N"
+        bad = np.frombuffer(b"\n".join(lines), np.uint8)
+        _, v, _ = shard.run_library(bad, d, "compress", preprocess=True, lenient=False, devices=ctxs)
+        assert v.err_line == 70001
+    finally:
+        for c in ctxs:
+            c.close()
+
+
+@pytest.mark.parametrize("mode", [3])
 def test_streaming_decode_edges(mode):
-    """Byte-local streaming decode (mode 3: fx_count / fx_scan / fx_emit,
-    mode 35: fx_fused): 0x20 runs across thread chunks and tiles, a final
+    """Byte-local streaming decode (fx_count / fx_scan / fx_emit): 0x20 runs across thread chunks and tiles, a final
     record without '\\n', unaligned device input, and bad records that hand
     the buffer to the record-aware kernel."""
     ctx = _lib.context()
@@ -468,7 +495,7 @@ def _streaming_decode_edges(mode):
                                                   dout.data_ptr(), dout.numel(), 0, r)
                 ctx.check(rc, "zs_decompress_device")
                 kname = ctx.lib.zs_last_kernel(ctx.h).decode()
-            assert kname == ("fx_fused" if mode == 35 else "fx_count+fx_scan+fx_emit"), kname
+            assert kname == "fx_count+fx_scan+fx_emit", kname
             assert dout[:r.out_bytes].cpu().numpy().tobytes() == want, off
     # a dangling escape at EOF, an escaped '\n', unknown codes: record-aware path
     comp = _oracle_check(b"\n".join(lines) + b"\n", d, False, True)
@@ -477,9 +504,9 @@ def _streaming_decode_edges(mode):
         _oracle_check(bad, d, False, False, "decompress")
 
 
-@pytest.mark.parametrize("mode", [3, 35])
+@pytest.mark.parametrize("mode", [3])
 def test_decode_capacity(mode):
-    """Streaming decode (3: three launches, 35: fx_fused) with an output
+    """Streaming decode (fx_count / fx_scan / fx_emit) with an output
     buffer too small: ZS_E_CAPACITY with the bytes needed, and nothing
     written past the caller's capacity."""
     ctx = _lib.context()
@@ -504,7 +531,7 @@ def _decode_capacity(mode):
             ctx.set_dictionary(d)
             rc = ctx.lib.zs_decompress_device(ctx.h, din.data_ptr(), comp.size, dout.data_ptr(), cap, 0, r)
             kname = ctx.lib.zs_last_kernel(ctx.h).decode()
-        assert kname == ("fx_fused" if mode == 35 else "fx_count+fx_scan+fx_emit"), kname
+        assert kname == "fx_count+fx_scan+fx_emit", kname
         assert rc == -5 and r.out_bytes == buf.size
         assert bool((dout[cap:] == 0xAB).all())
     r = _lib.Result()

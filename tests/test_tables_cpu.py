@@ -27,7 +27,11 @@ def test_header_symbols_exported():
         declared = set(re.findall(r"^(?:int|int64_t|float|void|const char)\s*\*?\s*(zs_\w+)\(",
                                   fh.read(), re.M))
     assert declared == set(_lib.EXPORTS)
-    for name in declared:
+    with open(f"{ROOT}/include/zs_debug.h") as fh:
+        debug = set(re.findall(r"^(?:int|int64_t|float|void|const char)\s*\*?\s*(zs_\w+)\(",
+                               fh.read(), re.M))
+    assert debug == set(_lib.DEBUG_EXPORTS)
+    for name in declared | debug:
         assert hasattr(lib, name), name
 
 
