@@ -334,35 +334,103 @@ __device__ __forceinline__ unsigned cx_emit_range(const Job &job, const CxSmem &
     return esc;
 }
 
-// Stage window bytes [ws, ws+len) (positions before the buffer read as '\n'
-// so offset 0 is a line start; positions past the end as '\n').
-__device__ __forceinline__ void cx_load_window(const uint8_t *in, long long n, long long ws, int len, uint8_t *win) {
-    const bool aligned = ((reinterpret_cast<uintptr_t>(in) & 15) == 0) && ws >= 0 && ws + len <= n && (len & 15) == 0;
-    if (aligned) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(in + ws);
-        uint4 *dst = reinterpret_cast<uint4 *>(win);
-        for (int k = threadIdx.x; k < len / 16; k += CX_NT) dst[k] = __ldcs(src + k);
-    } else {
-        for (int k = threadIdx.x; k < len; k += CX_NT) {
-            const long long g = ws + k;
-            win[k] = g < 0 ? (uint8_t)'\n' : (g < n ? __ldcs(in + g) : (uint8_t)'\n');
-        }
+// ---- asynchronous bulk copies (TMA engine) into shared memory ----
+__device__ __forceinline__ unsigned cx_saddr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cx_mbar_init(uint64_t *mbar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cx_saddr(mbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// one thread: arm the mbarrier with `bytes` and copy global [src, src+bytes)
+// to shared dst in pieces (src, dst 16-byte aligned, bytes a multiple of 16)
+__device__ __forceinline__ void cx_bulk_load(void *dst, const void *src, unsigned bytes, uint64_t *mbar) {
+    const unsigned mb = cx_saddr(mbar), d = cx_saddr(dst);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic accesses first
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    constexpr unsigned PIECE = 8192;
+    for (unsigned o = 0; o < bytes; o += PIECE) {
+        const unsigned nb = bytes - o < PIECE ? bytes - o : PIECE;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(d + o), "l"(reinterpret_cast<const char *>(src) + o), "r"(nb), "r"(mb)
+                     : "memory");
     }
 }
+__device__ __forceinline__ void cx_mbar_wait(uint64_t *mbar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n"
+        "}\n" ::"r"(cx_saddr(mbar)), "r"(parity) : "memory");
+}
 
-// Staged tile output -> HBM: bytes until dst is 16-byte aligned, then 16-byte stores.
+// Stage window bytes [ws, ws+len) (positions before the buffer read as '\n'
+// so offset 0 is a line start; positions past the end as '\n').  Interior
+// windows of a 16-byte aligned buffer arrive by one bulk copy (TMA) that
+// thread 0 issued (returns true: wait on the mbarrier); windows of an
+// unaligned buffer are read as aligned 16-byte chunks and shifted into place
+// in registers; the first and last windows of a buffer bytewise.
+__device__ __forceinline__ bool cx_load_window(const uint8_t *in, long long n, long long ws, int len, uint8_t *win,
+                                               uint64_t *mbar) {
+    const unsigned mis = (unsigned)((reinterpret_cast<uintptr_t>(in) + (uintptr_t)ws) & 15);
+    const bool interior = ws >= 0 && ws + len <= n && (len & 15) == 0;
+    if (interior && mis == 0) {
+        if (threadIdx.x == 0) cx_bulk_load(win, in + ws, (unsigned)len, mbar);
+        return true;
+    }
+    if (interior && ws + len + 16 <= n) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(in + ws - mis);
+        uint4 *dst = reinterpret_cast<uint4 *>(win);
+        const unsigned sel = 0x3210u + 0x1111u * (mis & 3);  // byte shift within a word pair
+        const unsigned q = mis >> 2;
+        for (int k = threadIdx.x; k < len / 16; k += CX_NT) {
+            const uint4 a = __ldcs(src + k), b = __ldcs(src + k + 1);
+            const unsigned w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            uint4 v;
+            // q is the same for every thread: the branches do not diverge
+            if (q == 0) v = make_uint4(__byte_perm(w[0], w[1], sel), __byte_perm(w[1], w[2], sel),
+                                       __byte_perm(w[2], w[3], sel), __byte_perm(w[3], w[4], sel));
+            else if (q == 1) v = make_uint4(__byte_perm(w[1], w[2], sel), __byte_perm(w[2], w[3], sel),
+                                            __byte_perm(w[3], w[4], sel), __byte_perm(w[4], w[5], sel));
+            else if (q == 2) v = make_uint4(__byte_perm(w[2], w[3], sel), __byte_perm(w[3], w[4], sel),
+                                            __byte_perm(w[4], w[5], sel), __byte_perm(w[5], w[6], sel));
+            else v = make_uint4(__byte_perm(w[3], w[4], sel), __byte_perm(w[4], w[5], sel),
+                                __byte_perm(w[5], w[6], sel), __byte_perm(w[6], w[7], sel));
+            dst[k] = v;
+        }
+        return false;
+    }
+    for (int k = threadIdx.x; k < len; k += CX_NT) {
+        const long long g = ws + k;
+        win[k] = g < 0 ? (uint8_t)'\n' : (g < n ? __ldcs(in + g) : (uint8_t)'\n');
+    }
+    return false;
+}
+
+// Staged tile output -> HBM: bytes until dst is 16-byte aligned, then 16-byte
+// stores, each built from the two aligned 16-byte staging chunks it spans.
 __device__ __forceinline__ void cx_store_out(uint8_t *dst, const uint8_t *src, int len) {
     const int head = min(len, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
     if ((int)threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
     const int nvec = (len - head) >> 4;
     uint4 *d4 = reinterpret_cast<uint4 *>(dst + head);
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);  // src is 16-byte aligned
+    const unsigned sel = 0x3210u + 0x1111u * (head & 3), q = (unsigned)head >> 2;
     for (int k = threadIdx.x; k < nvec; k += CX_NT) {
-        const uint8_t *q = src + head + 16 * k;
+        if (head == 0) {
+            d4[k] = s4[k];
+            continue;
+        }
+        const uint4 a = s4[k], b = s4[k + 1];  // bytes head + 16k .. head + 16k + 15
+        const unsigned w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
         uint4 v;
-        v.x = q[0] | (q[1] << 8) | (q[2] << 16) | ((unsigned)q[3] << 24);
-        v.y = q[4] | (q[5] << 8) | (q[6] << 16) | ((unsigned)q[7] << 24);
-        v.z = q[8] | (q[9] << 8) | (q[10] << 16) | ((unsigned)q[11] << 24);
-        v.w = q[12] | (q[13] << 8) | (q[14] << 16) | ((unsigned)q[15] << 24);
+        if (q == 0) v = make_uint4(__byte_perm(w[0], w[1], sel), __byte_perm(w[1], w[2], sel),
+                                   __byte_perm(w[2], w[3], sel), __byte_perm(w[3], w[4], sel));
+        else if (q == 1) v = make_uint4(__byte_perm(w[1], w[2], sel), __byte_perm(w[2], w[3], sel),
+                                        __byte_perm(w[3], w[4], sel), __byte_perm(w[4], w[5], sel));
+        else if (q == 2) v = make_uint4(__byte_perm(w[2], w[3], sel), __byte_perm(w[3], w[4], sel),
+                                        __byte_perm(w[4], w[5], sel), __byte_perm(w[5], w[6], sel));
+        else v = make_uint4(__byte_perm(w[3], w[4], sel), __byte_perm(w[4], w[5], sel),
+                            __byte_perm(w[5], w[6], sel), __byte_perm(w[6], w[7], sel));
         d4[k] = v;
     }
     for (int k = head + (nvec << 4) + threadIdx.x; k < len; k += CX_NT) dst[k] = src[k];
@@ -421,6 +489,8 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
     __shared__ int s_head_nl, s_last_nl, s_nrare, s_err_ord, s_r0, s_r2, s_nfe;
     __shared__ unsigned s_esc, s_skip, s_flag, s_inl;
     __shared__ unsigned long long s_pre_out, s_pre_lines;
+    __shared__ __align__(8) uint64_t s_mbar;  // window bulk copies
+    unsigned mbar_phase = 0;
 
     // tokenizer transducer (static: constant addresses); rows of CX_LUTS bytes so
     // the same byte in different states falls in different banks
@@ -459,7 +529,10 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
     }
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    if (tid == 0) s_esc = 0;
+    if (tid == 0) {
+        s_esc = 0;
+        cx_mbar_init(&s_mbar);
+    }
     PhaseClock pc;
     pc.start();
 
@@ -480,11 +553,15 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
         const long long T1 = min(job.n, T0 + CX_TILE);
         const long long ws = T0 - CX_HEAD;
         const int tile_end = (int)(T1 - ws);
-        cx_load_window(job.in, job.n, ws, cx_align16(tile_end), S.win);
+        const bool bulk = cx_load_window(job.in, job.n, ws, cx_align16(tile_end), S.win, &s_mbar);
         for (int k = tid; k < CX_WORDS; k += CX_NT) S.gbits[k] = S.fbits[k] = 0u;
         S.lane_b[tid] = 0;  // lane output adjustments (compaction gaps, arena lines)
-        if (PA && tid < CX_HIST) S.hist[tid] = 0;  // P3 buckets
+        if (SL && tid < CX_HIST) S.hist[tid] = 0;  // P3 buckets
         if (lane == 0) S.njobs[tid >> 5] = 0;
+        if (bulk) {
+            cx_mbar_wait(&s_mbar, mbar_phase);
+            mbar_phase ^= 1u;
+        }
         __syncthreads();
         // the final tile closes a last line without '\n' with a virtual one
         int win_end = tile_end;
