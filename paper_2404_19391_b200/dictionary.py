@@ -85,26 +85,33 @@ class Dictionary:
         self._validate()
 
     def _validate(self):
-        if not 2 <= self.l_min <= self.l_max <= MAX_PATTERN_LEN:
-            raise ValueError(f"bad length bounds [{self.l_min}, {self.l_max}]")
-        if len(self.learned) > MAX_PATTERNS:
-            raise ValueError(f"{len(self.learned)} learned patterns, max {MAX_PATTERNS}")
-        if len(set(self.learned)) != len(self.learned):
-            raise ValueError("duplicate learned patterns")
+        """The reference's construction checks, first failing rule wins;
+        the ValueError texts are part of the drop-in contract
+        (dictionary.py:79-99, pinned by tests/test_serialize.py)."""
+        lo, hi = self.l_min, self.l_max
+        rules = [
+            (lambda: 2 <= lo <= hi <= MAX_PATTERN_LEN, lambda: f"bad length bounds [{lo}, {hi}]"),
+            (lambda: len(self.learned) <= MAX_PATTERNS,
+             lambda: f"{len(self.learned)} learned patterns, max {MAX_PATTERNS}"),
+            (lambda: len(set(self.learned)) == len(self.learned), lambda: "duplicate learned patterns"),
+        ]
+        for ok, msg in rules:
+            if not ok():
+                raise ValueError(msg())
         for p in self.learned:
-            if not self.l_min <= len(p) <= self.l_max:
-                raise ValueError(f"pattern {p!r} outside [{self.l_min}, {self.l_max}]")
-            if not set(p) <= ALPHABET:
+            if not lo <= len(p) <= hi:
+                raise ValueError(f"pattern {p!r} outside [{lo}, {hi}]")
+            if not ALPHABET.issuperset(p):
                 raise ValueError(f"pattern {p!r} has non-alphabet bytes")
-        for b in self.identity:
-            if not 0x21 <= b <= 0x7E:
-                raise ValueError(f"identity byte 0x{b:02x} not printable")
+        bad = sorted(b for b in self.identity if not 0x21 <= b <= 0x7E)
+        if bad:
+            raise ValueError(f"identity byte 0x{bad[0]:02x} not printable")
 
     @cached_property
     def code_of(self) -> dict:
-        codes = {bytes([b]): b for b in self.identity}
-        codes.update({p: 0x80 + i for i, p in enumerate(self.learned)})
-        return codes
+        """pattern -> code: an identity byte is its own code, learned[i] is 0x80 + i."""
+        return {**{bytes([b]): b for b in self.identity},
+                **{p: 0x80 + i for i, p in enumerate(self.learned)}}
 
     @cached_property
     def encode_trie(self) -> PatternTrie:
@@ -112,19 +119,22 @@ class Dictionary:
 
     @cached_property
     def decode_tables(self):
-        """(exp_len i32[256], valid u8[256], exp_off i64[257], exp_flat u8[])"""
-        exps = [b""] * 256
+        """(exp_len i32[256], valid u8[256], exp_off i64[257], exp_flat u8[]):
+        the per-code expansion table the decoder takes (the reference's
+        dictionary.py:112-129 layout), built as arrays over the code space."""
+        ident = np.fromiter(sorted(self.identity), np.int64, len(self.identity))
+        learned = 0x80 + np.arange(len(self.learned), dtype=np.int64)
         valid = np.zeros(256, np.uint8)
-        for b in self.identity:
-            exps[b] = bytes([b])
-            valid[b] = 1
-        for i, p in enumerate(self.learned):
-            exps[0x80 + i] = p
-            valid[0x80 + i] = 1
-        exp_len = np.array([len(e) for e in exps], np.int32)
-        exp_off = np.zeros(257, np.int64)
-        np.cumsum(exp_len, out=exp_off[1:])
-        exp_flat = np.frombuffer(b"".join(exps), np.uint8).copy()
+        valid[ident] = 1
+        valid[learned] = 1
+        exp_len = np.zeros(256, np.int32)
+        exp_len[ident] = 1
+        exp_len[learned] = [len(p) for p in self.learned]
+        exp_off = np.concatenate([[0], np.cumsum(exp_len, dtype=np.int64)])
+        exp_flat = np.zeros(int(exp_off[-1]), np.uint8)
+        exp_flat[exp_off[ident]] = ident
+        for code, p in zip(learned.tolist(), self.learned):
+            exp_flat[exp_off[code]:exp_off[code + 1]] = np.frombuffer(p, np.uint8)
         return exp_len, valid, exp_off, exp_flat
 
     def cache_key(self):
@@ -150,43 +160,50 @@ def serialize(d: Dictionary) -> bytes:
     return b"\n".join(head + list(d.learned)) + b"\n"
 
 
-def deserialize(data: bytes) -> Dictionary:
-    rows = data.split(b"\n")
-    if rows and rows[-1] == b"":
-        rows.pop()
+def _header(rows):
+    """(prepopulate mode, l_min, l_max) from the three ZSD1 header rows; the
+    exception types and texts are the reference's (dictionary.py:332-373)."""
     if not rows or rows[0] != _MAGIC:
         if rows and rows[0][:3] == _MAGIC[:3]:
             raise UnsupportedVersion(f"unsupported version {rows[0]!r}")
         raise BadMagic("not a ZSD dictionary file")
     if len(rows) < 3:
         raise DictionaryFormatError("truncated header")
-    if not rows[1].startswith(b"prepopulate="):
+    key, _, mode_b = rows[1].partition(b"=")
+    if key != b"prepopulate" or not rows[1].startswith(b"prepopulate="):
         raise DictionaryFormatError(f"bad prepopulate line {rows[1]!r}")
-    mode = rows[1][len(b"prepopulate="):].decode("ascii", "replace")
+    mode = mode_b.decode("ascii", "replace")
     if mode not in PREPOPULATE_SETS:
         raise DictionaryFormatError(f"unknown prepopulate mode {mode!r}")
-    fields = rows[2].split(b" ")
-    if len(fields) != 2 or not fields[0].startswith(b"lmin=") or not fields[1].startswith(b"lmax="):
-        raise DictionaryFormatError(f"bad bounds line {rows[2]!r}")
+    bounds = rows[2].split(b" ")
     try:
-        l_min, l_max = int(fields[0][5:]), int(fields[1][5:])
+        if len(bounds) != 2 or bounds[0][:5] != b"lmin=" or bounds[1][:5] != b"lmax=":
+            raise ValueError
+        l_min, l_max = (int(f[5:]) for f in bounds)
     except ValueError:
         raise DictionaryFormatError(f"bad bounds line {rows[2]!r}") from None
     if not 2 <= l_min <= l_max <= MAX_PATTERN_LEN:
         raise DictionaryFormatError(f"bad length bounds [{l_min}, {l_max}]")
+    return mode, l_min, l_max
+
+
+def deserialize(data: bytes) -> Dictionary:
+    """ZSD1 bytes -> Dictionary, with the reference's checks and messages."""
+    rows = data.split(b"\n")
+    if rows and rows[-1] == b"":
+        del rows[-1]
+    mode, l_min, l_max = _header(rows)
     patterns = rows[3:]
     if len(patterns) > MAX_PATTERNS:
         raise TooManyPatterns(f"{len(patterns)} patterns, max {MAX_PATTERNS}")
     seen = set()
     for p in patterns:
-        if len(p) > l_max:
-            raise PatternTooLong(f"pattern {p!r} longer than lmax={l_max}")
-        if len(p) < l_min:
-            raise DictionaryFormatError(f"pattern {p!r} shorter than lmin={l_min}")
-        if not set(p) <= ALPHABET:
-            raise NonAlphabetByteInPattern(f"pattern {p!r}")
-        if p in seen:
-            raise DictionaryFormatError(f"duplicate pattern {p!r}")
+        problem = (PatternTooLong(f"pattern {p!r} longer than lmax={l_max}") if len(p) > l_max else
+                   DictionaryFormatError(f"pattern {p!r} shorter than lmin={l_min}") if len(p) < l_min else
+                   NonAlphabetByteInPattern(f"pattern {p!r}") if not ALPHABET.issuperset(p) else
+                   DictionaryFormatError(f"duplicate pattern {p!r}") if p in seen else None)
+        if problem is not None:
+            raise problem
         seen.add(p)
     return Dictionary(patterns, mode, l_min=l_min, l_max=l_max)
 

@@ -12,6 +12,8 @@ line's ``batch_lines`` batch are written to ``dst`` before ``LineError``
 is raised (pipeline.py:154-161 writes batches in order as they finish).
 """
 
+import os
+import threading
 import time
 from dataclasses import dataclass
 
@@ -163,9 +165,21 @@ def run_stream(src, dst, d, direction="compress", *, preprocess=False, lenient=F
     lock is held for the whole stream); `dst.write` receives bytes."""
     if direction not in ("compress", "decompress"):
         raise ValueError(f"bad direction {direction!r}")
-    # the staging buffers are per context: one stream at a time per device
-    with _lib.context(device).lock:
+    # the page-locked staging is per device: one stream at a time per device
+    with _stream_lock(device):
         return _run_stream(src, dst, d, direction, preprocess, lenient, batch_lines, device, segment_bytes)
+
+
+_locks_guard = threading.Lock()
+_stream_locks = {}
+
+
+def _stream_lock(device):
+    if device is None:
+        device = int(os.environ.get("ZS_DEVICE", "0"))  # _lib.context's default
+    key = device if isinstance(device, int) else id(device)
+    with _locks_guard:
+        return _stream_locks.setdefault(key, threading.Lock())
 
 
 def _run_stream(src, dst, d, direction, preprocess, lenient, batch_lines, device, segment_bytes):

@@ -40,8 +40,12 @@ def full(rep, dst, name):
                          capture_output=True, text=True).stdout
     hot = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_hot.py"), rep, "30"],
                          capture_output=True, text=True).stdout
+    phases = ""
+    if name == "compress":  # per-phase instruction accounting (source-line ranges of zs_cx.cuh)
+        phases = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "phase_ranges.py"), rep],
+                                capture_output=True, text=True).stdout
     with open(os.path.join(dst, f"ncu_{name}.txt"), "w") as fh:
-        fh.write(txt + "\n" + hot)
+        fh.write(txt + "\n" + phases + "\n" + hot)
     print(txt)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
                           "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
@@ -61,7 +65,8 @@ def main():
     rnd = sys.argv[1]
     dst = os.path.join(ROOT, "profiles", rnd)
     os.makedirs(dst, exist_ok=True)
-    for f in ("bench.json", "bench_ref.json", "gpu_tests.log", "smoke.log", "configs.json", "train.json"):
+    for f in ("bench.json", "bench_ref.json", "bench_c5.json", "gpu_tests.log", "smoke.log", "configs.json",
+              "train.json"):
         if os.path.exists(os.path.join(OUT, f)):
             shutil.copy(os.path.join(OUT, f), os.path.join(dst, f))
     launches(dst)
