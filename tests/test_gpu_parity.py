@@ -420,6 +420,65 @@ def test_sharded_gpu_codec(world):
     assert blob == want and v.total_lines == st["lines"]
 
 
+def test_parse_optimal_vs_brute_force():
+    """The GPU parse is a minimum-cost parse (reference test_codec.py:57-69):
+    payload length == codec.oracle_parse_cost (exhaustive recursion, no trie,
+    no DP) on short lines over random dictionaries, escape bytes included."""
+    from paper_2404_19391_b200.codec import oracle_parse_cost
+    rng = random.Random(91)
+    for _ in range(40):
+        pats = {bytes(rng.choice(b"CcN1(=O") for _ in range(rng.randint(2, 5))) for _ in range(rng.randint(0, 12))}
+        d = z.Dictionary(sorted(pats), "smiles", l_min=2, l_max=5)
+        lines = [bytes(rng.choice(b"CcN1(=O \tx") for _ in range(rng.randint(0, 16))) for _ in range(25)]
+        recs, _ = z.compress_lines(d, lines)
+        assert [len(r) for r in recs] == [oracle_parse_cost(d, ln) for ln in lines]
+
+
+def test_random_access_vs_oracle():
+    """RecordIndex against the CPU oracle's restatement of the reference
+    decoder (numba_impl.py:74-139 via oracle.decompress_batch): every
+    requested record's bytes, and for bad records the reference's
+    UnknownCode(code, offset) / TruncatedEscape(offset), with escape-heavy
+    records from a random dictionary and records with unknown codes and
+    dangling escapes mixed in."""
+    rng = random.Random(77)
+    d = z.Dictionary([b"CC", b"c1", b"ccc", b"(=O)"], "smiles")
+    t = oracle.Tables(d.learned, bytes(sorted(d.identity)))
+    lines = [bytes(rng.choice(b"Cc1()=O \t\xff") for _ in range(rng.randrange(0, 50))) for _ in range(4000)]
+    recs, _ = oracle.compress_batch(t, lines)
+    for k in rng.sample(range(len(recs)), 60):  # corrupt some records
+        kind = rng.randrange(3)
+        if kind == 0:
+            recs[k] = recs[k] + b" "              # dangling escape
+        elif kind == 1:
+            recs[k] = recs[k][:1] + b"\x9f" + recs[k][1:]  # unknown code
+        else:
+            recs[k] = b""
+    ref = oracle.decompress_batch(t, recs)
+    starts = np.concatenate([[0], np.cumsum(ref["out_lens"])])
+    ix = z.RecordIndex(b"\n".join(recs) + b"\n", d)
+    assert len(ix) == len(recs)
+    good = [i for i in range(len(recs)) if ref["status"][i] == 0]
+    sel = [rng.choice(good) for _ in range(3000)]
+    got = ix.decode(sel)
+    assert got == [ref["out"][starts[i]:starts[i + 1]] for i in sel]
+    data, off = ix.decode_packed(sel)
+    assert [data[a:b].tobytes() for a, b in zip(off[:-1], off[1:])] == got
+    for i in range(len(recs)):
+        st = int(ref["status"][i])
+        if st == 0:
+            continue
+        ep = int(ref["errpos"][i])
+        if st == 1:
+            with pytest.raises(z.UnknownCode) as e:
+                ix.decode([good[0], i])
+            assert (e.value.code, e.value.offset) == (recs[i][ep], ep)
+        else:
+            with pytest.raises(z.TruncatedEscape) as e:
+                ix.decode([i])
+            assert e.value.offset == ep
+
+
 def test_run_library_two_contexts(corpus_hashes):
     """The single-process multi-GPU API (shard.run_library) with two real
     contexts on one device (one shard each, run concurrently) reproduces the

@@ -208,3 +208,41 @@ def test_cli_train_and_bench(tmp_path, capsys):
     assert len(rows) == 4 and "c.smi" in rows[1] and "b.smi" in rows[1]
     for r in rows[2:]:
         assert all(0.0 < float(x) <= 1.5 for x in r.split()[1:])
+
+
+def test_bench_tables_match_reference(tmp_path, capsys):
+    """`zsmiles bench` (ablation table and cross-dictionary matrix) prints the
+    same ratio cells as the reference's own CLI on the same corpora
+    (tests/golden/bench_cases.json, made by running the reference,
+    make_bench_golden.py), and the paper's Table I / II trends hold as the
+    reference's acceptance test states them (test_acceptance.py:111-149):
+    renumbering on beats off for every prepopulation, 'smiles' is the best
+    prepopulation, and each corpus compresses best with its own dictionary."""
+    import json
+    import os
+    from conftest import ROOT
+    with open(os.path.join(ROOT, "tests", "golden", "bench_cases.json")) as fh:
+        g = json.load(fh)
+    paths = {}
+    for name, (kind, n, seed) in g["corpora"].items():
+        p = tmp_path / f"{name}.smi"
+        p.write_bytes(synth.generate(kind, n, seed).tobytes())
+        paths[name] = str(p)
+    for c in g["cases"]:
+        assert cli_main(["bench", "-i", *[paths[k] for k in c["corpora"]], *c["args"]]) == 0
+        rows = capsys.readouterr().out.strip().splitlines()
+        if len(c["corpora"]) == 1:
+            cells = [r.split()[:3] for r in rows[1:]]
+            assert cells == c["cells"], c["name"]
+            ratio = {(r[0] == "yes", r[1]): float(r[2]) for r in cells}
+            for m in ("printable", "smiles", "none"):
+                assert ratio[(True, m)] < ratio[(False, m)]
+            for pre in (True, False):
+                assert ratio[(pre, "smiles")] <= min(ratio[(pre, "printable")], ratio[(pre, "none")])
+        else:
+            cells = [r.split() for r in rows[2:]]
+            assert cells == c["cells"], c["name"]
+            grid = [[float(x) for x in r[1:]] for r in cells]
+            for te in range(len(grid)):
+                assert all(grid[te][te] <= grid[tr][te] for tr in range(len(grid)))
+
