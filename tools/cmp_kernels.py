@@ -1,6 +1,7 @@
-"""Compress kernel comparison (device API, HBM-resident input): lane-chunk
-(mode 3, default: byte-exact parse slices), lane-chunk parsing line ranges
-(mode 19) and the queue-based in-place kernel (mode 11).
+"""Compress kernel comparison (device API, HBM-resident input, modes of
+zs_set_transducer, include/zs_debug.h): 3 compress_cx with the product-automaton
+parse (default), 19 without the long-line slices, 67 the DFA + transducer
+parse, 131 every phase on byte-exact slices, 1 the generic transducer kernel.
 
     python tools/cmp_kernels.py [lines]
 """
@@ -26,7 +27,7 @@ def main():
         dout = torch.empty(2 * buf.size + 64, dtype=torch.uint8, device="cuda")
         r = _lib.Result()
         outs = {}
-        for mode in (3, 19, 11):
+        for mode in (3, 19, 67, 131, 1):
             ctx.lib.zs_set_transducer(ctx.h, mode)
             for _ in range(3):
                 rc = ctx.lib.zs_compress_device(ctx.h, din.data_ptr(), buf.size, dout.data_ptr(), dout.numel(),
@@ -36,8 +37,7 @@ def main():
             outs[mode] = bytes(dout[:r.out_bytes].cpu().numpy())
             print(f"{kind:9s} {buf.size / 1e6:8.1f} MB mode {mode:2d} {ctx.lib.zs_last_kernel(ctx.h).decode():22s} "
                   f"{ms:8.3f} ms {buf.size / ms / 1e6:8.1f} GB/s")
-        assert outs[3] == outs[11], kind
-        assert outs[19] == outs[11], kind
+        assert all(o == outs[3] for o in outs.values()), kind
     ctx.lib.zs_set_transducer(ctx.h, 3)
 
 
