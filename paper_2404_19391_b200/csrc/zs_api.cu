@@ -670,7 +670,7 @@ bool build_pa(HostTables &ht) {
     }
     const int npc = (int)cols.size();
     if (npc * 4 > 255 || (long long)P * npc * 4 > 65536) return false;
-    if (CX_O_DFA + cx_align16(P * npc * 4) > cx_dyn_smem_limit()) return false;
+    if (cx_pa_smem_bytes(P, npc, true) > cx_dyn_smem_limit()) return false;
     std::vector<int> col_rep(npc, -1);
     for (int b = 0; b < 256; ++b)
         if (col_rep[cmap[b]] < 0) col_rep[cmap[b]] = ht.cx_cmap[b];
@@ -765,9 +765,10 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
         if (cx) {
             const bool kw = !ctx->ht.cx_ok;
             const bool pa = ctx->ht.pa_ok && !kw && !ctx->no_pa;
-            const int g2 = (int)std::min<long long>(nt, (long long)ctx->n_sm * CX_CTAS);
+            const int ctas = pa && !ctx->slices ? cx_ctas<true, false>() : cx_ctas<true, true>();
+            const int g2 = (int)std::min<long long>(nt, (long long)ctx->n_sm * ctas);
             if (pa) {
-                const int smem = cx_pa_smem_bytes(ctx->ht.pa_states, ctx->ht.pa_cols);
+                const int smem = cx_pa_smem_bytes(ctx->ht.pa_states, ctx->ht.pa_cols, ctx->slices != 0);
                 auto k = ctx->slices ? compress_cx<true, true> : compress_cx<true, false>;
                 CK(set_smem(k, smem));
                 CxTables ct{nullptr, nullptr, nullptr, ctx->d_pacmap.as<uint8_t>(), ctx->ht.pa_states, 0,

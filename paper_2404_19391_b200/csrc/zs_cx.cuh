@@ -42,10 +42,9 @@
 
 namespace zs {
 
-constexpr int CX_NT = 384;
-constexpr int CX_CTAS = 2;                        // resident CTAs per SM
+constexpr int CX_NT = 256;
 constexpr int CX_NW = CX_NT / 32;
-constexpr int CX_CC = 78;                         // bytes of line ends per lane (tile 29,952 B)
+constexpr int CX_CC = 78;                         // bytes of line ends per lane (tile 19,968 B)
 constexpr int CX_TILE = CX_NT * CX_CC;
 constexpr int CX_HEAD = 2048;                     // staged before the tile
 constexpr int CX_WIN = CX_HEAD + CX_TILE;         // multiple of 32 (bitmap words)
@@ -56,7 +55,7 @@ constexpr int CX_CODES = 20;                      // code-slot row stride (0 esc
                                                   // rows of random states spread over the 32 banks)
 constexpr int CX_LUTS = 260;                      // tokenizer LUT row stride (65 words)
 constexpr int CX_T2S = 18;                        // transducer row stride in u16 (9 words, same reason)
-constexpr int CX_OUTCAP = 17408;                  // staging (tile output up to ratio ~0.55)
+constexpr int CX_OUTCAP = 11264;                  // staging (tile output up to ratio ~0.55)
 constexpr int CX_RARE = 64;                       // rare lines per tile
 constexpr int CX_JOBS = 16;                       // '%nn' compactions per warp and tile
 constexpr int CX_WARM = 32;                       // P4 warm-up bytes right of a slice (speculative entry)
@@ -108,6 +107,16 @@ constexpr int CX_O_HIST = CX_O_POOL + CX_POOL * 4;
 constexpr int CX_O_CODES = (CX_O_HIST + CX_HIST * 4 + 15) & ~15;  // code slots, when they fit here
 constexpr int CX_CODES_CAP = 256 * CX_CODES;                        // (transducer DFAs: <= 256 states)
 constexpr int CX_O_DFA = CX_O_CODES + CX_CODES_CAP;
+
+// Per kernel variant: resident CTAs per SM and where the dictionary tables
+// start.  The default kernel (product automaton, line-lane phases) needs
+// neither the P3 line pool / buckets (slices only) nor the code slots
+// (DFA + transducer only), so its tables follow the job lists and three CTAs
+// fit an SM: barriers of one CTA are covered by two others.
+template <bool PA, bool SL>
+__host__ __device__ constexpr int cx_ctas() { return (PA && !SL) ? 3 : 2; }
+template <bool PA, bool SL>
+__host__ __device__ constexpr int cx_o_tab() { return (PA && !SL) ? CX_O_POOL : PA ? CX_O_CODES : CX_O_DFA; }
 static_assert(CX_O_JOBS % 16 == 0, "int4 job slots");
 
 struct CxLayout {
@@ -143,7 +152,9 @@ struct CxTables {
 };
 
 // shared memory of compress_cx<true>: the fixed buffers, then the parse automaton
-__host__ __device__ inline int cx_pa_smem_bytes(int ns, int nc) { return CX_O_DFA + cx_align16(ns * nc * 4); }
+__host__ __device__ inline int cx_pa_smem_bytes(int ns, int nc, bool slices) {
+    return (slices ? cx_o_tab<true, true>() : cx_o_tab<true, false>()) + cx_align16(ns * nc * 4);
+}
 
 // kw: a 32-entry key ring per thread (stride 33 words: conflict-free banks)
 constexpr int CX_KW_RING = 33;
@@ -166,7 +177,7 @@ struct CxSmem {
     int *hist;       // [CX_HIST] event-count buckets (P3, PA)
 };
 
-__device__ inline CxSmem cx_carve(uint8_t *p, int o_t2, int o_codes) {
+__device__ inline CxSmem cx_carve(uint8_t *p, int o_t2, int o_codes, int o_tab) {
     CxSmem S;
     S.win = p + CX_O_WIN;
     S.rbits = reinterpret_cast<unsigned *>(p + CX_O_RB);
@@ -182,7 +193,7 @@ __device__ inline CxSmem cx_carve(uint8_t *p, int o_t2, int o_codes) {
     S.njobs = reinterpret_cast<int *>(p + CX_O_NJOBS);
     S.pool = reinterpret_cast<uint32_t *>(p + CX_O_POOL);
     S.hist = reinterpret_cast<int *>(p + CX_O_HIST);
-    S.dfa = reinterpret_cast<uint16_t *>(p + CX_O_DFA);
+    S.dfa = reinterpret_cast<uint16_t *>(p + o_tab);
     S.t2 = reinterpret_cast<uint16_t *>(p + o_t2);
     S.codes = p + o_codes;
     return S;
@@ -312,6 +323,41 @@ __device__ __forceinline__ unsigned cx_emit_range(const Job &job, const CxSmem &
     unsigned esc = 0;
     const uint8_t *__restrict__ win = S.win;
     const uint8_t *__restrict__ explen = S.explen;
+    if (STAGED) {
+        // explicit 32-bit shared addresses: with generic pointers the compiler
+        // rebuilds the shared window base (S2R SR_CgaCtaId, LEA) every code
+        const unsigned wb = (unsigned)__cvta_generic_to_shared(win), eb = (unsigned)__cvta_generic_to_shared(explen);
+        const unsigned ob = (unsigned)__cvta_generic_to_shared(o);
+        unsigned ww = (unsigned)w;
+        auto lb = [](unsigned a) {  // pure load: the window and explen do not change during the walk
+            unsigned v;
+            asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+            return v;
+        };
+        for (int p = p0; p <= p1;) {
+            const unsigned c = lb(wb + (unsigned)p);
+            if (c == 0x20) {
+                w = ww;
+                if (cx_bit(S.fbits, p)) {
+                    for (int r = 0; r < n_rare; ++r)  // an arena line's marker?
+                        if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p)
+                            esc += cx_emit_arena(job, S.explen, S.rare[r].aoff, o, w, S.rare[r].gs);
+                } else {
+                    o[w] = 0x20;
+                    o[w + 1] = job.in[ws + p];
+                    w += 2;
+                    ++esc;
+                }
+                ww = (unsigned)w;
+                ++p;
+            } else {
+                asm volatile("st.shared.u8 [%0], %1;" ::"r"(ob + ww), "r"(c) : "memory");
+                ++ww;
+                p += (int)lb(eb + c);
+            }
+        }
+        return esc;
+    }
     for (int p = p0; p <= p1;) {
         const unsigned c = win[p];
         if (c == 0x20) {
@@ -481,7 +527,7 @@ __device__ __forceinline__ int cx_prev_nl(const unsigned *rb, int q, int lo) {
 // lanes, but a block barrier between phases (measured slower on C2 than the
 // barrier-free line-lane pipeline; kept as a mode)
 template <bool PA, bool SL>
-__global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb, CxTables ct) {
+__global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job job, Tables tb, CxTables ct) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int s_tmp[CX_NW];
     __shared__ unsigned long long s_tmp64[CX_NW];
@@ -498,7 +544,7 @@ __global__ void __launch_bounds__(CX_NT, CX_CTAS) compress_cx(Job job, Tables tb
     __shared__ __align__(16) uint8_t s_explen[256];
     __shared__ __align__(16) uint8_t s_exp0[256];  // first byte of each code's expansion (P4 re-parse)
     __shared__ __align__(16) uint8_t s_cmap[256];
-    CxSmem S = cx_carve(smem, ct.o_t2, ct.o_codes);
+    CxSmem S = cx_carve(smem, ct.o_t2, ct.o_codes, cx_o_tab<PA, SL>());
     S.lut = s_lut;
     S.explen = s_explen;
     {
