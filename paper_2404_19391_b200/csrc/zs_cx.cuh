@@ -975,15 +975,6 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
                     }
                 };
                 if (fail) {
-#ifdef ZS_CHECKS
-                    if (t < 4) {
-                        char buf[96];
-                        int k = 0;
-                        for (int j = ls; j <= q && k < 90; ++j) buf[k++] = job.in[ws + j] == '\n' ? '|' : (char)job.in[ws + j];
-                        buf[k] = 0;
-                        printf("tile %lld tid %d fail line [%d,%d] oid %08x: %s\n", t, tid, ls, q, oid, buf);
-                    }
-#endif
                     cx_rare(S, &s_nrare, ls, q, RK_ARENA, own, local, 0, 0);
                     fill(ls, q);
                 } else if (oid != 0xffffffffu) {

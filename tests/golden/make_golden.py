@@ -340,6 +340,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also hash the 10M (C2) and 1M skewed corpora")
     ap.add_argument("--skip-small", action="store_true")
+    ap.add_argument("--c3-5m", action="store_true", help="also hash the full 5M-line skewed corpus (C3)")
     args = ap.parse_args()
 
     ddir = os.path.join(HERE, "dicts")
@@ -377,6 +378,8 @@ def main():
         if args.big:
             jobs += [("c2_10m", "aromatic", 10_000_000, 2024),
                      ("c3_skewed_1m", "skewed", 1_000_000, 2025)]
+        if args.c3_5m:
+            jobs += [("c3_skewed_5m", "skewed", 5_000_000, 2025)]
         for name, kind, n, seed in jobs:
             if name in hashes:
                 continue
