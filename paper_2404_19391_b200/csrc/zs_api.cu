@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <array>
 #include <map>
+#include <mutex>
 #include <set>
 #include <cstdio>
 #include <cstring>
@@ -139,6 +140,7 @@ struct zs_ctx {
     // shim scratch
     DevBuf s_flat, s_starts, s_out, s_lens, s_dec, s_stat, s_errpos, s_tot, s_ids, s_outst;
     Ctl *h_ctl = nullptr;  // pinned, NSLOT slots
+    uint8_t *h_last = nullptr;  // pinned: the device input's last byte (run_device)
     float last_ms = 0.f;
     int timing = 0;
     cudaStream_t user_stream = nullptr;  // zs_set_stream: device-pointer calls order after it
@@ -697,9 +699,22 @@ bool build_pa(HostTables &ht) {
     return true;
 }
 
+// The dynamic shared-memory limit of a kernel is one value per device: raise
+// it when a launch needs more than the value set so far, and skip the call
+// otherwise (it is not free on the per-launch path)
 template <typename K>
 cudaError_t set_smem(K kernel, int bytes) {
-    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    static std::map<std::pair<const void *, int>, int> limit;  // (kernel, device) -> bytes set
+    static std::mutex mu;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_pair(reinterpret_cast<const void *>(kernel), dev);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = limit.find(key);
+    if (it != limit.end() && it->second >= bytes) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) limit[key] = bytes;
+    return e;
 }
 
 typedef void (*TileKernel)(Job, Tables);
@@ -899,19 +914,16 @@ int run_device(zs_ctx *ctx, bool compress, const uint8_t *d_in, int64_t n, uint8
     CK(cudaSetDevice(ctx->dev));
     memset(res, 0, sizeof *res);
     if (int rc = after_user_stream(ctx)) return rc;
-    bool trailing = true;
-    if (n > 0) {
-        uint8_t last;
-        CK(cudaMemcpyAsync(&last, d_in + n - 1, 1, cudaMemcpyDeviceToHost, ctx->stream[0]));
-        CK(cudaStreamSynchronize(ctx->stream[0]));
-        trailing = last == '\n';
-    }
+    // the input's last byte (the trailing-newline rule) arrives with the
+    // results: an async copy into pinned memory, read after the call's sync
+    if (n > 0) CK(cudaMemcpyAsync(ctx->h_last, d_in + n - 1, 1, cudaMemcpyDeviceToHost, ctx->stream[0]));
     bool general = false;
     for (int attempt = 0; attempt < 5; ++attempt) {
         int rc = launch_stream(ctx, 0, compress, d_in, n, d_out, out_cap, flags, true, general);
         if (rc) return rc;
         CK(cudaEventSynchronize(ctx->ev_ctl[0]));
         if (n > 0) CK(cudaEventElapsedTime(&ctx->last_ms, ctx->ev0, ctx->ev1));
+        const bool trailing = n == 0 || *ctx->h_last == '\n';
         rc = collect(ctx, 0, n, nullptr, trailing, 0, res, false);
         if (rc == 1) continue;  // arena grown, re-run
         if (rc == 3) {          // bad record: the record-aware kernel decides
@@ -1123,6 +1135,7 @@ int zs_ctx_create(int device, zs_ctx **out) {
     if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_ctl, zs_ctx::NSLOT * sizeof(Ctl));
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_last, 16);
     if (e != cudaSuccess) {
         delete ctx;
         return ZS_E_CUDA;
@@ -1156,6 +1169,7 @@ int zs_ctx_destroy(zs_ctx *ctx) {
     if (ctx->ev_user) cudaEventDestroy(ctx->ev_user);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
+    if (ctx->h_last) cudaFreeHost(ctx->h_last);
     delete ctx;
     return ZS_OK;
 }
