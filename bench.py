@@ -77,8 +77,9 @@ def golden_c2():
 
 
 class ClockSampler:
-    """SM clocks and throttle reasons sampled (NVML, every 5 ms) during the
-    timed region."""
+    """SM clocks and throttle reasons sampled (NVML, every 2 ms) during the
+    timed region.  NVML is initialised before __enter__ returns, so even a
+    timed region of a few ms gets its first sample inside it."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
@@ -87,6 +88,7 @@ class ClockSampler:
         self.index = index
         self.sm, self.mx, self.reasons = [], 0.0, set()
         self.stop = threading.Event()
+        self.ready = threading.Event()
         self.t = None
 
     def _handle(self, nv):
@@ -100,16 +102,20 @@ class ClockSampler:
 
     def _run(self):
         import pynvml as nv
-        nv.nvmlInit()
-        h = self._handle(nv)
-        self.mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
-        while not self.stop.is_set():
+        try:
+            nv.nvmlInit()
+            h = self._handle(nv)
+            self.mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        finally:
+            self.ready.set()
+        while True:
             self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
             r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
             for name, bit in self.REASONS.items():
                 if r & bit:
                     self.reasons.add(name)
-            self.stop.wait(0.005)
+            if self.stop.wait(0.002):
+                break
         nv.nvmlShutdown()
 
     def __enter__(self):
@@ -117,6 +123,7 @@ class ClockSampler:
             import pynvml  # noqa: F401
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            self.ready.wait(timeout=10)
         except Exception:
             self.t = None
         return self

@@ -24,6 +24,11 @@ int zs_build_tables_host(const int32_t *children, const int16_t *term_code, int3
 int zs_build_t2_host(const int32_t *children, const int16_t *term_code, int32_t n_nodes,
                      uint16_t *dfa2, uint32_t *t2, int32_t *n_windows, int32_t *n_masks);
 
+/* Host-only: the newline-aligned chunk boundaries zs_*_host would use for a
+ * buffer with chunk size `chunk` bytes (cuts[0] = 0 ... n).  Writes up to cap
+ * entries; returns the number of boundaries, or <0 on bad arguments. */
+int64_t zs_debug_chunk_cuts(const uint8_t *h_in, int64_t n, int64_t chunk, int64_t *cuts, int64_t cap);
+
 /* compress-kernel selection for parity tests and ablations (default 3):
  * bits 0+1 clear: the generic key-window / trie-walk kernel (compress_tiles);
  * bit 4: compress_cx parses line-lane ranges instead of byte-exact slices;

@@ -32,7 +32,7 @@ EXPORTS = (
 )
 # measurement / inspection hooks (include/zs_debug.h), not part of the boundary
 DEBUG_EXPORTS = ("zs_build_tables_host", "zs_build_t2_host", "zs_set_transducer", "zs_set_phase_timing",
-                 "zs_last_phase_cycles")
+                 "zs_last_phase_cycles", "zs_debug_chunk_cuts")
 
 
 class Result(ctypes.Structure):
@@ -87,6 +87,7 @@ def load():
             "zs_set_phase_timing": (ctypes.c_int, [P, ctypes.c_int]),
             "zs_build_t2_host": (ctypes.c_int, [P, P, I32, P, P, P, P]),
             "zs_set_transducer": (ctypes.c_int, [P, ctypes.c_int]),
+            "zs_debug_chunk_cuts": (I64, [P, I64, I64, P, I64]),
             "zs_last_phase_cycles": (ctypes.c_int, [P, P]),
             "zs_last_kernel": (ctypes.c_char_p, [P]),
             "zs_stream": (P, [P]),
@@ -103,7 +104,11 @@ def load():
             "zs_host_free": (ctypes.c_int, [P, P]),
         }
         for name, (res, args) in sig.items():
-            f = getattr(lib, name)
+            f = getattr(lib, name, None)
+            if f is None and os.environ.get("ZS_LIB"):
+                continue  # an alternative (e.g. older) build used for a comparison
+            if f is None:
+                raise ImportError(f"{LIB_PATH} does not export {name}")
             f.restype = res
             f.argtypes = args
         _lib = lib

@@ -940,6 +940,29 @@ int run_device(zs_ctx *ctx, bool compress, const uint8_t *d_in, int64_t n, uint8
     return ZS_E_NOMEM;
 }
 
+// Host-buffer chunk boundaries, each just past a newline.  Sizes ramp up
+// from ch/16 (the first D2H / kernel starts after a short H2D) to ch and back
+// down over the last ~ch bytes (a short tail of kernel + D2H after the last
+// H2D).  cuts[0] = 0, cuts.back() = n.
+std::vector<long long> chunk_cuts(const uint8_t *h_in, long long n, long long ch) {
+    const long long lo = std::max<long long>(ch >> 4, 1 << 18);
+    long long up = lo;
+    std::vector<long long> cuts{0};
+    while (cuts.back() < n) {
+        const long long s = cuts.back(), rem = n - s;
+        long long size = std::min(up, ch);
+        up = std::min(2 * up, ch);  // (unclamped doubling overflowed after ~41 chunks)
+        if (rem < 2 * size) size = std::max(lo, rem / 2);
+        long long e = std::min<long long>(n, s + size);
+        if (e < n) {
+            const void *nl = memchr(h_in + e, '\n', (size_t)(n - e));
+            e = nl ? (long long)((const uint8_t *)nl - h_in) + 1 : n;
+        }
+        cuts.push_back(e);
+    }
+    return cuts;
+}
+
 // Host-buffer pipeline: newline-aligned chunks, NSLOT slots on NSLOT streams so
 // chunk k+1's H2D and kernel overlap chunk k's D2H.
 int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t *h_out,
@@ -956,26 +979,8 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
         const long long mb = e ? atoll(e) : 64;
         return (mb > 0 ? mb : 64) << 20;
     }();
-    // chunk boundaries just past a newline.  Sizes ramp up from CH/16 (the
-    // first D2H / kernel starts after a short H2D) and back down over the
-    // last ~CH bytes (a short tail of kernel + D2H after the last H2D);
-    // decompress chunks are 3/8 as large (the output is ~2.6x the input).
     const long long ch = compress ? CH : std::max<long long>(CH * 3 / 8, 1 << 20);
-    const long long lo = std::max<long long>(ch >> 4, 1 << 18);
-    long long up = lo;
-    std::vector<long long> cuts{0};
-    while (cuts.back() < n) {
-        const long long s = cuts.back(), rem = n - s;
-        long long size = std::min(up, ch);
-        up *= 2;
-        if (rem < 2 * size) size = std::max(lo, rem / 2);
-        long long e = std::min<long long>(n, s + size);
-        if (e < n) {
-            const void *nl = memchr(h_in + e, '\n', (size_t)(n - e));
-            e = nl ? (long long)((const uint8_t *)nl - h_in) + 1 : n;
-        }
-        cuts.push_back(e);
-    }
+    const std::vector<long long> cuts = chunk_cuts(h_in, n, ch);
     const int nch = (int)cuts.size() - 1;
     // ZS_TRACE=1: per-chunk event timeline on stderr (H2D end, kernel end,
     // D2H end, ms from the call's start) -- a measurement aid
@@ -991,7 +996,7 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
     };
     std::vector<int> chunk_of_slot(zs_ctx::NSLOT, -1);
     long long written = 0, line_base = 0;
-    bool general = false;  // a chunk hit a bad record: the record-aware kernel from then on
+    bool general = false;  // a chunk hit a bad record: its re-runs (and later re-runs) use the record-aware kernel
     bool capacity_hit = false;
     int pending = -1;  // slot whose output is waiting for D2H
     long long pend_len = 0, pend_n = 0;
@@ -1328,6 +1333,13 @@ int zs_set_stream(zs_ctx *ctx, void *stream) {
     if (!ctx) return ZS_E_ARG;
     ctx->user_stream = static_cast<cudaStream_t>(stream);
     return ZS_OK;
+}
+
+int64_t zs_debug_chunk_cuts(const uint8_t *h_in, int64_t n, int64_t chunk, int64_t *cuts, int64_t cap) {
+    if (n < 0 || (n > 0 && !h_in) || chunk <= 0 || (cap > 0 && !cuts)) return ZS_E_ARG;
+    const std::vector<long long> c = chunk_cuts(h_in, n, chunk);
+    for (size_t k = 0; k < c.size() && (int64_t)k < cap; ++k) cuts[k] = c[k];
+    return (int64_t)c.size();
 }
 
 int zs_set_transducer(zs_ctx *ctx, int on) {

@@ -305,6 +305,7 @@ __device__ __forceinline__ unsigned cx_emit_arena(const Job &job, const uint8_t 
             ++esc;
             ++i;
         } else {
+            ZS_ASSERT(explen[c] != 0);
             o[w++] = c;
             i += explen[c];
         }
@@ -340,8 +341,11 @@ __device__ __forceinline__ unsigned cx_emit_range(const Job &job, const CxSmem &
                 w = ww;
                 if (cx_bit(S.fbits, p)) {
                     for (int r = 0; r < n_rare; ++r)  // an arena line's marker?
-                        if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p)
+                        if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p) {
+                            const unsigned long long w0 = w;
                             esc += cx_emit_arena(job, S.explen, S.rare[r].aoff, o, w, S.rare[r].gs);
+                            ZS_ASSERT(w - w0 == (unsigned long long)S.rare[r].out);
+                        }
                 } else {
                     o[w] = 0x20;
                     o[w + 1] = job.in[ws + p];
@@ -349,8 +353,10 @@ __device__ __forceinline__ unsigned cx_emit_range(const Job &job, const CxSmem &
                     ++esc;
                 }
                 ww = (unsigned)w;
+                ZS_ASSERT(ww <= (unsigned)CX_STAGE);
                 ++p;
             } else {
+                ZS_ASSERT(ww < (unsigned)CX_STAGE);
                 asm volatile("st.shared.u8 [%0], %1;" ::"r"(ob + ww), "r"(c) : "memory");
                 ++ww;
                 p += (int)lb(eb + c);
@@ -1424,7 +1430,7 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
                 const int sz = R1 >= R0 ? (R1 - R0 + CX_NT) / CX_NT : 0;
                 const int s0 = R0 + tid * sz, e0 = min(R1, s0 + sz - 1);
                 const bool any = sz > 0 && s0 <= e0;
-                const bool spec = any && win[e0] != '\n';
+                const bool spec = any && win[e0] != '\n' && e0 < R1;  // (R1: nothing of the tile right of it)
                 // the guess: the state after a short warm-up over the next slice's
                 // first bytes from a virtual line end (the right neighbour
                 // rewrites those bytes last; a stale read only changes the guess)
@@ -1471,13 +1477,13 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
                 int rlo = s0, rj = 0;
                 if (sz > 0 && s0 <= e0) {
                     // entry state at e0
-                    if (PA && win[e0] != '\n') {
+                    if (PA && win[e0] != '\n' && e0 < R1) {
                         // no warm-up: enter in the line-end state; a wrong guess
                         // is repaired below from the right neighbour's exit
                         // state, only up to where the two parses converge
                         spec = true;
                         spec_state = 0;
-                    } else if (win[e0] != '\n') {
+                    } else if (win[e0] != '\n' && e0 < R1) {
                         // every such entry is checked below, also when a newline was
                         // found (the check does not depend on when the right
                         // neighbour rewrites these bytes; it rewrites them last)
@@ -1600,6 +1606,7 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
         for (int r = tid; r < n_rare; r += CX_NT) {
             CxRare &R = S.rare[r];
             if (R.kind == RK_ARENA) {
+                ZS_ASSERT(R.ls >= 0 && R.ls <= R.le && R.le < CX_WIN);
                 long long ge = ws + R.le, gs = ws + R.ls;
                 if (R.glob) {
                     gs = ge;
@@ -1807,6 +1814,7 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
             }
         }
         const bool staged = tile_out <= (unsigned long long)CX_STAGE;
+        ZS_ASSERT(p6off <= tile_out);
         pc.mark(job, 5);  // output scan
         unsigned esc = 0;
         if (staged && p6a <= p6b)

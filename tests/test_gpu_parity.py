@@ -423,6 +423,29 @@ def test_sharded_gpu_codec(world):
     assert blob == want and v.total_lines == st["lines"]
 
 
+@pytest.mark.parametrize("mode", [3, 19, 67, 131])
+def test_fuzz_regressions(mode):
+    """Inputs the randomised GPU sweep (tools/fuzz_gpu.py) once broke, shrunk
+    (tools/fuzz_bisect.py) and pinned against the oracle in every kernel mode
+    (tests/golden/fuzz_cases.json.gz)."""
+    import gzip
+    import json
+    import os
+    from conftest import ROOT
+    with gzip.open(os.path.join(ROOT, "tests", "golden", "fuzz_cases.json.gz"), "rt") as fh:
+        cases = json.load(fh)["cases"]
+    ctx = _lib.context()
+    try:
+        ctx.lib.zs_set_transducer(ctx.h, mode)
+        for c in cases:
+            d = z.Dictionary([bytes.fromhex(p) for p in c["learned"]], None, l_min=c["l_min"], l_max=c["l_max"],
+                             identity=bytes.fromhex(c["identity"]))
+            payload = bytes.fromhex(c["payload"])
+            _oracle_check(payload, d, c["pre"], c["lenient"])
+    finally:
+        ctx.lib.zs_set_transducer(ctx.h, 3)
+
+
 def test_parse_optimal_vs_brute_force():
     """The GPU parse is a minimum-cost parse (reference test_codec.py:57-69):
     payload length == codec.oracle_parse_cost (exhaustive recursion, no trie,

@@ -105,3 +105,31 @@ def test_default_dictionary_is_fast():
     t = oracle.Tables.from_zsd(golden_dict_bytes())
     fast, dfa, codes, ml = build_tables(t)
     assert fast == 1 and ml == 6 and dfa.shape[0] <= 256
+
+
+@pytest.mark.parametrize("chunk", [4096, 1 << 16, 64 << 20])
+def test_host_chunk_cuts(chunk):
+    """zs_*_host's newline-aligned chunking: cuts start at 0, end at n,
+    increase strictly, each interior cut sits just past a newline, and chunk
+    sizes stay bounded.  Hundreds of chunks (the 4 KB case) pin the ramp
+    against overflow -- its doubling once went unclamped and wrapped after
+    ~41 chunks (a 2.7 GB input crashed in memchr)."""
+    lib = _lib.load()
+    rng = np.random.default_rng(7)
+    lines = [b"C" * int(k) for k in rng.integers(1, 200, 12000)] + [b"c1ccccc1" * 2000]
+    buf = np.frombuffer(b"\n".join(lines) + b"\n", np.uint8)
+    n = buf.size
+    cap = 1 << 16
+    cuts = np.zeros(cap, np.int64)
+    m = lib.zs_debug_chunk_cuts(_lib.ptr(buf), n, chunk, _lib.ptr(cuts), cap)
+    assert 2 <= m <= cap
+    c = cuts[:m]
+    assert c[0] == 0 and c[-1] == n
+    assert (np.diff(c) > 0).all()
+    assert (buf[c[1:-1] - 1] == ord("\n")).all()
+    longest = max(len(x) for x in lines) + 1
+    assert np.diff(c).max() <= max(chunk, 1 << 18) + longest
+    if chunk == 4096:
+        assert m > 100
+    assert lib.zs_debug_chunk_cuts(None, 0, chunk, None, 0) == 1
+    assert lib.zs_debug_chunk_cuts(_lib.ptr(buf), n, 0, _lib.ptr(cuts), cap) < 0
