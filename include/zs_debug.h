@@ -34,7 +34,9 @@ int64_t zs_debug_chunk_cuts(const uint8_t *h_in, int64_t n, int64_t chunk, int64
  * bit 4: compress_cx parses line-lane ranges instead of byte-exact slices;
  * bit 6: compress_cx parses with the DFA + cost-window transducer instead of
  * the product automaton; bit 7: compress_cx runs every phase on byte-exact
- * slices (balanced lanes, block barriers between phases) */
+ * slices (balanced lanes, block barriers between phases); bit 8: lines longer
+ * than the staged window go to the general routine (one thread each) instead
+ * of the block-parallel long-line kernels */
 int zs_set_transducer(zs_ctx *ctx, int on);
 
 /* profiling aid: per-phase SM cycles of the tile kernels (summed over CTAs,

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -22,6 +23,7 @@
 #include "zs_kernels.cuh"
 #include "zs_fx.cuh"
 #include "zs_cx.cuh"
+#include "zs_ll.cuh"
 #include "zs_ix.cuh"
 #include "zs_train.cuh"
 
@@ -128,6 +130,10 @@ struct zs_ctx {
     // per-slot work buffers (NSLOT-deep host pipeline)
     DevBuf ctl[NSLOT], ts[NSLOT], terr[NSLOT], in[NSLOT], out[NSLOT], arena[NSLOT];  // arena: per slot
     DevBuf fxs[NSLOT];  // streaming-decode scratch per slot
+    // long lines (zs_ll.cuh) per slot: the recorded lines, the tiles' last
+    // newlines, per-block arrays, events, renumbered lines, decisions, output
+    DevBuf ll[NSLOT], tl[NSLOT], llb[NSLOT], lle[NSLOT], llc[NSLOT], llr[NSLOT], lld[NSLOT], llo[NSLOT];
+    int no_ll = 0;  // debug: long lines on the general routine (one thread each)
     DevBuf ixs;     // record-index scratch
     // dictionary training (zs_train.cuh): corpus, census scratch, rank table, selection state
     struct {
@@ -743,8 +749,11 @@ BatchKernel batch_kernel(int w) {
 }
 
 // one whole-buffer launch (device pointers) on `slot`'s buffers and stream
+int run_ll(zs_ctx *ctx, int slot, const uint8_t *d_in, long long nt, int flags, int *n_ll_out, int *launches);
+
 int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, long long n,
-                  uint8_t *d_out, long long out_cap, int flags, bool timed, bool general = false) {
+                  uint8_t *d_out, long long out_cap, int flags, bool timed, bool general = false,
+                  bool ll = false) {
     const bool cx = compress && (ctx->ht.cx_ok || ctx->ht.kw_ok) && !general && !ctx->no_t2 && !ctx->no_ip;
     const bool fx = !compress && ctx->fx_ok && !general;
     const long long tile = cx ? CX_TILE : fx ? FX_TILE : TILE;
@@ -774,6 +783,21 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
     job.arena_cap = (long long)ctx->arena[slot].cap;
     job.timing = ctx->timing;
     ctx->nk[slot] = nt > 0 ? 1 : 0;
+    // long lines: mode 0 records them (a re-run codes them first, mode 1)
+    const bool ll_ok = cx && ctx->ht.pa_ok && ctx->ht.cx_ok && !ctx->no_pa && !ctx->no_ll && nt > 0;
+    int ll_n = 0, ll_launches = 0;
+    if (ll_ok) {
+        if (ctx->ll[slot].reserve(sizeof(LLine) * LL_CAP) || ctx->tl[slot].reserve(sizeof(long long) * nt))
+            return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(long lines)");
+        if (ll) {
+            if (int rc = run_ll(ctx, slot, d_in, nt, flags, &ll_n, &ll_launches)) return rc;
+        }
+        job.ll = ctx->ll[slot].as<LLine>();
+        job.tl = ctx->tl[slot].as<long long>();
+        job.ll_cap = LL_CAP;
+        job.ll_mode = ll ? 1 : 0;
+        job.ll_n = ll_n;
+    }
     if (nt > 0) {
         const int grid = (int)std::min<long long>(nt, ctx->n_sm);
         if (timed) CK(cudaEventRecord(ctx->ev0, st));
@@ -790,6 +814,22 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
                             ctx->ht.pa_cols, 0, 0, ctx->p4_lane ? 0 : 1, 0, smem, ctx->d_pa.as<uint32_t>()};
                 k<<<g2, CX_NT, smem, st>>>(job, ctx->tb, ct);
                 ctx->last_kernel = ctx->slices ? "compress_cx<slices>" : "compress_cx";
+                if (ll && ll_n > 0) {  // the coded long lines to the offsets compress_cx reserved
+                    ll_place<<<dim3(ll_n, 64), LL_NT, 0, st>>>(job.ll, ll_n, ctx->llo[slot].as<uint8_t>(),
+                                                              d_out, out_cap);
+                    ++ll_launches;
+                    static const bool trace = getenv("ZS_LL_TRACE") != nullptr;
+                    if (trace) {  // measurement / debug aid: the coded lines after placement
+                        std::vector<LLine> L(ll_n);
+                        CK(cudaStreamSynchronize(st));
+                        CK(cudaMemcpy(L.data(), job.ll, sizeof(LLine) * ll_n, cudaMemcpyDeviceToHost));
+                        for (const auto &l : L)
+                            fprintf(stderr, "zs_ll ge %lld gs %lld nblk %d ev %d+%d status %d cost %lld esc %lld "
+                                    "obase %lld dst %lld\n", l.ge, l.gs, l.nblk, l.ev0, l.nev, l.status, l.cost,
+                                    l.esc, l.obase, l.dst);
+                    }
+                }
+                ctx->nk[slot] += ll_launches;
             } else {
                 const CxLayout L = kw ? cx_layout(ctx->ht.kw_states, 0, 2 * ctx->ht.kw_cols)
                                       : cx_layout(ctx->ht.cx_states, ctx->ht.n_windows, ctx->ht.cx_cols);
@@ -849,6 +889,198 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
     return ZS_OK;
 }
 
+// Long lines (zs_ll.cuh): code the lines compress_cx recorded on `slot` in
+// its last run (mode 0) with the block-parallel kernels, on the slot's
+// stream; the host reads back the few sizes it allocates by.  On return the
+// slot's line list holds, sorted by ge, every recorded line with its output
+// size (or LL_FALLBACK) for compress_cx's mode 1.
+int run_ll(zs_ctx *ctx, int slot, const uint8_t *d_in, long long nt, int flags, int *n_ll_out, int *launches) {
+    cudaStream_t st = ctx->stream[slot];
+    const int n_ll = (int)std::min<unsigned long long>(ctx->h_ctl[slot].ll_n, (unsigned long long)LL_CAP);
+    *n_ll_out = n_ll;
+    if (n_ll == 0) return ZS_OK;
+    LLine *d_ln = ctx->ll[slot].as<LLine>();
+    std::vector<LLine> L(n_ll);
+    auto d2h = [&](void *dst, const void *src, size_t bytes) -> int {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return ZS_OK;
+    };
+    if (int rc = d2h(L.data(), d_ln, sizeof(LLine) * n_ll)) return rc;
+    std::sort(L.begin(), L.end(), [](const LLine &a, const LLine &b) { return a.ge < b.ge; });
+    CK(cudaMemcpyAsync(d_ln, L.data(), sizeof(LLine) * n_ll, cudaMemcpyHostToDevice, st));
+    ll_setup<<<(n_ll * 32 + 255) / 256, 256, 0, st>>>(d_ln, n_ll, ctx->tl[slot].as<long long>(), nt, CX_TILE);
+    int nk = 1;
+    if (int rc = d2h(L.data(), d_ln, sizeof(LLine) * n_ll)) return rc;
+    // blocks of 256 bytes per line, within the per-launch byte budget
+    long long bytes = 0;
+    int nb = 0;
+    for (auto &l : L) {
+        const long long len = l.ge - l.gs;
+        l.blk0 = nb;
+        l.nblk = 0;
+        l.ev0 = l.nev = 0;
+        if (len <= 0 || len >= (1ll << 30) || bytes + len > LL_MAXBYTES) {
+            l.status = LL_FALLBACK;
+            continue;
+        }
+        l.nblk = (int)((len + LL_B - 1) / LL_B);
+        nb += l.nblk;
+        bytes += len;
+    }
+    CK(cudaMemcpyAsync(d_ln, L.data(), sizeof(LLine) * n_ll, cudaMemcpyHostToDevice, st));
+    if (nb == 0) {
+        CK(cudaStreamSynchronize(st));
+        *launches += nk;
+        return ZS_OK;
+    }
+    // Buffers at their worst case for `bytes` line bytes (a byte starts at
+    // most one ring token; a 1-byte token grows to 3; an escape doubles), so
+    // the passes below queue without host round trips.  Per block: map, cnt,
+    // rlen, pin, pout, g, x, ocnt, oesc, ooff (4 B) and par (16 B), nb + 1 each.
+    const size_t nb1 = (size_t)nb + 1, a4 = (nb1 * 4 + 15) & ~(size_t)15;
+    const size_t ne = (size_t)bytes + 1, e4 = (ne * 4 + 15) & ~(size_t)15, e2 = (ne * 2 + 15) & ~(size_t)15;
+    const size_t nseg = (ne + LL_SEG - 1) / LL_SEG;
+    const size_t rcap = 3 * (size_t)bytes + 64, ocap = 2 * rcap + (size_t)n_ll + 64;
+    const bool pre = (flags & ZS_F_PREPROCESS) != 0;
+    if (ctx->llb[slot].reserve(a4 * 10 + nb1 * 16 + 64) ||
+        (pre && (ctx->lle[slot].reserve(2 * e4 + e2 + ne + 64) ||
+                 ctx->llc[slot].reserve(nseg * (LL_NCOL + 1) * 8))) ||
+        ctx->llr[slot].reserve(rcap) || ctx->lld[slot].reserve(rcap) || ctx->llo[slot].reserve(ocap))
+        return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(long lines)");
+    uint8_t *pb = ctx->llb[slot].as<uint8_t>();
+    LLWork W{};
+    W.in = d_in;
+    W.ln = d_ln;
+    W.n_ll = n_ll;
+    W.nb = nb;
+    W.preprocess = pre ? 1 : 0;
+    W.map = reinterpret_cast<unsigned *>(pb);
+    W.cnt = reinterpret_cast<int *>(pb + a4);
+    W.rlen = reinterpret_cast<int *>(pb + 2 * a4);
+    W.pin = reinterpret_cast<unsigned *>(pb + 3 * a4);
+    W.pout = reinterpret_cast<unsigned *>(pb + 4 * a4);
+    W.g = reinterpret_cast<int *>(pb + 5 * a4);
+    W.x = reinterpret_cast<int *>(pb + 6 * a4);
+    W.ocnt = reinterpret_cast<int *>(pb + 7 * a4);
+    W.oesc = reinterpret_cast<int *>(pb + 8 * a4);
+    W.ooff = reinterpret_cast<int *>(pb + 9 * a4);
+    W.par = reinterpret_cast<uint4 *>(pb + 10 * a4);
+    int *flag = reinterpret_cast<int *>(pb + 10 * a4 + nb1 * 16);  // fix-loop flags: colour, parse, emit
+    if (pre) {
+        uint8_t *pe = ctx->lle[slot].as<uint8_t>();
+        W.epos = reinterpret_cast<int *>(pe);
+        W.epart = reinterpret_cast<int *>(pe + e4);
+        W.eflag = reinterpret_cast<uint16_t *>(pe + 2 * e4);
+        W.ecol = pe + 2 * e4 + e2;
+    }
+    int *exits = pre ? ctx->llc[slot].as<int>() : nullptr;
+    int *assumed = pre ? exits + nseg * (LL_NCOL + 1) : nullptr;
+    W.R = ctx->llr[slot].as<uint8_t>();
+    W.D = ctx->lld[slot].as<uint8_t>();
+    W.O = ctx->llo[slot].as<uint8_t>();
+    W.pa = ctx->d_pa.as<uint32_t>();
+    W.cmap = ctx->d_pacmap.as<uint8_t>();
+    W.pa_words = ctx->ht.pa_states * ctx->ht.pa_cols;
+    W.explen = ctx->tb.exp_len;
+    const int gb = (nb + LL_NT - 1) / LL_NT;
+    const int gseg = (int)((nseg + LL_NT - 1) / LL_NT);
+    const int pa_smem = W.pa_words * 4;
+    CK(set_smem(ll_parse, pa_smem));
+    CK(set_smem(ll_parse_fix, pa_smem));
+    // a fix pass per stage: the flag tells whether the pass changed an exit
+    auto colour_pass = [&](int pass) -> int {
+        W.changed = flag;
+        CK(cudaMemsetAsync(flag, 0, sizeof(int), st));
+        ll_colour<<<gseg, LL_NT, 0, st>>>(W, (int)(ne - 1), pass, exits, assumed);
+        ++nk;
+        return ZS_OK;
+    };
+    auto parse_pass = [&]() -> int {
+        W.changed = flag + 1;
+        CK(cudaMemsetAsync(flag + 1, 0, sizeof(int), st));
+        ll_parse_fix<<<gb, LL_NT, pa_smem, st>>>(W);
+        ++nk;
+        return ZS_OK;
+    };
+    auto emit_pass = [&]() -> int {
+        W.changed = flag + 2;
+        CK(cudaMemsetAsync(flag + 2, 0, sizeof(int), st));
+        ll_emit_fix<<<gb, LL_NT, 0, st>>>(W);
+        ++nk;
+        return ZS_OK;
+    };
+    auto settle = [&](int which, const std::function<int()> &pass) -> int {
+        for (int changed = 1; changed;) {
+            if (int rc = pass()) return rc;
+            if (int rc = d2h(&changed, flag + which, sizeof(int))) return rc;
+        }
+        return ZS_OK;
+    };
+    // stage 0: tokens, events, colours
+    if (pre) {
+        ll_tok_map<true><<<gb, LL_NT, 0, st>>>(W);
+        ll_scan<LLMap><<<1, LL_SNT, 0, st>>>(W.map, W.map, nb);
+        ll_tok_count<<<gb, LL_NT, 0, st>>>(W);
+        ll_scan<LLAdd><<<1, LL_SNT, 0, st>>>(W.cnt, W.cnt, nb);
+        ll_scan<LLXor><<<1, LL_SNT, 0, st>>>(W.par, W.par, nb);
+        ll_tok_events<<<gb, LL_NT, 0, st>>>(W);
+        // ne - 1 = the events bound; ll_pair / ll_colour stop at the real count
+        ll_pair<<<(int)((ne - 1 + LL_NT - 1) / LL_NT), LL_NT, 0, st>>>(W, (int)(ne - 1));
+        nk += 7;
+        for (int pass = 0; pass < 3; ++pass)
+            if (int rc = colour_pass(pass)) return rc;
+    } else {
+        ll_tok_map<false><<<gb, LL_NT, 0, st>>>(W);
+        ++nk;
+    }
+    // stages 1-3 queue with two fix passes each; one round trip checks that
+    // the last pass of each changed nothing (else that stage settles and
+    // everything after it runs again)
+    for (int from = 1;;) {
+        if (from <= 1) {
+            ll_rlen<<<gb, LL_NT, 0, st>>>(W);
+            ll_scan<LLAdd><<<1, LL_SNT, 0, st>>>(W.rlen, W.rlen, nb);
+            ll_rewrite<<<gb, LL_NT, 0, st>>>(W);
+            ll_parse<<<gb, LL_NT, pa_smem, st>>>(W);
+            nk += 4;
+            for (int k = 0; k < 2; ++k)
+                if (int rc = parse_pass()) return rc;
+        }
+        if (from <= 2) {
+            ll_emit_count<<<gb, LL_NT, 0, st>>>(W);
+            ++nk;
+            for (int k = 0; k < 2; ++k)
+                if (int rc = emit_pass()) return rc;
+        }
+        ll_scan<LLAdd><<<1, LL_SNT, 0, st>>>(W.ocnt, W.ooff, nb);
+        ll_emit_write<<<gb, LL_NT, 0, st>>>(W);
+        nk += 2;
+        int f[3] = {0, 0, 0};
+        if (int rc = d2h(f, flag, sizeof f)) return rc;
+        if (pre && f[0]) {  // colours still moving: settle them, then redo everything after
+            if (int rc = settle(0, [&] { return colour_pass(1); })) return rc;
+            from = 1;
+            CK(cudaMemsetAsync(flag, 0, sizeof(int), st));
+            continue;
+        }
+        if (f[1]) {
+            if (int rc = settle(1, parse_pass)) return rc;
+            from = 2;
+            continue;
+        }
+        if (f[2]) {
+            if (int rc = settle(2, emit_pass)) return rc;
+            from = 3;
+            continue;
+        }
+        break;
+    }
+    CK(cudaGetLastError());
+    *launches += nk;
+    return ZS_OK;
+}
+
 // Fill res from a finished slot; returns ZS_OK, or 1 = re-run needed
 // (arena exhausted), 2 = output capacity exceeded.
 int collect(zs_ctx *ctx, int slot, long long n, const uint8_t *h_last_byte_src, bool trailing,
@@ -862,6 +1094,7 @@ int collect(zs_ctx *ctx, int slot, long long n, const uint8_t *h_last_byte_src, 
     }
     (void)h_last_byte_src;
     if (c.overflow & 12ull) return 3;  // fast kernel met a case it hands over: re-run the general one
+    if (c.overflow & 16ull) return 4;  // long lines recorded: code them, run again (mode 1)
     zs_result r{};
     r.lines = (long long)c.lines;
     r.in_bytes = n;
@@ -917,9 +1150,9 @@ int run_device(zs_ctx *ctx, bool compress, const uint8_t *d_in, int64_t n, uint8
     // the input's last byte (the trailing-newline rule) arrives with the
     // results: an async copy into pinned memory, read after the call's sync
     if (n > 0) CK(cudaMemcpyAsync(ctx->h_last, d_in + n - 1, 1, cudaMemcpyDeviceToHost, ctx->stream[0]));
-    bool general = false;
-    for (int attempt = 0; attempt < 5; ++attempt) {
-        int rc = launch_stream(ctx, 0, compress, d_in, n, d_out, out_cap, flags, true, general);
+    bool general = false, ll = false;
+    for (int attempt = 0; attempt < 6; ++attempt) {
+        int rc = launch_stream(ctx, 0, compress, d_in, n, d_out, out_cap, flags, true, general, ll);
         if (rc) return rc;
         CK(cudaEventSynchronize(ctx->ev_ctl[0]));
         if (n > 0) CK(cudaEventElapsedTime(&ctx->last_ms, ctx->ev0, ctx->ev1));
@@ -928,6 +1161,10 @@ int run_device(zs_ctx *ctx, bool compress, const uint8_t *d_in, int64_t n, uint8
         if (rc == 1) continue;  // arena grown, re-run
         if (rc == 3) {          // bad record: the record-aware kernel decides
             general = true;
+            continue;
+        }
+        if (rc == 4) {          // long lines: the block-parallel long-line kernels first
+            ll = true;
             continue;
         }
         if (rc == 2) {
@@ -1010,7 +1247,7 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
         int rc = collect(ctx, slot, cn, nullptr, true, line_base, &r, false);
         if (rc < 0) return rc;
         (void)clen;
-        if (rc == 1 || rc == 2 || rc == 3) return 10 + rc;  // caller re-runs this chunk synchronously
+        if (rc >= 1 && rc <= 4) return 10 + rc;  // caller re-runs this chunk synchronously
         long long ob = (long long)ctx->h_ctl[slot].total_out;
         if (!capacity_hit && written + ob <= out_cap && ob > 0 && !r.err_line)
             CK(cudaMemcpyAsync(h_out + written, ctx->out[slot].p, ob, cudaMemcpyDeviceToHost,
@@ -1052,6 +1289,7 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
         mark(k, 1, slot);
         if (pending >= 0) {
             rc = finish(pending, pend_n, pend_len);
+            bool ll_chunk = false;
             while (rc >= 10) {  // re-run the previous chunk synchronously with bigger buffers
                 const int ps = pending;
                 CK(cudaStreamSynchronize(ctx->stream[ps]));
@@ -1060,9 +1298,10 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
                 CK(cudaMemcpyAsync(ctx->in[ps].p, h_in + cuts[k - 1], pend_n, cudaMemcpyHostToDevice,
                                    ctx->stream[ps]));
                 general |= rc == 13;
+                ll_chunk |= rc == 14;
                 rc = launch_stream(ctx, ps, compress, ctx->in[ps].as<uint8_t>(), pend_n,
                                    ctx->out[ps].as<uint8_t>(), (long long)ctx->out[ps].cap, flags, false,
-                                   general);
+                                   general, ll_chunk && !general);
                 if (rc) return rc;
                 rc = finish(ps, pend_n, pend_len);
             }
@@ -1073,6 +1312,7 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
     }
     if (pending >= 0 && !res->err_line) {
         int rc = finish(pending, pend_n, pend_len);
+        bool ll_chunk = false;
         while (rc >= 10) {
             const int ps = pending;
             CK(cudaStreamSynchronize(ctx->stream[ps]));
@@ -1081,9 +1321,10 @@ int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t
             CK(cudaMemcpyAsync(ctx->in[ps].p, h_in + cuts[nch - 1], pend_n, cudaMemcpyHostToDevice,
                                ctx->stream[ps]));
             general |= rc == 13;
+            ll_chunk |= rc == 14;
             rc = launch_stream(ctx, ps, compress, ctx->in[ps].as<uint8_t>(), pend_n,
                                ctx->out[ps].as<uint8_t>(), (long long)ctx->out[ps].cap, flags, false,
-                               general);
+                               general, ll_chunk && !general);
             if (rc) return rc;
             rc = finish(ps, pend_n, pend_len);
         }
@@ -1350,6 +1591,7 @@ int zs_set_transducer(zs_ctx *ctx, int on) {
     ctx->p4_lane = (on & 16) ? 1 : 0;  // bit 4: compress_cx parse over line-lane ranges, not byte slices
     ctx->no_pa = (on & 64) ? 1 : 0;    // bit 6: DFA + transducer parse instead of the product automaton
     ctx->slices = (on & 128) ? 1 : 0;  // bit 7: compress_cx on byte-exact slices in every phase
+    ctx->no_ll = (on & 256) ? 1 : 0;   // bit 8: long lines on the general routine, not zs_ll.cuh
     return ZS_OK;
 }
 

@@ -76,6 +76,7 @@ struct CxRare {
     int out;           // output bytes of the arena line incl. its '\n' (RK_ARENA)
     int glob;          // the line starts before the window (only its '\n' at le is staged)
     long long gs;      // global offset of the line's first byte (RK_ARENA)
+    int ll;            // RK_ARENA coded by the long-line kernels: its Job.ll entry; -1 = none
 };
 
 __host__ __device__ inline int cx_align16(int x) { return (x + 15) & ~15; }
@@ -343,6 +344,7 @@ __device__ __forceinline__ unsigned cx_emit_range(const Job &job, const CxSmem &
                     for (int r = 0; r < n_rare; ++r)  // an arena line's marker?
                         if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p) {
                             const unsigned long long w0 = w;
+                            ZS_ASSERT(S.rare[r].ll < 0);  // tiles with long lines emit direct
                             esc += cx_emit_arena(job, S.explen, S.rare[r].aoff, o, w, S.rare[r].gs);
                             ZS_ASSERT(w - w0 == (unsigned long long)S.rare[r].out);
                         }
@@ -369,8 +371,16 @@ __device__ __forceinline__ unsigned cx_emit_range(const Job &job, const CxSmem &
         if (c == 0x20) {
             if (cx_bit(S.fbits, p)) {
                 for (int r = 0; r < n_rare; ++r)  // an arena line's marker?
-                    if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p)
-                        esc += cx_emit_arena(job, S.explen, S.rare[r].aoff, o, w, S.rare[r].gs);
+                    if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p) {
+                        if (S.rare[r].ll >= 0) {  // long line: its bytes are placed by ll_place
+                            LLine &L = job.ll[S.rare[r].ll];
+                            L.dst = (long long)w;
+                            w += (unsigned long long)S.rare[r].out;
+                            esc += (unsigned)L.esc;
+                        } else {
+                            esc += cx_emit_arena(job, S.explen, S.rare[r].aoff, o, w, S.rare[r].gs);
+                        }
+                    }
             } else {
                 o[w] = 0x20;
                 o[w + 1] = job.in[ws + p];
@@ -503,6 +513,7 @@ __device__ __forceinline__ void cx_rare(const CxSmem &S, int *n, int ls, int le,
         R.aoff = 0;
         R.glob = glob;
         R.gs = 0;
+        R.ll = -1;
     }
 }
 
@@ -539,7 +550,7 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
     __shared__ unsigned long long s_tmp64[CX_NW];
     __shared__ long long s_tile;
     __shared__ int s_head_nl, s_last_nl, s_nrare, s_err_ord, s_r0, s_r2, s_nfe;
-    __shared__ unsigned s_esc, s_skip, s_flag, s_inl;
+    __shared__ unsigned s_esc, s_skip, s_flag, s_inl, s_has_ll;
     __shared__ unsigned long long s_pre_out, s_pre_lines;
     __shared__ __align__(8) uint64_t s_mbar;  // window bulk copies
     unsigned mbar_phase = 0;
@@ -596,7 +607,7 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
             s_nrare = 0;
             s_err_ord = 0x7fffffff;
             s_r0 = s_r2 = 0x7fffffff;
-            s_esc = s_skip = s_flag = 0;
+            s_esc = s_skip = s_flag = s_has_ll = 0;
         }
         __syncthreads();
         const long long t = s_tile;
@@ -676,6 +687,7 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
         }
         S.lane_a[tid] = cut;
         __syncthreads();
+        if (tid == 0 && job.tl) job.tl[t] = s_last_nl >= CX_HEAD ? ws + s_last_nl : -1;
         pc.mark(job, 0);  // load, newline bitmap, lane cuts
         // lane range (cut, end]; end = next lane's cut (last lane: the tile's last '\n')
         const int end = tid + 1 < CX_NT ? S.lane_a[tid + 1] : s_last_nl;
@@ -1605,12 +1617,44 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
         // ---- rare lines: general routine (HBM arena), one thread each ----
         for (int r = tid; r < n_rare; r += CX_NT) {
             CxRare &R = S.rare[r];
+            if (R.kind == RK_ARENA && R.glob && job.ll_mode == 0) {
+                // a long line: recorded for the block-parallel long-line kernels
+                // (the host runs them and this kernel again, in mode 1)
+                const unsigned long long i = atomicAdd(&job.ctl->ll_n, 1ull);
+                if (i < (unsigned long long)job.ll_cap) {
+                    job.ll[i].ge = ws + R.le;
+                    atomicOr(&job.ctl->overflow, 16ull);
+                    R.kind = RK_DROP;
+                }
+            }
             if (R.kind == RK_ARENA) {
                 ZS_ASSERT(R.ls >= 0 && R.ls <= R.le && R.le < CX_WIN);
                 long long ge = ws + R.le, gs = ws + R.ls;
                 if (R.glob) {
-                    gs = ge;
-                    while (gs > 0 && job.in[gs - 1] != '\n') --gs;
+                    int i = -1;
+                    if (job.ll_mode == 1) {  // coded by the long-line kernels?
+                        int lo = 0, hi = job.ll_n - 1;
+                        while (lo < hi) {
+                            const int mid = (lo + hi) >> 1;
+                            if (job.ll[mid].ge < ge) lo = mid + 1;
+                            else hi = mid;
+                        }
+                        if (job.ll_n > 0 && job.ll[lo].ge == ge) i = lo;
+                    }
+                    if (i >= 0) {
+                        gs = job.ll[i].gs;
+                        if (job.ll[i].status == LL_OK) {
+                            R.gs = gs;
+                            R.ll = i;
+                            R.out = (int)job.ll[i].cost + 1;
+                            atomicAdd(&S.lane_b[R.lane], R.out);
+                            s_has_ll = 1;
+                            continue;
+                        }
+                    } else {
+                        gs = ge;
+                        while (gs > 0 && job.in[gs - 1] != '\n') --gs;
+                    }
                 }
                 unsigned aoff = 0;
                 int kind = E_NONE, eoff = -1;
@@ -1813,7 +1857,7 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
                 if (!(sz > 0 && s0 <= e0)) p6b = p6a - 1;  // empty slice
             }
         }
-        const bool staged = tile_out <= (unsigned long long)CX_STAGE;
+        const bool staged = tile_out <= (unsigned long long)CX_STAGE && !s_has_ll;
         ZS_ASSERT(p6off <= tile_out);
         pc.mark(job, 5);  // output scan
         unsigned esc = 0;

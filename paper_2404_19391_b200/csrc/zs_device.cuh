@@ -102,8 +102,27 @@ struct Ctl {                    // zeroed before every launch
     unsigned long long arena_used;
     unsigned long long overflow;   // output or arena capacity exceeded
     unsigned long long in_lines;   // lines seen (records in)
+    unsigned long long ll_n;       // long lines recorded (compress_cx, Job.ll_mode 0)
     unsigned long long phase[8];   // per-phase SM cycles (thread 0), when Job.timing
 };
+
+// A line longer than compress_cx's staged window ("long line", zs_ll.cuh):
+// recorded by compress_cx (ge), sorted by ge on the host, then coded by the
+// block-parallel long-line kernels before compress_cx runs again and takes
+// its output size from here.
+struct LLine {
+    long long ge;     // global offset of the terminating '\n' (n: the virtual one at EOF)
+    long long gs;     // global offset of the first byte
+    long long obase;  // output bytes (payload + '\n') in the long-line workspace
+    long long dst;    // output offset compress_cx reserved for the line; -1 = none
+    long long cost;   // payload bytes (without the '\n')
+    long long esc;    // escapes
+    int blk0, nblk;   // 256-byte blocks [blk0, blk0 + nblk) of the line
+    int ev0, nev;     // ring-token events [ev0, ev0 + nev) (preprocess)
+    int status;       // LL_OK, or LL_FALLBACK: the general routine codes the line
+    int pad;
+};
+enum : int { LL_OK = 0, LL_FALLBACK = 1 };
 
 struct TileState {
     unsigned int flag;
@@ -131,6 +150,12 @@ struct Job {
     uint8_t *arena;
     long long arena_cap;
     int timing;  // accumulate per-phase clock64 deltas into Ctl.phase
+    // long lines (compress_cx): mode 0 records them in `ll` (up to ll_cap) and
+    // flags Ctl.overflow bit 16; mode 1 takes the coded ones from `ll` (ll_n
+    // entries sorted by ge); mode 2 codes every line in the kernel
+    LLine *ll = nullptr;
+    long long *tl = nullptr;  // per tile: global offset of its last '\n', -1 = none
+    int ll_mode = 2, ll_n = 0, ll_cap = 0;
 };
 
 // Phase clocks and the other measurement hooks are compiled in only with
