@@ -3,6 +3,7 @@
     python -m paper_2404_19391_b200.build [--force]
 """
 
+import glob
 import os
 import subprocess
 import sys
@@ -10,8 +11,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "zs_api.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("zs_api.cu", "zs_kernels.cuh", "zs_device.cuh", "zs_fx.cuh", "zs_cx.cuh", "zs_ix.cuh", "zs_train.cuh")] + \
-       [os.path.join(ROOT, "include", f) for f in ("zs.h", "zs_debug.h")]
+# every source and header of the library (a new header is a dependency without listing it)
+DEPS = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")) + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) +
+              glob.glob(os.path.join(ROOT, "include", "*.h")))
 OUT = os.path.join(HERE, "libzs.so")
 # measurement build: per-phase clocks compiled in (tools/phase_cx.py loads it via ZS_LIB)
 OUT_PHASES = os.path.join(HERE, "libzs_phases.so")

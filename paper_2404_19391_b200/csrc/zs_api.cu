@@ -14,6 +14,7 @@
 #include <set>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
 #include <cstdlib>
 #include <functional>
 #include <string>
@@ -133,6 +134,7 @@ struct zs_ctx {
     // long lines (zs_ll.cuh) per slot: the recorded lines, the tiles' last
     // newlines, per-block arrays, events, renumbered lines, decisions, output
     DevBuf ll[NSLOT], tl[NSLOT], llb[NSLOT], lle[NSLOT], llc[NSLOT], llr[NSLOT], lld[NSLOT], llo[NSLOT];
+    DevBuf d_lltok;  // long-line tokenizer tables
     int no_ll = 0;  // debug: long lines on the general routine (one thread each)
     DevBuf ixs;     // record-index scratch
     // dictionary training (zs_train.cuh): corpus, census scratch, rank table, selection state
@@ -749,7 +751,8 @@ BatchKernel batch_kernel(int w) {
 }
 
 // one whole-buffer launch (device pointers) on `slot`'s buffers and stream
-int run_ll(zs_ctx *ctx, int slot, const uint8_t *d_in, long long nt, int flags, int *n_ll_out, int *launches);
+int run_ll(zs_ctx *ctx, int slot, const uint8_t *d_in, long long n_in, long long nt, int flags, int *n_ll_out,
+           int *launches);
 
 int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, long long n,
                   uint8_t *d_out, long long out_cap, int flags, bool timed, bool general = false,
@@ -790,7 +793,7 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
         if (ctx->ll[slot].reserve(sizeof(LLine) * LL_CAP) || ctx->tl[slot].reserve(sizeof(long long) * nt))
             return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(long lines)");
         if (ll) {
-            if (int rc = run_ll(ctx, slot, d_in, nt, flags, &ll_n, &ll_launches)) return rc;
+            if (int rc = run_ll(ctx, slot, d_in, n, nt, flags, &ll_n, &ll_launches)) return rc;
         }
         job.ll = ctx->ll[slot].as<LLine>();
         job.tl = ctx->tl[slot].as<long long>();
@@ -815,7 +818,7 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
                 k<<<g2, CX_NT, smem, st>>>(job, ctx->tb, ct);
                 ctx->last_kernel = ctx->slices ? "compress_cx<slices>" : "compress_cx";
                 if (ll && ll_n > 0) {  // the coded long lines to the offsets compress_cx reserved
-                    ll_place<<<dim3(ll_n, 64), LL_NT, 0, st>>>(job.ll, ll_n, ctx->llo[slot].as<uint8_t>(),
+                    ll_place<<<dim3(ll_n, 512), LL_NT, 0, st>>>(job.ll, ll_n, ctx->llo[slot].as<uint8_t>(),
                                                               d_out, out_cap);
                     ++ll_launches;
                     static const bool trace = getenv("ZS_LL_TRACE") != nullptr;
@@ -894,16 +897,24 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
 // stream; the host reads back the few sizes it allocates by.  On return the
 // slot's line list holds, sorted by ge, every recorded line with its output
 // size (or LL_FALLBACK) for compress_cx's mode 1.
-int run_ll(zs_ctx *ctx, int slot, const uint8_t *d_in, long long nt, int flags, int *n_ll_out, int *launches) {
+int run_ll(zs_ctx *ctx, int slot, const uint8_t *d_in, long long n_in, long long nt, int flags, int *n_ll_out,
+           int *launches) {
     cudaStream_t st = ctx->stream[slot];
     const int n_ll = (int)std::min<unsigned long long>(ctx->h_ctl[slot].ll_n, (unsigned long long)LL_CAP);
     *n_ll_out = n_ll;
     if (n_ll == 0) return ZS_OK;
     LLine *d_ln = ctx->ll[slot].as<LLine>();
     std::vector<LLine> L(n_ll);
+    // ZS_LL_TRACE: host time at each round trip (a measurement aid)
+    static const bool trace = getenv("ZS_LL_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    int trips = 0;
     auto d2h = [&](void *dst, const void *src, size_t bytes) -> int {
         CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        if (trace)
+            fprintf(stderr, "zs_ll trip %d at %.1f us\n", ++trips,
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
         return ZS_OK;
     };
     if (int rc = d2h(L.data(), d_ln, sizeof(LLine) * n_ll)) return rc;
@@ -945,12 +956,13 @@ int run_ll(zs_ctx *ctx, int slot, const uint8_t *d_in, long long nt, int flags, 
     const bool pre = (flags & ZS_F_PREPROCESS) != 0;
     if (ctx->llb[slot].reserve(a4 * 10 + nb1 * 16 + 64) ||
         (pre && (ctx->lle[slot].reserve(2 * e4 + e2 + ne + 64) ||
-                 ctx->llc[slot].reserve(nseg * (LL_NCOL + 1) * 8))) ||
+                 ctx->llc[slot].reserve(nseg * LL_CS * 8))) ||
         ctx->llr[slot].reserve(rcap) || ctx->lld[slot].reserve(rcap) || ctx->llo[slot].reserve(ocap))
         return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(long lines)");
     uint8_t *pb = ctx->llb[slot].as<uint8_t>();
     LLWork W{};
     W.in = d_in;
+    W.n = n_in;
     W.ln = d_ln;
     W.n_ll = n_ll;
     W.nb = nb;
@@ -975,7 +987,7 @@ int run_ll(zs_ctx *ctx, int slot, const uint8_t *d_in, long long nt, int flags, 
         W.ecol = pe + 2 * e4 + e2;
     }
     int *exits = pre ? ctx->llc[slot].as<int>() : nullptr;
-    int *assumed = pre ? exits + nseg * (LL_NCOL + 1) : nullptr;
+    int *assumed = pre ? exits + nseg * LL_CS : nullptr;
     W.R = ctx->llr[slot].as<uint8_t>();
     W.D = ctx->lld[slot].as<uint8_t>();
     W.O = ctx->llo[slot].as<uint8_t>();
@@ -983,6 +995,13 @@ int run_ll(zs_ctx *ctx, int slot, const uint8_t *d_in, long long nt, int flags, 
     W.cmap = ctx->d_pacmap.as<uint8_t>();
     W.pa_words = ctx->ht.pa_states * ctx->ht.pa_cols;
     W.explen = ctx->tb.exp_len;
+    if (!ctx->d_lltok.p) {
+        LLTok T;
+        ll_tok_build(T);
+        if (ctx->d_lltok.reserve(sizeof T)) return fail(ctx, cudaErrorMemoryAllocation, "cudaMalloc(tokenizer)");
+        CK(cudaMemcpy(ctx->d_lltok.p, &T, sizeof T, cudaMemcpyHostToDevice));
+    }
+    W.tok = ctx->d_lltok.as<LLTok>();
     const int gb = (nb + LL_NT - 1) / LL_NT;
     const int gseg = (int)((nseg + LL_NT - 1) / LL_NT);
     const int pa_smem = W.pa_words * 4;
@@ -1028,8 +1047,11 @@ int run_ll(zs_ctx *ctx, int slot, const uint8_t *d_in, long long nt, int flags, 
         // ne - 1 = the events bound; ll_pair / ll_colour stop at the real count
         ll_pair<<<(int)((ne - 1 + LL_NT - 1) / LL_NT), LL_NT, 0, st>>>(W, (int)(ne - 1));
         nk += 7;
+        if (int rc = colour_pass(0)) return rc;
+        ll_umin<<<1, LL_SNT, 0, st>>>(W, (int)(ne - 1), assumed);
+        ++nk;
         for (int pass = 0; pass < 3; ++pass)
-            if (int rc = colour_pass(pass)) return rc;
+            if (int rc = colour_pass(1)) return rc;
     } else {
         ll_tok_map<false><<<gb, LL_NT, 0, st>>>(W);
         ++nk;

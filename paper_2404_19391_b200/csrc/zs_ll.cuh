@@ -48,7 +48,7 @@
 namespace zs {
 
 constexpr int LL_B = 256;        // bytes of the original line per block
-constexpr int LL_NT = 256;       // threads per CTA of the per-block kernels
+constexpr int LL_NT = 128;       // threads per CTA of the per-block kernels (small CTAs: a MB line fills the SMs)
 constexpr int LL_SNT = 1024;     // the scan CTA
 constexpr int LL_CAP = 32768;    // long lines per launch
 constexpr long long LL_MAXBYTES = 1ll << 28;  // long-line bytes per launch (beyond: general routine; keeps offsets 32-bit)
@@ -56,6 +56,7 @@ constexpr int LL_WARM = 8;       // parse warm-up bytes of a guessed entry
 
 struct LLWork {
     const uint8_t *in;
+    long long n;            // input bytes (reads stay inside [in, in + n))
     LLine *ln;
     int n_ll;
     int nb;                 // blocks
@@ -84,6 +85,59 @@ struct LLWork {
     const uint8_t *cmap;
     int pa_words;
     const uint8_t *explen;
+    const struct LLTok *tok;  // tokenizer tables (ll_tok_build)
+};
+
+// Sequential byte reads (either direction) through aligned 16-byte loads: a
+// thread walks its block's bytes in registers instead of one L2 request per
+// byte.  A 16-byte chunk that is not inside [lo, hi) is read bytewise.
+struct LLRd {
+    uintptr_t lo, hi, ck = ~(uintptr_t)0;
+    uint4 v;
+    __device__ LLRd(const void *lo_, const void *hi_)
+        : lo(reinterpret_cast<uintptr_t>(lo_)), hi(reinterpret_cast<uintptr_t>(hi_)) {}
+    __device__ __forceinline__ unsigned operator()(const uint8_t *p) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(p), c = a & ~(uintptr_t)15;
+        if (c != ck) {
+            if (c < lo || c + 16 > hi) return *p;
+            v = __ldg(reinterpret_cast<const uint4 *>(c));
+            ck = c;
+        }
+        const unsigned k = (unsigned)(a & 15);
+        const unsigned w = k < 8 ? (k < 4 ? v.x : v.y) : (k < 12 ? v.z : v.w);
+        return (w >> (8 * (k & 3))) & 0xffu;
+    }
+};
+// workspace buffers carry slack past their last byte: no upper bound needed
+__device__ __forceinline__ LLRd ll_rd(const uint8_t *base) {
+    return LLRd(base, reinterpret_cast<const void *>(~(uintptr_t)0 >> 1));
+}
+
+// Sequential byte writes (either direction): a whole 4-byte word leaves with
+// one store; the partial words at the ends of a thread's range go byte by
+// byte (the neighbouring threads own their other bytes).
+struct LLWr {
+    uintptr_t wd = 0;
+    unsigned val = 0, mask = 0;
+    __device__ __forceinline__ void flush() {
+        if (mask == 0xfu) {
+            *reinterpret_cast<unsigned *>(wd) = val;
+        } else if (mask) {
+            for (int k = 0; k < 4; ++k)
+                if ((mask >> k) & 1u) reinterpret_cast<uint8_t *>(wd)[k] = (uint8_t)(val >> (8 * k));
+        }
+        mask = val = 0;
+    }
+    __device__ __forceinline__ void put(uint8_t *p, unsigned b) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(p), w = a & ~(uintptr_t)3;
+        if (w != wd) {
+            flush();
+            wd = w;
+        }
+        const unsigned k = (unsigned)(a & 3);
+        val |= (b & 0xffu) << (8 * k);
+        mask |= 1u << k;
+    }
 };
 
 __device__ __forceinline__ int ll_line_of(const LLine *ln, int n_ll, int b) {
@@ -212,17 +266,23 @@ struct LLTok {
     unsigned lo[256], hi[256];
     uint8_t e[8 * 256];
 };
-__device__ __forceinline__ void ll_tok_init(LLTok &T) {
-    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+// host: the tables from tk_entry
+inline void ll_tok_build(LLTok &T) {
+    for (int b = 0; b < 256; ++b) {
         unsigned lo = 0, hi = 0;
-        for (int s = 0; s < 4; ++s) {
-            lo |= (unsigned)(tk_entry(s, b) & 7u) << (8 * s);
-            hi |= (unsigned)(tk_entry(s + 4, b) & 7u) << (8 * s);
+        for (int q = 0; q < 4; ++q) {
+            lo |= (unsigned)(tk_entry(q, b) & 7u) << (8 * q);
+            hi |= (unsigned)(tk_entry(q + 4, b) & 7u) << (8 * q);
         }
         T.lo[b] = lo;
         T.hi[b] = hi;
     }
-    for (int k = threadIdx.x; k < 8 * 256; k += blockDim.x) T.e[k] = tk_entry(k >> 8, k & 255);
+    for (int k = 0; k < 8 * 256; ++k) T.e[k] = tk_entry(k >> 8, k & 255);
+}
+__device__ __forceinline__ void ll_tok_init(LLTok &T, const LLTok *g) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(g);
+    uint4 *dst = reinterpret_cast<uint4 *>(&T);
+    for (int k = threadIdx.x; k < (int)(sizeof(LLTok) / 16); k += blockDim.x) dst[k] = src[k];
     __syncthreads();
 }
 
@@ -231,16 +291,17 @@ __device__ __forceinline__ void ll_tok_init(LLTok &T) {
 // state); any '\r' sends the line to the general routine
 template <bool PRE>
 __global__ void __launch_bounds__(LL_NT) ll_tok_map(LLWork W) {
-    __shared__ LLTok T;
-    if (PRE) ll_tok_init(T);
+    __shared__ __align__(16) LLTok T;
+    if (PRE) ll_tok_init(T, W.tok);
     const int b = blockIdx.x * LL_NT + threadIdx.x;
     if (b >= W.nb) return;
     const LLBlk k = ll_blk(W, b);
     LLine &L = W.ln[k.line];
     const uint8_t *s = W.in + L.gs + k.off;
+    LLRd rd(W.in, W.in + W.n);
     unsigned v = 0x76543210u, cr = 0;
     for (int i = 0; i < k.len; ++i) {
-        const unsigned c = __ldg(s + i);
+        const unsigned c = rd(s + i);
         cr |= c == '\r';
         if (PRE) v = ll_apply(T.lo[c], T.hi[c], v);
     }
@@ -256,19 +317,19 @@ __device__ __forceinline__ unsigned ll_entry_state(const LLWork &W, const LLBlk 
 }
 
 // ring id of the token at s[i] ('%nn' or a digit); bounded by the line
-__device__ __forceinline__ unsigned ll_ring_id(const uint8_t *s, int i, long long rem, bool &pct) {
-    const unsigned c = __ldg(s + i);
+__device__ __forceinline__ unsigned ll_ring_id(LLRd &rd, const uint8_t *s, int i, long long rem, bool &pct) {
+    const unsigned c = rd(s + i);
     pct = c == '%';
     if (!pct) return c - '0';
-    const unsigned d1 = rem > 1 ? __ldg(s + i + 1) : '0', d2 = rem > 2 ? __ldg(s + i + 2) : '0';
+    const unsigned d1 = rem > 1 ? rd(s + i + 1) : '0', d2 = rem > 2 ? rd(s + i + 2) : '0';
     return (d1 - '0') * 10u + (d2 - '0');
 }
 
 // ring tokens per block and the XOR parity of their ids; a tokenize error
 // (a '%' without two digits is sticky, an open bracket at the end) -> fallback
 __global__ void __launch_bounds__(LL_NT) ll_tok_count(LLWork W) {
-    __shared__ LLTok T;
-    ll_tok_init(T);
+    __shared__ __align__(16) LLTok T;
+    ll_tok_init(T, W.tok);
     const int b = blockIdx.x * LL_NT + threadIdx.x;
     if (b >= W.nb) return;
     const LLBlk k = ll_blk(W, b);
@@ -278,12 +339,13 @@ __global__ void __launch_bounds__(LL_NT) ll_tok_count(LLWork W) {
     unsigned st = ll_entry_state(W, k, b);
     int cnt = 0;
     uint4 par = make_uint4(0, 0, 0, 0);
+    LLRd rd(W.in, W.in + W.n);
     for (int i = 0; i < k.len; ++i) {
-        const unsigned e = T.e[(st << 8) | __ldg(s + i)];
+        const unsigned e = T.e[(st << 8) | rd(s + i)];
         st = e & 7u;
         if (e & TK_RING) {
             bool pct;
-            unsigned id = ll_ring_id(s, i, len - k.off - i, pct);
+            unsigned id = ll_ring_id(rd, s, i, len - k.off - i, pct);
             if (id >= 100) id = 0;  // (a malformed '%' token: the line falls back)
             const unsigned bit = 1u << (id & 31);
             if (id < 32) par.x ^= bit;
@@ -306,8 +368,8 @@ __device__ __forceinline__ unsigned ll_par_bit(const uint4 &p, unsigned id) {
 // events of the block: line position, flags (id, '%nn', opens); an odd id
 // count over the line (an unpaired ring) -> fallback
 __global__ void __launch_bounds__(LL_NT) ll_tok_events(LLWork W) {
-    __shared__ LLTok T;
-    ll_tok_init(T);
+    __shared__ __align__(16) LLTok T;
+    ll_tok_init(T, W.tok);
     const int b = blockIdx.x * LL_NT + threadIdx.x;
     if (b >= W.nb) return;
     const LLBlk k = ll_blk(W, b);
@@ -322,12 +384,13 @@ __global__ void __launch_bounds__(LL_NT) ll_tok_events(LLWork W) {
         L.nev = W.cnt[L.blk0 + L.nblk] - ev;
     }
     unsigned st = ll_entry_state(W, k, b);
+    LLRd rd(W.in, W.in + W.n);
     for (int i = 0; i < k.len; ++i) {
-        const unsigned e = T.e[(st << 8) | __ldg(s + i)];
+        const unsigned e = T.e[(st << 8) | rd(s + i)];
         st = e & 7u;
         if (e & TK_RING) {
             bool pct;
-            unsigned id = ll_ring_id(s, i, len - k.off - i, pct);
+            unsigned id = ll_ring_id(rd, s, i, len - k.off - i, pct);
             if (id >= 100) id = 0;  // (a malformed '%' token: the line falls back)
             const unsigned open = ll_par_bit(par, id) ^ 1u;
             if (id < 32) par.x ^= 1u << id;
@@ -362,16 +425,27 @@ __global__ void __launch_bounds__(LL_NT) ll_pair(LLWork W, int n_bound) {
 
 // Colouring (smiles.py:163-183): rings in closing order, each the smallest
 // colour k with lc[k] (the event index of k's latest close) < its opening
-// event.  The events are cut into segments of LL_SEG, one thread each, and a
-// segment's incoming lc[] is a guess (no closes: exact at a line start) that
-// later passes check: a segment reads its left neighbour's exit, keeps only
-// the entries its own crossing rings can see (a close after the earliest
-// opening, before the segment, of a ring that closes in it; older entries act
-// as "free"), and runs again if that differs from what it assumed; a pass in
-// which no exit changed ends the iteration.  Colour 100 (RingIdOverflow)
-// marks the ring 0xff and its line falls back (ll_rlen).
-constexpr int LL_SEG = 512;
+// event.  The events are cut into segments of LL_SEG, one thread each; a
+// segment enters with a guessed lc[] (no closes: exact at a line start) and
+// later passes check it against the left neighbour's exit:
+//  * the segment's colours read the incoming lc[] only through its crossing
+//    rings (closing in it, opened before it): entries older than the earliest
+//    such opening u act as "free", so the incoming state normalised at u
+//    decides whether the segment runs again;
+//  * its exit is its own last closes for the colours it touched after its
+//    last line start, and the incoming entries for the others (no line start
+//    in it), so a neighbour's changed entries pass through without a re-run;
+//    exits are normalised at U (the earliest crossing-ring opening of all
+//    later segments, ll_umin), below which no later segment looks, so old
+//    entries stop travelling.
+// A pass in which no exit changed ends the iteration.  Colour 100
+// (RingIdOverflow) marks the ring 0xff; its line falls back (ll_rlen).
+constexpr int LL_SEG = 128;
 constexpr int LL_NCOL = 100;
+// ints per segment.  exits: lc[100], n (entries from n on are -1);
+// assumed: lc[100] (normalised at u), u, head, touched[4], U, n
+constexpr int LL_CS = 112;
+enum : int { LLC_N = 100, LLC_U = 100, LLC_HEAD = 101, LLC_T = 102, LLC_UU = 106, LLC_AN = 107 };
 
 __global__ void __launch_bounds__(LL_NT) ll_colour(LLWork W, int n_bound, int pass, int *exits, int *assumed) {
     const int sg = blockIdx.x * LL_NT + threadIdx.x;
@@ -379,50 +453,171 @@ __global__ void __launch_bounds__(LL_NT) ll_colour(LLWork W, int n_bound, int pa
     const int n_ev = min(n_bound, W.cnt[W.nb]);
     if (a >= n_ev) return;
     const int b = min(n_ev, a + LL_SEG);
-    // exits / assumed: LL_NCOL + 1 ints per segment (assumed[LL_NCOL] = u)
-    int *ex = exits + (size_t)sg * (LL_NCOL + 1), *as = assumed + (size_t)sg * (LL_NCOL + 1);
-    int lc[LL_NCOL];
-    if (pass == 0) {
-        for (int k = 0; k < LL_NCOL; ++k) lc[k] = -1;
-        for (int k = 0; k < LL_NCOL; ++k) as[k] = -1;
-        // the earliest opening before the segment among the rings closing in
-        // it up to its first line start (a: none, the incoming state is
-        // never read)
-        int u = a;
-        for (int e = a; e < b && !(W.eflag[e] & 0x200u); ++e) {
-            const int o = W.epart[e];
-            if (o >= 0) u = min(u, o);
-        }
-        as[LL_NCOL] = u;
-    } else {
-        const int u = as[LL_NCOL];
-        if (u == a) return;  // starts a line or has no crossing ring: exact since pass 0
-        const int *prev = exits + (size_t)(sg - 1) * (LL_NCOL + 1);
+    int *ex = exits + (size_t)sg * LL_CS, *as = assumed + (size_t)sg * LL_CS;
+    // lc: colours 0-7 in registers, the rest in local memory; entries from
+    // nc on are -1
+    int lr[8], lm[LL_NCOL - 8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) lr[j] = -1;
+    int nc = 0;
+    auto get = [&](int k) {
+        if (k >= 8) return lm[k - 8];
+        int v = -1;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v = k == j ? lr[j] : v;
+        return v;
+    };
+    auto set = [&](int k, int v) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) lr[j] = k == j ? v : lr[j];
+        if (k >= 8) lm[k - 8] = v;
+    };
+    const int U = pass > 0 ? as[LLC_UU] : -1;  // (pass 0: U is not known yet)
+    if (pass > 0) {
+        const int u = as[LLC_U], an = as[LLC_AN];
+        const int *prev = exits + (size_t)(sg - 1) * LL_CS;
+        const int pn = u < a || !as[LLC_HEAD] ? *(volatile const int *)&prev[LLC_N] : 0;
+        auto pv = [&](int k) { return k < pn ? *(volatile const int *)&prev[k] : -1; };
         bool same = true;
-        for (int k = 0; k < LL_NCOL; ++k) {
-            const int v = *(volatile const int *)&prev[k];
-            lc[k] = v > u ? v : -1;
-            same &= lc[k] == as[k];
+        if (u < a)
+            for (int k = 0; k < max(pn, an); ++k) {
+                const int v = pv(k);
+                same &= (v > u ? v : -1) == (k < an ? as[k] : -1);
+            }
+        if (same) {
+            // colours unchanged: the exit is the own closes (touched colours,
+            // or every colour after a line start) and the incoming entries
+            const bool head = as[LLC_HEAD] != 0;
+            const int en = ex[LLC_N], n = head ? en : max(en, pn);
+            bool diff = false;
+            for (int k = 0; k < n; ++k) {
+                const bool own = head || ((as[LLC_T + (k >> 5)] >> (k & 31)) & 1);
+                const int v0 = own ? (k < en ? ex[k] : -1) : pv(k);
+                const int v = v0 > U ? v0 : -1;
+                diff |= (k < en ? ex[k] : -1) != v;
+                ex[k] = v;
+            }
+            if (n != en) ex[LLC_N] = n;
+            if (diff) *W.changed = 1;
+            return;
         }
-        if (same) return;
-        for (int k = 0; k < LL_NCOL; ++k) as[k] = lc[k];
+        for (int k = 0; k < pn; ++k) {
+            const int v = pv(k);
+            set(k, v);
+            as[k] = v > u ? v : -1;
+        }
+        nc = pn;
+        as[LLC_AN] = pn;
     }
-    for (int e = a; e < b; ++e) {
-        if (W.eflag[e] & 0x200u)
-            for (int k = 0; k < LL_NCOL; ++k) lc[k] = -1;
-        const int o = W.epart[e];
-        if (o < 0) continue;  // opens a ring
-        int k = 0;
-        while (k < LL_NCOL && lc[k] > o) ++k;
-        if (k < LL_NCOL) lc[k] = e;
-        W.ecol[e] = W.ecol[o] = (uint8_t)(k < LL_NCOL ? k : 0xff);
+    // the walk, 16 events per step from vector loads; pass 0 also finds u:
+    // the earliest opening before the segment among the rings closing in it
+    // up to its first line start (a: none)
+    unsigned t0 = 0, t1 = 0, t2 = 0, t3 = 0, head = 0;  // colours touched since the last line start
+    int u = a;
+    for (int base = a; base < b; base += 16) {
+        uint16_t fl[16];
+        int pt[16];
+        if (base + 16 <= b) {
+            const uint4 f0 = *reinterpret_cast<const uint4 *>(W.eflag + base);
+            const uint4 f1 = *reinterpret_cast<const uint4 *>(W.eflag + base + 8);
+            const unsigned fw[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+#pragma unroll
+            for (int j = 0; j < 16; ++j) fl[j] = (uint16_t)(fw[j >> 1] >> (16 * (j & 1)));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int4 v = *reinterpret_cast<const int4 *>(W.epart + base + 4 * q);
+                pt[4 * q] = v.x;
+                pt[4 * q + 1] = v.y;
+                pt[4 * q + 2] = v.z;
+                pt[4 * q + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                fl[j] = base + j < b ? W.eflag[base + j] : 0;
+                pt[j] = base + j < b ? W.epart[base + j] : -1;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int e = base + j;
+            if (e >= b) break;
+            if (fl[j] & 0x200u) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) lr[q] = -1;
+                nc = 0;
+                t0 = t1 = t2 = t3 = 0;
+                head = 1;
+            }
+            const int o = pt[j];
+            if (o < 0) continue;  // opens a ring
+            if (!head) u = min(u, o);
+            int k = 8;
+#pragma unroll
+            for (int q = 7; q >= 0; --q) k = lr[q] < o ? q : k;  // (lr[q] = -1 beyond nc: free)
+            if (k == 8) {
+                while (k < nc && lm[k - 8] > o) ++k;
+                if (k == nc && nc < LL_NCOL) lm[k - 8] = -1;
+            }
+            nc = max(nc, min(k + 1, LL_NCOL));
+            if (k < LL_NCOL) {
+                set(k, e);
+                const unsigned bit = 1u << (k & 31);
+                if (k < 32) t0 |= bit;
+                else if (k < 64) t1 |= bit;
+                else if (k < 96) t2 |= bit;
+                else t3 |= bit;
+            }
+            W.ecol[e] = W.ecol[o] = (uint8_t)(k < LL_NCOL ? k : 0xff);
+        }
     }
+    if (pass == 0) {
+        as[LLC_U] = u;
+        as[LLC_AN] = 0;
+    }
+    as[LLC_HEAD] = (int)head;
+    as[LLC_T] = (int)t0;
+    as[LLC_T + 1] = (int)t1;
+    as[LLC_T + 2] = (int)t2;
+    as[LLC_T + 3] = (int)t3;
+    const int en = pass > 0 ? ex[LLC_N] : 0;
     bool diff = false;
-    for (int k = 0; k < LL_NCOL; ++k) {
-        diff |= ex[k] != lc[k];
-        ex[k] = lc[k];
+    for (int k = 0; k < max(nc, en); ++k) {
+        const int g = k < nc ? get(k) : -1;
+        const int v = g > U ? g : -1;
+        diff |= (k < en ? ex[k] : -1) != v;
+        ex[k] = v;
     }
+    ex[LLC_N] = max(nc, en);
     if (pass > 0 && diff) *W.changed = 1;
+}
+
+// U of every segment: the minimum u of the segments after it (unsegmented:
+// a later line's u lies past every event of this line, which then all
+// normalise away, as they may); one CTA
+__global__ void __launch_bounds__(LL_SNT) ll_umin(LLWork W, int n_bound, int *assumed) {
+    __shared__ int s[LL_SNT];
+    const int n_ev = min(n_bound, W.cnt[W.nb]);
+    const int nseg = (n_ev + LL_SEG - 1) / LL_SEG;
+    const int tid = threadIdx.x;
+    const int per = (nseg + LL_SNT - 1) / LL_SNT;
+    const int lo = min(nseg, tid * per), hi = min(nseg, lo + per);
+    int m = 0x7fffffff;
+    for (int k = lo; k < hi; ++k) m = min(m, assumed[(size_t)k * LL_CS + LLC_U]);
+    s[tid] = m;
+    __syncthreads();
+    for (int d = 1; d < LL_SNT; d <<= 1) {  // inclusive suffix min over the chunk minima
+        int v = s[tid];
+        if (tid + d < LL_SNT) v = min(v, s[tid + d]);
+        __syncthreads();
+        s[tid] = v;
+        __syncthreads();
+    }
+    int run = tid + 1 < LL_SNT ? s[tid + 1] : 0x7fffffff;  // min over the chunks after this one
+    for (int k = hi - 1; k >= lo; --k) {
+        assumed[(size_t)k * LL_CS + LLC_UU] = run;
+        run = min(run, assumed[(size_t)k * LL_CS + LLC_U]);
+    }
 }
 
 // ---------------------------------------------------------------- rewrite
@@ -468,28 +663,32 @@ __global__ void __launch_bounds__(LL_NT) ll_rewrite(LLWork W) {
     if (L.status != LL_OK) return;
     const uint8_t *s = W.in + L.gs;
     uint8_t *o = W.R + W.rlen[b];
+    LLRd rd(W.in, W.in + W.n);
+    LLWr wr;
     int e = W.preprocess ? W.cnt[b] : 0;
     const int eb = W.preprocess ? W.cnt[b + 1] : 0;
     int p = k.off + (W.preprocess ? ll_skip(W, k, e) : 0);
     const int end = k.off + k.len;
+    int next = e < eb ? W.epos[e] : 0x7fffffff;
     while (p < end) {
-        if (e < eb && W.epos[e] == p) {
+        if (p == next) {
             const unsigned col = W.ecol[e];
             if (col < 10) {
-                *o++ = (uint8_t)('0' + col);
+                wr.put(o++, '0' + col);
             } else {
-                o[0] = '%';
-                o[1] = (uint8_t)('0' + col / 10);
-                o[2] = (uint8_t)('0' + col % 10);
-                o += 3;
+                wr.put(o++, '%');
+                wr.put(o++, '0' + col / 10);
+                wr.put(o++, '0' + col % 10);
             }
             p += (W.eflag[e] & 0x80u) ? 3 : 1;
             ++e;
+            next = e < eb ? W.epos[e] : 0x7fffffff;
         } else {
-            *o++ = __ldg(s + p);
+            wr.put(o++, rd(s + p));
             ++p;
         }
     }
+    wr.flush();
 }
 
 // ---------------------------------------------------------------- parse
@@ -512,15 +711,18 @@ __global__ void __launch_bounds__(LL_NT) ll_parse(LLWork W) {
     if (L.status != LL_OK) return;
     const int lo = W.rlen[b], hi = W.rlen[b + 1], lend = W.rlen[L.blk0 + L.nblk];
     unsigned st = 0;
+    LLRd rd = ll_rd(W.R);
     if (!k.last)  // guessed entry: warm-up from the line-end state
-        for (int p = min(hi + LL_WARM, lend) - 1; p >= hi; --p) st = s_pa[(st + s_cm[W.R[p]]) >> 2] & 0xffffu;
+        for (int p = min(hi + LL_WARM, lend) - 1; p >= hi; --p) st = s_pa[(st + s_cm[rd(W.R + p)]) >> 2] & 0xffffu;
     W.pin[b] = st;
+    LLWr wr;
     for (int p = hi - 1; p >= lo; --p) {
-        const unsigned c = W.R[p];
+        const unsigned c = rd(W.R + p);
         const unsigned e = s_pa[(st + s_cm[c]) >> 2];
         st = e & 0xffffu;
-        W.D[p] = (uint8_t)ll_dec(e, c);
+        wr.put(W.D + p, ll_dec(e, c));
     }
+    wr.flush();
     W.pout[b] = st;
 }
 
@@ -563,8 +765,9 @@ __global__ void __launch_bounds__(LL_NT) ll_parse_fix(LLWork W) {
 
 // ---------------------------------------------------------------- emit
 // one decision at p: output bytes (2 for an escape), positions covered
-__device__ __forceinline__ void ll_step(const LLWork &W, const uint8_t *xl, int &p, int &out, int &esc) {
-    const unsigned c = W.D[p];
+__device__ __forceinline__ void ll_step(const LLWork &W, LLRd &rd, const uint8_t *xl, int &p, int &out,
+                                        int &esc) {
+    const unsigned c = rd(W.D + p);
     if (c == 0x20u) {
         out += 2;
         ++esc;
@@ -589,7 +792,8 @@ __global__ void __launch_bounds__(LL_NT) ll_emit_count(LLWork W) {
     }
     const int lo = W.rlen[b], hi = W.rlen[b + 1];
     int p = lo, out = 0, esc = 0;  // guess: a decision starts at the block's first byte
-    while (p < hi) ll_step(W, xl, p, out, esc);
+    LLRd rd = ll_rd(W.D);
+    while (p < hi) ll_step(W, rd, xl, p, out, esc);
     W.g[b] = lo;
     W.x[b] = p;
     W.ocnt[b] = out + (k.last ? 1 : 0);  // the line's '\n'
@@ -612,9 +816,10 @@ __global__ void __launch_bounds__(LL_NT) ll_emit_fix(LLWork W) {
     if (truth == gp) return;
     const int hi = W.rlen[b + 1];
     int a = truth, da = 0, ea = 0, db = 0, eb = 0;
+    LLRd rd = ll_rd(W.D);
     while (a != gp && min(a, gp) < hi) {
-        if (a < gp) ll_step(W, xl, a, da, ea);
-        else ll_step(W, xl, gp, db, eb);
+        if (a < gp) ll_step(W, rd, xl, a, da, ea);
+        else ll_step(W, rd, xl, gp, db, eb);
     }
     W.ocnt[b] += da - db;
     W.oesc[b] += ea - eb;
@@ -637,19 +842,21 @@ __global__ void __launch_bounds__(LL_NT) ll_emit_write(LLWork W) {
     const int hi = W.rlen[b + 1];
     uint8_t *o = W.O + W.ooff[b];
     int p = W.g[b];
+    LLRd rdd = ll_rd(W.D), rdr = ll_rd(W.R);
+    LLWr wr;
     while (p < hi) {
-        const unsigned c = W.D[p];
+        const unsigned c = rdd(W.D + p);
         if (c == 0x20u) {
-            o[0] = 0x20;
-            o[1] = W.R[p];
-            o += 2;
+            wr.put(o++, 0x20);
+            wr.put(o++, rdr(W.R + p));
             ++p;
         } else {
-            *o++ = (uint8_t)c;
+            wr.put(o++, c);
             p += xl[c];
         }
     }
-    if (k.last) *o = '\n';
+    if (k.last) wr.put(o, '\n');
+    wr.flush();
     if (W.oesc[b]) atomicAdd((unsigned long long *)&L.esc, (unsigned long long)W.oesc[b]);
     if (k.head) {
         L.obase = W.ooff[b];
