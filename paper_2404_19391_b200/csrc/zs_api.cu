@@ -818,7 +818,7 @@ int launch_stream(zs_ctx *ctx, int slot, bool compress, const uint8_t *d_in, lon
                 k<<<g2, CX_NT, smem, st>>>(job, ctx->tb, ct);
                 ctx->last_kernel = ctx->slices ? "compress_cx<slices>" : "compress_cx";
                 if (ll && ll_n > 0) {  // the coded long lines to the offsets compress_cx reserved
-                    ll_place<<<dim3(ll_n, 512), LL_NT, 0, st>>>(job.ll, ll_n, ctx->llo[slot].as<uint8_t>(),
+                    ll_place<<<dim3(ll_n, std::max(1, std::min(512, 4096 / ll_n))), LL_NT, 0, st>>>(job.ll, ll_n, ctx->llo[slot].as<uint8_t>(),
                                                               d_out, out_cap);
                     ++ll_launches;
                     static const bool trace = getenv("ZS_LL_TRACE") != nullptr;
