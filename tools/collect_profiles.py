@@ -66,7 +66,7 @@ def main():
     dst = os.path.join(ROOT, "profiles", rnd)
     os.makedirs(dst, exist_ok=True)
     for f in ("bench.json", "bench_ref.json", "bench_c5.json", "gpu_tests.log", "smoke.log", "configs.json",
-              "train.json"):
+              "train.json", "ll_check.log"):
         if os.path.exists(os.path.join(OUT, f)):
             shutil.copy(os.path.join(OUT, f), os.path.join(dst, f))
     launches(dst)

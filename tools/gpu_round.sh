@@ -20,4 +20,5 @@ if [ $rc -eq 0 ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^fx_(count|emit)" -s 6 -c 2 \
     -o gpurun_out/full_decompress -f $CMD > gpurun_out/ncu_d.log 2>&1; echo ncu_decompress=$?
 fi
+timeout 900 python tools/ll_check.py > gpurun_out/ll_check.log 2>&1; echo ll=$?; tail -8 gpurun_out/ll_check.log
 timeout 1500 python tools/configs.py > gpurun_out/configs.json 2> gpurun_out/configs.err; echo configs=$?
