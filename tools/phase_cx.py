@@ -15,7 +15,7 @@ import paper_2404_19391_b200 as z  # noqa: E402
 from paper_2404_19391_b200 import _lib  # noqa: E402
 
 NAMES = ["load+cuts", "w0 tokenizer", "w0 pairing", "w0 parse", "wait slowest", "rare+scan", "emit+lookback", "store"]
-TILE = 29952
+TILE = 19968  # CX_TILE (zs_cx.cuh)
 
 
 def main():
