@@ -24,10 +24,12 @@ from paper_2404_19391_b200 import _lib  # noqa: E402
 ALPHA = b"CcNnOoSsFlBrI()[]=#-+@/\\\\%.:*$~123456789"
 
 
-def rand_line(rng):
+def rand_line(rng, long_ok=True):
     k = rng.random()
     if k < 0.05:
         return b""
+    if k < 0.055 and long_ok:  # a long line (the long-line kernels): molecules joined by '.'
+        return b".".join(rand_line(rng, False) for _ in range(rng.randint(100, 1500)))
     if k < 0.65:  # SMILES-like: molecules with ring closures, some %nn
         parts = []
         for _ in range(rng.randint(1, 4)):
@@ -80,7 +82,7 @@ def main():
         if rng.random() < 0.2:  # a real corpus slice
             lines = synth.generate(rng.choice(["mixed", "skewed"]), n_lines, rng.randint(1, 99)).tobytes().split(b"\n")[:-1]
         payload = b"\n".join(lines) + (b"\n" if rng.random() < 0.8 else b"")
-        mode = rng.choice([3, 3, 3, 19, 67, 131, 1])
+        mode = rng.choice([3, 3, 3, 19, 67, 131, 1, 3 | 256])
         pre, len_ = rng.random() < 0.7, rng.random() < 0.7
         ctx.lib.zs_set_transducer(ctx.h, mode)
         try:
