@@ -172,3 +172,31 @@ def test_long_line_device_api_and_decode_roundtrip():
     back, _ = z.run_buffer(np.frombuffer(want, np.uint8), d, "decompress")
     want_back, _ = oracle.run_stream(t, want, "decompress", False, False, 1)
     assert back.tobytes() == want_back
+
+
+def test_long_line_caps_fall_back():
+    """More long lines than one launch records (32768) and more long-line
+    bytes than it codes (256 MB): the rest take the general routine, in one
+    device call, and the output is still the reference's."""
+    import torch
+    from paper_2404_19391_b200 import _lib as L
+    d = z.default_dictionary()
+    rng = random.Random(8)
+    mols = synth.generate("mixed", 20000, 7).tobytes().split(b"\n")[:-1]
+    bases = [_long(mols, 22600 + 37 * k, rng) for k in range(4)]  # > the staged window: always long
+    payload = b"\n".join(bases[k % 4] for k in range(33000)) + b"\n"
+    assert len(payload) > (256 << 20)
+    t = oracle.Tables(d.learned, bytes(sorted(d.identity)))
+    want, st = oracle.run_stream(t, payload, "compress", True, True, 16)
+    buf = np.frombuffer(payload, np.uint8)
+    din = torch.from_numpy(buf.copy()).cuda()
+    dout = torch.empty(2 * buf.size + 64, dtype=torch.uint8, device="cuda")
+    ctx = L.context()
+    r = L.Result()
+    with ctx.lock:
+        ctx.set_dictionary(d)
+        rc = ctx.lib.zs_compress_device(ctx.h, din.data_ptr(), buf.size, dout.data_ptr(), dout.numel(),
+                                        L.F_PREPROCESS | L.F_LENIENT, r)
+        ctx.check(rc, "zs_compress_device")
+    assert r.lines == 33000 and r.lines == st["lines"]
+    assert dout[:r.out_bytes].cpu().numpy().tobytes() == want
