@@ -1,9 +1,9 @@
 // zs_cx.cuh -- lane-chunk compress kernel (the encode hot path).
 //
-// One persistent 768-thread CTA per SM takes 50,688-byte tiles in ticket
+// Three persistent 256-thread CTAs per SM take 19,968-byte tiles in ticket
 // order.  A tile owns the lines whose terminating '\n' lies inside it (their
 // first bytes may sit in the 2 KB staged before the tile).  Every lane owns
-// a contiguous run of whole lines, ~100 bytes, cut at the newline nearest to
+// a contiguous run of whole lines, ~78 bytes, cut at the newline nearest to
 // its chunk boundary, and walks it in straight loops that all lanes of a
 // warp execute in lock step (no per-line queues, sorting or barriers):
 //
@@ -15,9 +15,10 @@
 //       events: open rings in 4 register slots, colours 0-9 from per-colour
 //       last-close positions; '%nn' lines are compacted in place with the
 //       freed bytes left as a gap of escape-only filler before the '\n'
-//   --  rare lines (drops, strict errors, lines the fast path cannot renumber,
-//       lines longer than the staged window) are rewritten to escape-only
-//       filler and handled by one thread each (general routine, HBM arena)
+//   --  rare lines (drops, strict errors, lines the fast path cannot renumber)
+//       are rewritten to escape-only filler and handled by one thread each
+//       (general routine, HBM arena); lines longer than the staged window are
+//       recorded for the long-line kernels (zs_ll.cuh) and placed by them
 //   P4  min-cost parse right to left across the lane's lines
 //       (numba_impl.py:32-56): per byte one AC-DFA lookup and one lookup in
 //       the cost-window transducer; '\n' is a DFA column whose transducer
