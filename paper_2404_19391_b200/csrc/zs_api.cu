@@ -1002,6 +1002,9 @@ int run_ll(zs_ctx *ctx, int slot, const uint8_t *d_in, long long n_in, long long
         CK(cudaMemcpy(ctx->d_lltok.p, &T, sizeof T, cudaMemcpyHostToDevice));
     }
     W.tok = ctx->d_lltok.as<LLTok>();
+    W.ecap = pre ? (long long)ne : 0;
+    W.rcap = (long long)rcap;
+    W.ocap = (long long)ocap;
     const int gb = (nb + LL_NT - 1) / LL_NT;
     const int gseg = (int)((nseg + LL_NT - 1) / LL_NT);
     const int pa_smem = W.pa_words * 4;

@@ -86,6 +86,7 @@ struct LLWork {
     int pa_words;
     const uint8_t *explen;
     const struct LLTok *tok;  // tokenizer tables (ll_tok_build)
+    long long ecap, rcap, ocap;  // events, R / D bytes, O bytes allocated (ZS_CHECKS asserts)
 };
 
 // Sequential byte reads (either direction) through aligned 16-byte loads: a
@@ -397,6 +398,7 @@ __global__ void __launch_bounds__(LL_NT) ll_tok_events(LLWork W) {
             else if (id < 64) par.y ^= 1u << (id - 32);
             else if (id < 96) par.z ^= 1u << (id - 64);
             else par.w ^= 1u << (id - 96);
+            ZS_ASSERT(ev < W.ecap);
             W.epos[ev] = k.off + i;
             W.eflag[ev] = (uint16_t)(id | (pct ? 0x80u : 0u) | (open << 8) | (ev == line_ev0 ? 0x200u : 0u));
             ++ev;
@@ -551,6 +553,7 @@ __global__ void __launch_bounds__(LL_NT) ll_colour(LLWork W, int n_bound, int pa
             }
             const int o = pt[j];
             if (o < 0) continue;  // opens a ring
+            ZS_ASSERT(o < e);
             if (!head) u = min(u, o);
             int k = 8;
 #pragma unroll
@@ -688,6 +691,7 @@ __global__ void __launch_bounds__(LL_NT) ll_rewrite(LLWork W) {
             ++p;
         }
     }
+    ZS_ASSERT(o - W.R <= W.rcap && (int)(o - W.R) == W.rlen[b + 1]);
     wr.flush();
 }
 
@@ -856,6 +860,7 @@ __global__ void __launch_bounds__(LL_NT) ll_emit_write(LLWork W) {
         }
     }
     if (k.last) wr.put(o, '\n');
+    ZS_ASSERT(o + (k.last ? 1 : 0) - W.O == W.ooff[b + 1] && o - W.O < W.ocap);
     wr.flush();
     if (W.oesc[b]) atomicAdd((unsigned long long *)&L.esc, (unsigned long long)W.oesc[b]);
     if (k.head) {
