@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
     __shared__ unsigned long long s_tmp64[CX_NW];
     __shared__ long long s_tile;
     __shared__ int s_head_nl, s_last_nl, s_nrare, s_err_ord, s_r0, s_r2, s_nfe;
-    __shared__ unsigned s_esc, s_skip, s_flag, s_inl, s_has_ll;
+    __shared__ unsigned s_esc, s_skip, s_flag, s_inl, s_has_ll, s_cr;
     __shared__ unsigned long long s_pre_out, s_pre_lines;
     __shared__ __align__(8) uint64_t s_mbar;  // window bulk copies
     unsigned mbar_phase = 0;
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
             s_nrare = 0;
             s_err_ord = 0x7fffffff;
             s_r0 = s_r2 = 0x7fffffff;
-            s_esc = s_skip = s_flag = s_has_ll = 0;
+            s_esc = s_skip = s_flag = s_has_ll = s_cr = 0;
         }
         __syncthreads();
         const long long t = s_tile;
@@ -633,9 +633,10 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
             win_end = tile_end + 1;
             if (tid == 0) S.win[tile_end] = '\n';
         }
-        // ---- P1: newline bitmap of [0, win_end) ----
+        // ---- P1: newline bitmap of [0, win_end); without renumbering also
+        // whether the window holds a '\r' (none: P2 has nothing to find) ----
         for (int wd = tid; wd < CX_WORDS; wd += CX_NT) {
-            unsigned m = 0;
+            unsigned m = 0, cr = 0;
             const int b0 = wd * 32;
             if (b0 < win_end) {
                 const unsigned *w4 = reinterpret_cast<const unsigned *>(S.win + b0);
@@ -645,10 +646,18 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
                     const unsigned z = ~(((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x | 0x7f7f7f7fu);
                     const unsigned nib = ((z >> 7) & 1u) | ((z >> 14) & 2u) | ((z >> 21) & 4u) | ((z >> 28) & 8u);
                     m |= nib << (4 * k);
+                    if (!job.preprocess) {
+                        const unsigned y = w4[k] ^ 0x0d0d0d0du;
+                        unsigned zc = ~(((y & 0x7f7f7f7fu) + 0x7f7f7f7fu) | y | 0x7f7f7f7fu);
+                        if (b0 + 4 * k + 4 > win_end)  // bytes past the window end are not data
+                            zc &= b0 + 4 * k >= win_end ? 0u : 0xffffffffu >> (8 * (b0 + 4 * k + 4 - win_end));
+                        cr |= zc;
+                    }
                 }
                 if (b0 + 32 > win_end) m &= (1u << (win_end - b0)) - 1u;
             }
             S.rbits[wd] = m;
+            if (cr) s_cr = 1;
         }
         __syncthreads();
         const int c0 = CX_HEAD + tid * CX_CC;
@@ -929,7 +938,11 @@ __global__ void __launch_bounds__(CX_NT, (cx_ctas<PA, SL>())) compress_cx(Job jo
                     rmask = 0;
                 }
             }
-            if (regular && first <= end) {
+            if (regular && first <= end && !job.preprocess && !s_cr) {
+                // without renumbering the tokenizer only looks for '\r' (line
+                // ends flag no errors), and the window has none: count lines
+                nlines += cx_popc_range(S.rbits, first, end);
+            } else if (regular && first <= end) {
                 walk_fast_range(first, end);
                 if (flags & 0x70u) {  // a CR or a tokenize error in the range (rare)
                     nlines = glob ? 1 : 0;
