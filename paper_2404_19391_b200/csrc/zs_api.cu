@@ -35,6 +35,10 @@ namespace {
 struct DevBuf {
     void *p = nullptr;
     size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { release(); }  // (zs_ctx_destroy sets the device first)
     cudaError_t reserve(size_t n) {
         if (n <= cap) return cudaSuccess;
         if (p) cudaFree(p);
@@ -1165,8 +1169,21 @@ int collect(zs_ctx *ctx, int slot, long long n, const uint8_t *h_last_byte_src, 
     return (c.overflow & 1ull) ? 2 : ZS_OK;
 }
 
-int run_device(zs_ctx *ctx, bool compress, const uint8_t *d_in, int64_t n, uint8_t *d_out,
-               int64_t out_cap, int flags, zs_result *res) {
+// The long-line buffers are sized for the worst case of the lines' bytes; a
+// call that needed more than 1 GB of them gives it back.
+void ll_trim(zs_ctx *ctx) {
+    for (int s = 0; s < zs_ctx::NSLOT; ++s) {
+        size_t tot = 0;
+        for (DevBuf *b : {&ctx->llb[s], &ctx->lle[s], &ctx->llc[s], &ctx->llr[s], &ctx->lld[s], &ctx->llo[s]})
+            tot += b->cap;
+        if (tot > (1ull << 30))
+            for (DevBuf *b : {&ctx->llb[s], &ctx->lle[s], &ctx->llc[s], &ctx->llr[s], &ctx->lld[s], &ctx->llo[s]})
+                b->release();
+    }
+}
+
+int run_device_(zs_ctx *ctx, bool compress, const uint8_t *d_in, int64_t n, uint8_t *d_out,
+                int64_t out_cap, int flags, zs_result *res) {
     if (!ctx || !res || n < 0 || (n > 0 && !d_in)) return ZS_E_ARG;
     if (!ctx->have_dict) return ZS_E_NODICT;
     CK(cudaSetDevice(ctx->dev));
@@ -1202,6 +1219,13 @@ int run_device(zs_ctx *ctx, bool compress, const uint8_t *d_in, int64_t n, uint8
     return ZS_E_NOMEM;
 }
 
+int run_device(zs_ctx *ctx, bool compress, const uint8_t *d_in, int64_t n, uint8_t *d_out,
+               int64_t out_cap, int flags, zs_result *res) {
+    const int rc = run_device_(ctx, compress, d_in, n, d_out, out_cap, flags, res);
+    if (ctx) ll_trim(ctx);
+    return rc;
+}
+
 // Host-buffer chunk boundaries, each just past a newline.  Sizes ramp up
 // from ch/16 (the first D2H / kernel starts after a short H2D) to ch and back
 // down over the last ~ch bytes (a short tail of kernel + D2H after the last
@@ -1227,8 +1251,21 @@ std::vector<long long> chunk_cuts(const uint8_t *h_in, long long n, long long ch
 
 // Host-buffer pipeline: newline-aligned chunks, NSLOT slots on NSLOT streams so
 // chunk k+1's H2D and kernel overlap chunk k's D2H.
+int run_host_(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t *h_out,
+              int64_t out_cap, int flags, zs_result *res);
+
 int run_host(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t *h_out,
              int64_t out_cap, int flags, zs_result *res) {
+    const int rc = run_host_(ctx, compress, h_in, n, h_out, out_cap, flags, res);
+    if (ctx) {
+        for (int s = 0; s < zs_ctx::NSLOT; ++s) cudaStreamSynchronize(ctx->stream[s]);  // (error paths return early)
+        ll_trim(ctx);
+    }
+    return rc;
+}
+
+int run_host_(zs_ctx *ctx, bool compress, const uint8_t *h_in, int64_t n, uint8_t *h_out,
+              int64_t out_cap, int flags, zs_result *res) {
     if (!ctx || !res || n < 0 || (n > 0 && !h_in)) return ZS_E_ARG;
     if (!ctx->have_dict) return ZS_E_NODICT;
     CK(cudaSetDevice(ctx->dev));
