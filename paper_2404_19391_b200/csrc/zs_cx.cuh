@@ -326,7 +326,7 @@ __device__ __forceinline__ unsigned cx_emit_range(const Job &job, const CxSmem &
     unsigned esc = 0;
     const uint8_t *__restrict__ win = S.win;
     const uint8_t *__restrict__ explen = S.explen;
-    if (STAGED) {
+    if constexpr (STAGED) {
         // explicit 32-bit shared addresses: with generic pointers the compiler
         // rebuilds the shared window base (S2R SR_CgaCtaId, LEA) every code
         const unsigned wb = (unsigned)__cvta_generic_to_shared(win), eb = (unsigned)__cvta_generic_to_shared(explen);
@@ -366,35 +366,36 @@ __device__ __forceinline__ unsigned cx_emit_range(const Job &job, const CxSmem &
             }
         }
         return esc;
-    }
-    for (int p = p0; p <= p1;) {
-        const unsigned c = win[p];
-        if (c == 0x20) {
-            if (cx_bit(S.fbits, p)) {
-                for (int r = 0; r < n_rare; ++r)  // an arena line's marker?
-                    if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p) {
-                        if (S.rare[r].ll >= 0) {  // long line: its bytes are placed by ll_place
-                            LLine &L = job.ll[S.rare[r].ll];
-                            L.dst = (long long)w;
-                            w += (unsigned long long)S.rare[r].out;
-                            esc += (unsigned)L.esc;
-                        } else {
-                            esc += cx_emit_arena(job, S.explen, S.rare[r].aoff, o, w, S.rare[r].gs);
+    } else {
+        for (int p = p0; p <= p1;) {
+            const unsigned c = win[p];
+            if (c == 0x20) {
+                if (cx_bit(S.fbits, p)) {
+                    for (int r = 0; r < n_rare; ++r)  // an arena line's marker?
+                        if (S.rare[r].kind == RK_ARENA && (S.rare[r].glob ? S.rare[r].le : S.rare[r].ls) == p) {
+                            if (S.rare[r].ll >= 0) {  // long line: its bytes are placed by ll_place
+                                LLine &L = job.ll[S.rare[r].ll];
+                                L.dst = (long long)w;
+                                w += (unsigned long long)S.rare[r].out;
+                                esc += (unsigned)L.esc;
+                            } else {
+                                esc += cx_emit_arena(job, S.explen, S.rare[r].aoff, o, w, S.rare[r].gs);
+                            }
                         }
-                    }
+                } else {
+                    o[w] = 0x20;
+                    o[w + 1] = job.in[ws + p];
+                    w += 2;
+                    ++esc;
+                }
+                ++p;
             } else {
-                o[w] = 0x20;
-                o[w + 1] = job.in[ws + p];
-                w += 2;
-                ++esc;
+                o[w++] = (uint8_t)c;
+                p += explen[c];
             }
-            ++p;
-        } else {
-            o[w++] = (uint8_t)c;
-            p += explen[c];
         }
+        return esc;
     }
-    return esc;
 }
 
 // ---- asynchronous bulk copies (TMA engine) into shared memory ----

@@ -449,6 +449,9 @@ constexpr int LL_NCOL = 100;
 constexpr int LL_CS = 112;
 enum : int { LLC_N = 100, LLC_U = 100, LLC_HEAD = 101, LLC_T = 102, LLC_UU = 106, LLC_AN = 107 };
 
+// (lm[k] is read only for k < nc, every such entry written first; nvcc cannot
+// see that through the lambdas)
+#pragma nv_diag_suppress 549
 __global__ void __launch_bounds__(LL_NT) ll_colour(LLWork W, int n_bound, int pass, int *exits, int *assumed) {
     const int sg = blockIdx.x * LL_NT + threadIdx.x;
     const int a = sg * LL_SEG;
@@ -594,6 +597,8 @@ __global__ void __launch_bounds__(LL_NT) ll_colour(LLWork W, int n_bound, int pa
     ex[LLC_N] = max(nc, en);
     if (pass > 0 && diff) *W.changed = 1;
 }
+
+#pragma nv_diag_default 549
 
 // U of every segment: the minimum u of the segments after it (unsegmented:
 // a later line's u lies past every event of this line, which then all
