@@ -277,11 +277,22 @@ def run_reference(args, ws, rank):
                                            f"run_stream compress (preprocess, lenient) + decompress, "
                                            f"workers={workers}, backend={backend}, {cpu_model()}"},
                 "e2e": {"value": round(v, 4), "unit": "MB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    out["cpu_baseline"]["single_worker"] = single_worker_sample()
     try:
         out["port_baseline"] = port_sample(400_000)
     except Exception as e:  # the port is context, not the arm
         out["port_baseline"] = {"unavailable": str(e)}
     print(json.dumps(out), flush=True)
+
+
+def single_worker_sample(lines=5000):
+    """The reference's run_stream with workers=1 (beside the all-threads arm)."""
+    r = reference_sample(lines, 2, 1, 1)
+    if r is None:
+        return None
+    v, dt, nbytes, backend = r
+    return {"value": round(v, 4), "unit": "MB/s", "cores": 1,
+            "sample": f"first {lines} lines of C2 ({nbytes} B), workers=1, backend={backend}, x2"}
 
 
 def cpu_baseline_block():
@@ -298,6 +309,7 @@ def cpu_baseline_block():
             "sample": f"first 20000 lines of C2 ({nbytes} B): zsmiles run_stream compress (preprocess, "
                       f"lenient) + decompress, workers={threads}, backend={backend}, x3 after a warm-up; "
                       f"{cpu_model()}",
+            "single_worker": single_worker_sample(),
             "port_baseline": port}
 
 
