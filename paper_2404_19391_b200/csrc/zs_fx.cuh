@@ -119,12 +119,12 @@ __device__ __forceinline__ unsigned fx_escaped(const uint8_t *in, long long p) {
 }
 
 // load the 32-byte slice at c0 (cnt valid bytes; the rest read as 0)
-template <bool ALIGNED>
+template <bool ALIGNED, bool KEEP = false>
 __device__ __forceinline__ void fx_load(const uint8_t *in, long long c0, int cnt, uint4 &va, uint4 &vb) {
     if (ALIGNED && cnt == FX_B) {
         const uint4 *src = reinterpret_cast<const uint4 *>(in + c0);
-        va = __ldcs(src);
-        vb = __ldcs(src + 1);
+        va = KEEP ? __ldg(src) : __ldcs(src);
+        vb = KEEP ? __ldg(src + 1) : __ldcs(src + 1);
     } else {
         unsigned w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(FX_NT) fx_count(Job job, const unsigned *ctab,
         const long long c0 = t * (long long)FX_TILE + (long long)tid * FX_B;
         const int cnt = (int)max(0ll, min((long long)FX_B, job.n - c0));
         uint4 va, vb;
-        fx_load<ALIGNED>(job.in, c0, cnt, va, vb);
+        fx_load<ALIGNED, true>(job.in, c0, cnt, va, vb);  // cached: fx_emit reads it again
         const unsigned acc = cnt == FX_B ? fx_count_slice<true>(s_tab, lane, va, vb, cnt)
                                          : fx_count_slice<false>(s_tab, lane, va, vb, cnt);
         unsigned sum = acc & 0x3ffu, bad = (acc >> 10) & 0x3fu, marks = (acc >> 16) & 0x3fu;
@@ -380,19 +380,20 @@ __global__ void __launch_bounds__(FX_NT) fx_emit(Job job, const unsigned long lo
     const unsigned a_stage = sa(stage);
     const bool ends_nl = job.n > 0 && job.in[job.n - 1] == '\n';
 
-    long long t = blockIdx.x;
+    // tiles from the end: the input fx_count read last is the one still in L2
+    long long t = job.n_tiles - 1 - blockIdx.x;
     uint4 na = make_uint4(0, 0, 0, 0), nb4 = na;
-    if (t < job.n_tiles) {
+    if (t >= 0) {
         const long long c0 = t * (long long)FX_TILE + (long long)tid * FX_B;
         fx_load<ALIGNED>(job.in, c0, (int)max(0ll, min((long long)FX_B, job.n - c0)), na, nb4);
     }
-    for (; t < job.n_tiles; t += gridDim.x) {
+    for (; t >= 0; t -= gridDim.x) {
         const long long c0 = t * (long long)FX_TILE + (long long)tid * FX_B;
         const int cnt = (int)max(0ll, min((long long)FX_B, job.n - c0));
         const uint4 va = na, vb = nb4;
         // prefetch the next tile's slice
-        const long long tn = t + gridDim.x;
-        if (tn < job.n_tiles) {
+        const long long tn = t - gridDim.x;
+        if (tn >= 0) {
             const long long cn = tn * (long long)FX_TILE + (long long)tid * FX_B;
             fx_load<ALIGNED>(job.in, cn, (int)max(0ll, min((long long)FX_B, job.n - cn)), na, nb4);
         }
