@@ -200,3 +200,22 @@ def test_long_line_caps_fall_back():
         ctx.check(rc, "zs_compress_device")
     assert r.lines == 33000 and r.lines == st["lines"]
     assert dout[:r.out_bytes].cpu().numpy().tobytes() == want
+
+
+def test_long_lines_through_run_stream_segments():
+    """run_stream with segments much shorter than the long lines (the staging
+    grows to hold a line) gives the oracle's stream and stats."""
+    import io
+    d = z.default_dictionary()
+    rng = random.Random(12)
+    mols = synth.generate("mixed", 20000, 7).tobytes().split(b"\n")[:-1]
+    payload = b"".join(_long(mols, rng.choice((3000, 40000, 150000)), rng) + b"\n" + b"\n".join(mols[:50]) + b"\n"
+                       for _ in range(6))
+    t = oracle.Tables(d.learned, bytes(sorted(d.identity)))
+    for pre in (False, True):
+        want, st = oracle.run_stream(t, payload, "compress", pre, True, 1)
+        dst = io.BytesIO()
+        res = z.run_stream(io.BytesIO(payload), dst, d, "compress", preprocess=pre, lenient=True,
+                           segment_bytes=8192)
+        assert dst.getvalue() == want
+        assert (res.lines, res.escapes) == (st["lines"], st["escapes"])
