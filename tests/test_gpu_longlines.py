@@ -219,3 +219,22 @@ def test_long_lines_through_run_stream_segments():
                            segment_bytes=8192)
         assert dst.getvalue() == want
         assert (res.lines, res.escapes) == (st["lines"], st["escapes"])
+
+
+def test_long_lines_in_later_host_chunks():
+    """A buffer of several 64 MB host-API chunks with long lines in the later
+    ones: the chunk pipeline re-runs just those chunks with the long-line
+    kernels (their slots' own buffers), output bit-exact."""
+    d = z.default_dictionary()
+    rng = random.Random(13)
+    mols = synth.generate("mixed", 20000, 7).tobytes().split(b"\n")[:-1]
+    base = synth.generate("aromatic", 1_600_000, 2024).tobytes()  # ~74 MB
+    lines = base.split(b"\n")[:-1]
+    for at in (1_000_000, 1_300_000, 1_599_000):
+        lines[at] = _long(mols, rng.choice((9000, 60000, 400000)), rng)
+    payload = b"\n".join(lines) + b"\n"
+    t = oracle.Tables(d.learned, bytes(sorted(d.identity)))
+    want, st = oracle.run_stream(t, payload, "compress", True, True, 16)
+    got, res = z.run_buffer(np.frombuffer(payload, np.uint8), d, "compress", preprocess=True, lenient=True)
+    assert got.tobytes() == want
+    assert (res.lines, res.escapes) == (st["lines"], st["escapes"])
